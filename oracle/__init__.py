@@ -1,0 +1,165 @@
+"""CPU ORACLE for Cleora's hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2102_02302_b200``) never imports it and shares no code with it.
+
+The arithmetic lives in ``cleora_oracle.c`` (plain C + OpenMP over rows, fp64
+accumulation, fp32 storage per iteration); this module only marshals arrays.
+What each function computes, with the paper passage it follows
+(PAPER.md = arXiv 2102.02302):
+
+* :func:`build_csr` -- M = D^-1 A, ``M_ab = e_ab / deg(v_a)`` (PAPER.md:79-81,
+  §3.2 "Embedding"; Algorithm 1 line 3), readings B1-B4.
+* :func:`hash_init` -- ``T_0 ~ U(-1,1)`` (Alg. 1 line 4 PAPER.md:92)
+  realised as the id-keyed hash of reading I1.  **Exact values: parity unpinned by
+  the paper** (the paper fixes only the distribution, which the tests pin).
+* :func:`step` -- one ``T_i = M T_{i-1}`` followed by row L2 normalisation
+  (Alg. 1 lines 6-7).
+* :func:`embed` -- Algorithm 1 with Q = 1 chunk.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "cleora_oracle.c")
+_LIB = os.path.join(_HERE, "libcleora_oracle.so")
+_lib = None
+
+OK, EUSAGE, EDATA, ENOMEM = 0, 2, 3, 4
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"oracle {what} failed with code {code}")
+        self.code = code
+
+
+def build_lib(force: bool = False) -> str:
+    """Compile the oracle (gcc -O2 -fopenmp; no -ffast-math: IEEE semantics matter)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                               "-fno-fast-math", "-ffp-contract=off",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        build_lib()
+        lib = ctypes.CDLL(_LIB)
+        vp = ctypes.c_void_p
+        i32p, i64p = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64)
+        f32p, f64p = ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double)
+        lib.oracle_build.restype = ctypes.c_int
+        lib.oracle_build.argtypes = [i32p, i32p, f32p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.POINTER(vp)]
+        lib.oracle_csr_free.argtypes = [vp]
+        lib.oracle_csr_nnz.restype = ctypes.c_int64
+        lib.oracle_csr_nnz.argtypes = [vp]
+        lib.oracle_csr_n.restype = ctypes.c_int32
+        lib.oracle_csr_n.argtypes = [vp]
+        lib.oracle_csr_copy.argtypes = [vp, i64p, i32p, f32p, f64p, f64p]
+        lib.oracle_hash_value.restype = ctypes.c_float
+        lib.oracle_hash_value.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64]
+        lib.oracle_hash_init.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, f32p]
+        lib.oracle_step_rows.argtypes = [vp, ctypes.c_int32, f32p, f32p, ctypes.c_int64, ctypes.c_int64]
+        lib.oracle_embed.argtypes = [vp, ctypes.c_int32, ctypes.c_uint64, ctypes.c_int32, f32p, f32p]
+        lib.oracle_num_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(ctypes.POINTER(t))
+
+
+@dataclass
+class Csr:
+    """The oracle's M in CSR (original node labelling).  ``e`` is e_ab in fp64."""
+    n: int
+    nnz: int
+    row_ptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+    e: np.ndarray
+    deg: np.ndarray
+    _h: ctypes.c_void_p = None
+
+    def __del__(self):
+        if self._h is not None and _lib is not None:
+            _lib.oracle_csr_free(self._h)
+            self._h = None
+
+
+def build_csr(src, dst, w, n: int, directed: bool) -> Csr:
+    """M = D^-1 A per readings B1-B4.  Raises OracleError(EDATA) on bad input."""
+    src = np.ascontiguousarray(src, np.int32)
+    dst = np.ascontiguousarray(dst, np.int32)
+    if w is not None:
+        w = np.ascontiguousarray(w, np.float32)
+    h = ctypes.c_void_p()
+    rc = _L().oracle_build(_p(src, ctypes.c_int32), _p(dst, ctypes.c_int32), _p(w, ctypes.c_float),
+                           int(src.shape[0]), int(n), int(bool(directed)), ctypes.byref(h))
+    if rc != OK:
+        raise OracleError(rc, "build")
+    nnz = int(_lib.oracle_csr_nnz(h))
+    rp = np.empty(n + 1, np.int64); col = np.empty(nnz, np.int32); val = np.empty(nnz, np.float32)
+    e = np.empty(nnz, np.float64); deg = np.empty(n, np.float64)
+    _lib.oracle_csr_copy(h, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), _p(val, ctypes.c_float),
+                         _p(e, ctypes.c_double), _p(deg, ctypes.c_double))
+    return Csr(n, nnz, rp, col, val, e, deg, h)
+
+
+def build_from(g) -> Csr:
+    """build_csr for a ``gen.EdgeList``."""
+    return build_csr(g.src, g.dst, g.w, g.n, g.directed)
+
+
+def hash_value(seed: int, v: int, j: int) -> float:
+    return float(_L().oracle_hash_value(seed, v, j))
+
+
+def hash_init(n: int, d: int, seed: int, row_begin: int = 0) -> np.ndarray:
+    """T_0 rows [row_begin, row_begin+n) (reading I1)."""
+    out = np.empty((n, d), np.float32)
+    _L().oracle_hash_init(seed, row_begin, row_begin + n, d, _p(out, ctypes.c_float))
+    return out
+
+
+def step(M: Csr, T_in: np.ndarray, r0: int = 0, r1: int | None = None) -> np.ndarray:
+    """Rows [r0, r1) of normalize_rows(M . T_in) (Alg. 1 lines 6-7)."""
+    r1 = M.n if r1 is None else r1
+    T_in = np.ascontiguousarray(T_in, np.float32)
+    assert T_in.shape[0] == M.n
+    d = T_in.shape[1]
+    out = np.empty((r1 - r0, d), np.float32)
+    _L().oracle_step_rows(M._h, d, _p(T_in, ctypes.c_float), _p(out, ctypes.c_float), r0, r1)
+    return out
+
+
+def embed(M: Csr, d: int, seed: int, iters: int, keep_all: bool = False):
+    """Algorithm 1 with Q = 1: T_iters (or the list [T_0 .. T_iters] when keep_all)."""
+    T = hash_init(M.n, d, seed)
+    if keep_all:
+        out = [T]
+        for _ in range(iters):
+            T = step(M, T)
+            out.append(T)
+        return out
+    for _ in range(iters):
+        T = step(M, T)
+    return T
+
+
+def num_threads() -> int:
+    return int(_L().oracle_num_threads())
