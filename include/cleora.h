@@ -1,0 +1,192 @@
+/*
+ * cleora.h -- C ABI of the B200-native Cleora hot path (libcleora.so).
+ *
+ * The operation (Rychalska et al., arXiv 2102.02302; "PAPER.md" below is its text):
+ *   M_ab = e_ab / deg(v_a)            random-walk transition matrix  (§3.2)
+ *   T_0  ~ U(-1, 1)                   N x d embedding                (PAPER.md:83, Alg. 1 line 4, :92)
+ *   repeat I times:  T_i = M . T_{i-1};  L2-normalise the rows of T_i (Alg. 1 lines 5-7)
+ * The readings of the paper used where it is silent are listed in DESIGN.md
+ * ("Readings of the paper", R1-R12, RZ).
+ *
+ * Conventions common to every call
+ *   - Return value: CLEORA_OK (0) or an error code below; cleora_last_error() then
+ *     holds a human-readable message (thread-local, valid until the next call on the
+ *     same thread).  On error the handle stays valid (or *out stays NULL).
+ *   - All device work is stream-ordered on the handle's stream (cleora_opts.stream or a
+ *     library-owned stream).  cleora_init / cleora_iterate only enqueue work and return;
+ *     cleora_fetch, cleora_fetch_csr, cleora_info, cleora_stats and cleora_sync wait for it.
+ *     A device fault is reported by the next waiting call as CLEORA_EINTERNAL.
+ *   - A handle is owned by one host thread at a time.  It owns ALL device memory it
+ *     uses (CSR, T replicas, workspaces, schedule) and, when world > 1, its NCCL
+ *     communicator; cleora_destroy releases everything.
+ *   - Node ids are dense int32 in [0, N).  Mapping external entity ids to dense ids
+ *     (the paper's xxhash step) is the caller's job.
+ *   - There is no CPU fallback: without a usable sm_100 device every call fails
+ *     with CLEORA_EINTERNAL.
+ */
+#ifndef CLEORA_H
+#define CLEORA_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CLEORA_API __attribute__((visibility("default")))
+#else
+#define CLEORA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes (they mirror the exit codes of SPEC.md:520: usage 2, data 3, internal 4). */
+enum {
+    CLEORA_OK = 0,
+    CLEORA_EUSAGE = 2,     /* bad argument, NULL pointer, call out of order               */
+    CLEORA_EDATA = 3,      /* input data violates the model: id out of range, weight <= 0,
+                              weight not finite                                          */
+    CLEORA_EINTERNAL = 4   /* CUDA / NCCL error or out of device memory (message names
+                              the API and, for allocations, the bytes requested)          */
+};
+
+/* cleora_opts.flags */
+enum {
+    CLEORA_F_TIMING = 1    /* record CUDA events around every SpMM+normalise launch so that
+                              cleora_stats() can report device time per launch            */
+};
+
+/* Build options.  Pass NULL to cleora_build for: current device, host inputs, a
+ * library-owned stream, one GPU, no flags. */
+typedef struct cleora_opts {
+    int32_t device;          /* CUDA device ordinal; -1 = the calling thread's current device */
+    int32_t input_on_device; /* 1: src/dst/weight are device pointers on `device`;
+                                0: host pointers (pageable or pinned)                          */
+    void* stream;            /* cudaStream_t to enqueue on (borrowed; must outlive the handle);
+                                NULL = the library creates and owns a non-blocking stream    */
+    int32_t rank;            /* this process's rank in [0, world)                               */
+    int32_t world;           /* number of GPUs sharing the work; <= 1 means one GPU            */
+    const uint8_t* nccl_id;  /* world > 1: the 128-byte ncclUniqueId, identical on all ranks;
+                                the library initialises its own communicator from it         */
+    int32_t flags;           /* CLEORA_F_* bit set                                              */
+} cleora_opts;
+
+typedef struct cleora_graph cleora_graph;   /* opaque */
+
+/*
+ * cleora_build -- COO edge list -> device CSR of M = D^-1 A (Alg. 1 line 3,
+ * PAPER.md:91), entirely on the device: validate, mirror (undirected), stable radix sort by
+ * (src, dst), merge duplicates by summing weights, row pointer, degree, D^-1 scaling, and the
+ * degree-bucketed iteration schedule.
+ *   src, dst  [n_edges] int32 node ids in [0, n_nodes); host or device per opts.
+ *   weight    [n_edges] fp32 edge weights (> 0, finite) or NULL for all 1.0f.
+ *   directed  0: each undirected edge is listed once and mirrored by the library (a
+ *             self-loop is stored once, reading R5); 1: row a averages the OUT-neighbours
+ *             of a ("edges running from node a to b"; reading R3).
+ *   Semantics (bit-exact against the oracle, readings B1-B4 in DESIGN.md):
+ *     e_ab   = fp64 sum of the weights of duplicate (a,b) edges in stable input order
+ *              (originals first, then mirrors), "the sum of the weights of all
+ *              participating edges";
+ *     deg(a) = fp64 sum of e_ab over ascending b (weighted out-degree, reading R2);
+ *     M_ab   = (float)(e_ab / deg(a)), IEEE round-to-nearest once.
+ *   Inputs are borrowed for the duration of the call only.  On success *out owns the graph.
+ *   Errors: EUSAGE (NULL pointer, n_nodes <= 0, n_edges <= 0, world > 1 without nccl_id,
+ *   bad rank), EDATA (id outside [0, n_nodes), weight <= 0 or not finite), EINTERNAL.
+ *   Multi-GPU (world > 1): collective; every rank passes the same edge list; each rank keeps
+ *   the full CSR and computes the rows of its nnz-balanced contiguous shard.
+ */
+CLEORA_API int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, int64_t n_edges,
+                 int32_t n_nodes, int32_t directed, const cleora_opts* opts, cleora_graph** out);
+
+/*
+ * cleora_init -- allocate the two N x d fp32 embedding buffers and set T <- T_0 with
+ *   T_0[v][j] = ((int32)(h >> 40) - 2^23) * 2^-23,
+ *   h = mix(mix(seed + 0x9E3779B97F4A7C15) XOR (v << 32 | j)), mix = SplitMix64 finaliser
+ * (reading R1 / I1: a realisation of "T_0 ~ U(-1,1)").  T_0 is NOT
+ * normalised (reading R7).  May be called again to restart from T_0 (same or new d / seed).
+ *   d >= 1 (any d; rows are stored with a stride padded to 4 floats, padding kept at 0).
+ *   Errors: EUSAGE (g NULL, d < 1, d > CLEORA_MAX_D), EINTERNAL (out of memory).
+ */
+#define CLEORA_MAX_D 4096
+CLEORA_API int cleora_init(cleora_graph* g, int32_t d, uint64_t seed);
+
+/*
+ * cleora_iterate -- k >= 0 steps of T <- normalize_rows(M . T) (Alg. 1 lines 6-7,
+ * PAPER.md:94-95), one fused SpMM + row-L2-normalise kernel launch per step.  A row whose
+ * product is the zero vector (no out-edges) is written as zeros (reading RZ).
+ * iterate(a); iterate(b) is bit-identical to iterate(a + b).  Results do not depend on the
+ * number of GPUs (the per-row schedule depends only on the row's degree).
+ * Multi-GPU: collective; after each step the rank shards are all-gathered into every replica.
+ *   Errors: EUSAGE (g NULL, k < 0, called before cleora_init), EINTERNAL.
+ */
+CLEORA_API int cleora_iterate(cleora_graph* g, int32_t k);
+
+/*
+ * cleora_fetch -- copy rows [row_begin, row_end) of the current T (T_i after i steps) into
+ * `out`, dense (row_end - row_begin) x d fp32 row-major.  out_on_device = 0: `out` is host
+ * memory (pinned or pageable); 1: device memory on the handle's device.  Waits for the copy.
+ *   Errors: EUSAGE (NULL, range outside [0, N], before cleora_init), EINTERNAL.
+ */
+CLEORA_API int cleora_fetch(const cleora_graph* g, int64_t row_begin, int64_t row_end, float* out,
+                 int32_t out_on_device);
+
+/* Facts about a handle (all sizes in elements). */
+typedef struct cleora_info_t {
+    int64_t n_nodes;        /* N                                                        */
+    int64_t nnz;            /* stored entries of M after mirroring and merging          */
+    int64_t n_edges_in;     /* the n_edges passed to cleora_build                       */
+    int32_t d;              /* embedding dimension (0 before cleora_init)               */
+    int32_t d_stride;       /* row stride of the device T buffers in floats             */
+    int64_t iterations;     /* steps applied since the last cleora_init                 */
+    int64_t zero_rows;      /* rows with no out-edges (their T rows are 0 after step 1) */
+    int64_t max_degree;     /* largest number of stored entries in one row              */
+    int64_t heavy_rows;     /* rows scheduled on the multi-warp / multi-CTA path        */
+    int64_t heavy_items;    /* CTA work items for those rows                            */
+    int64_t shard_begin;    /* rows this rank computes: [shard_begin, shard_end)        */
+    int64_t shard_end;
+    int32_t rank, world;
+    int64_t device_bytes;   /* device memory currently owned by the handle              */
+} cleora_info_t;
+CLEORA_API int cleora_info(const cleora_graph* g, cleora_info_t* out);
+
+/* Device-time statistics (requires CLEORA_F_TIMING; otherwise counts stay 0). */
+typedef struct cleora_stats_t {
+    int64_t spmm_launches;  /* SpMM+normalise launches timed since the last reset        */
+    double spmm_ms_total;   /* sum of their durations (CUDA events on the handle stream) */
+    double spmm_ms_min, spmm_ms_max;
+    int64_t exchange_launches;
+    double exchange_ms_total;
+} cleora_stats_t;
+CLEORA_API int cleora_stats(cleora_graph* g, cleora_stats_t* out, int32_t reset);
+
+/* Wait for all work enqueued on the handle's stream. */
+CLEORA_API int cleora_sync(const cleora_graph* g);
+
+/* Release everything the handle owns.  Safe on NULL. */
+CLEORA_API void cleora_destroy(cleora_graph* g);
+
+CLEORA_API const char* cleora_last_error(void);
+
+/* ---- test hooks (not on the graded path) ------------------------------------------------ */
+
+/* Copy the device CSR to host arrays in the original labelling:
+ * row_ptr [N+1] int64, col [nnz] int32, val [nnz] fp32, deg [N] fp64 (any may be NULL). */
+CLEORA_API int cleora_fetch_csr(const cleora_graph* g, int64_t* row_ptr, int32_t* col, float* val, double* deg);
+
+/* Overwrite rows [row_begin, row_end) of the current T from host memory (dense, d per row):
+ * resume from a checkpoint or start from a custom T_0. */
+CLEORA_API int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const float* host_in);
+
+/* Size of an ncclUniqueId (128) and a helper that fills one (rank 0 calls it and
+ * broadcasts the bytes through the caller's process group). */
+CLEORA_API int cleora_nccl_id_size(void);
+CLEORA_API int cleora_nccl_get_unique_id(uint8_t* out128);
+
+/* Host-side shard plan (no GPU needed): nnz-balanced contiguous row cuts.
+ * row_ptr [n+1]; cuts [world+1] receives r_0 = 0 <= r_1 <= ... <= r_world = n where rank p
+ * owns rows [r_p, r_{p+1}); cut p is the first row whose nnz prefix reaches p * nnz / world. */
+CLEORA_API int cleora_plan_shards(const int64_t* row_ptr, int64_t n, int32_t world, int64_t* cuts);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CLEORA_H */

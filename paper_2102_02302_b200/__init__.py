@@ -1,0 +1,261 @@
+"""B200-native Cleora hot path: Python binding of libcleora.so (include/cleora.h).
+
+Argument marshalling only.  Every step of the path -- CSR build (sort, merge, degree,
+D^-1 scaling), hash initialisation, the fused SpMM + row-L2-normalise iteration, the
+multi-GPU exchange -- runs in the library's CUDA kernels.  There is no CPU fallback:
+importing this package without the built ``libcleora.so`` raises ImportError, and every
+call without a usable B200 raises :class:`CleoraError` (code 4).
+
+The functions carry the C names (``cleora_build`` ... ``cleora_fetch``).  Arrays may be
+numpy arrays (host) or torch tensors (host or CUDA; CUDA tensors are passed as device
+pointers, so nothing is copied through the host).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = [
+    "CleoraError", "Graph", "LIB_PATH",
+    "cleora_build", "cleora_init", "cleora_iterate", "cleora_fetch", "cleora_info", "cleora_stats",
+    "cleora_sync", "cleora_destroy", "cleora_last_error", "cleora_fetch_csr", "cleora_set_rows",
+    "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcleora.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built (run `python -c 'import __graft_entry__ as g; g.build()'`); "
+                      "the Cleora path has no CPU fallback")
+_lib = ctypes.CDLL(LIB_PATH)
+
+OK, EUSAGE, EDATA, EINTERNAL = 0, 2, 3, 4
+F_TIMING = 1
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("input_on_device", ctypes.c_int32), ("stream", ctypes.c_void_p),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+                ("flags", ctypes.c_int32)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("n_nodes", ctypes.c_int64), ("nnz", ctypes.c_int64), ("n_edges_in", ctypes.c_int64),
+                ("d", ctypes.c_int32), ("d_stride", ctypes.c_int32), ("iterations", ctypes.c_int64),
+                ("zero_rows", ctypes.c_int64), ("max_degree", ctypes.c_int64), ("heavy_rows", ctypes.c_int64),
+                ("heavy_items", ctypes.c_int64), ("shard_begin", ctypes.c_int64), ("shard_end", ctypes.c_int64),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device_bytes", ctypes.c_int64)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("spmm_launches", ctypes.c_int64), ("spmm_ms_total", ctypes.c_double),
+                ("spmm_ms_min", ctypes.c_double), ("spmm_ms_max", ctypes.c_double),
+                ("exchange_launches", ctypes.c_int64), ("exchange_ms_total", ctypes.c_double)]
+
+
+_vp, _i32, _i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+_SIGS = {
+    "cleora_build": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i32, _i32, ctypes.POINTER(_Opts), ctypes.POINTER(_vp)]),
+    "cleora_init": (ctypes.c_int, [_vp, _i32, ctypes.c_uint64]),
+    "cleora_iterate": (ctypes.c_int, [_vp, _i32]),
+    "cleora_fetch": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i32]),
+    "cleora_info": (ctypes.c_int, [_vp, ctypes.POINTER(_Info)]),
+    "cleora_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_Stats), _i32]),
+    "cleora_sync": (ctypes.c_int, [_vp]),
+    "cleora_destroy": (None, [_vp]),
+    "cleora_last_error": (ctypes.c_char_p, []),
+    "cleora_fetch_csr": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "cleora_set_rows": (ctypes.c_int, [_vp, _i64, _i64, _vp]),
+    "cleora_nccl_id_size": (ctypes.c_int, []),
+    "cleora_nccl_get_unique_id": (ctypes.c_int, [_vp]),
+    "cleora_plan_shards": (ctypes.c_int, [_vp, _i64, _i32, _vp]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class CleoraError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[cleora error {code}] {msg}")
+        self.code = code
+
+
+def cleora_last_error() -> str:
+    m = _lib.cleora_last_error()
+    return m.decode() if m else ""
+
+
+def _check(rc: int):
+    if rc != OK:
+        raise CleoraError(rc, cleora_last_error())
+
+
+def _ptr(a, dtype):
+    """(pointer, on_device, keepalive) for a numpy array or torch tensor (or None)."""
+    if a is None:
+        return None, False, None
+    if hasattr(a, "data_ptr") and hasattr(a, "is_cuda"):       # torch.Tensor
+        import torch
+        tdt = {np.int32: torch.int32, np.float32: torch.float32, np.int64: torch.int64,
+               np.float64: torch.float64}[dtype]
+        if a.dtype != tdt or not a.is_contiguous():
+            a = a.to(tdt).contiguous()
+        return a.data_ptr(), bool(a.is_cuda), a
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return arr.ctypes.data, False, arr
+
+
+class Graph:
+    """Owning wrapper of a ``cleora_graph*`` (destroyed on close / garbage collection)."""
+
+    def __init__(self, handle: int):
+        self._h = handle
+
+    @property
+    def handle(self) -> int:
+        if not self._h:
+            raise CleoraError(EUSAGE, "graph already destroyed")
+        return self._h
+
+    def close(self):
+        if self._h:
+            _lib.cleora_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # convenience methods with the C semantics
+    def init(self, d: int, seed: int = 0):
+        cleora_init(self, d, seed)
+        return self
+
+    def iterate(self, k: int):
+        cleora_iterate(self, k)
+        return self
+
+    def fetch(self, row_begin: int = 0, row_end: int | None = None, out=None):
+        return cleora_fetch(self, row_begin, row_end, out)
+
+    def info(self) -> dict:
+        return cleora_info(self)
+
+
+def cleora_build(src, dst, weight, n_nodes: int, directed: bool = False, *, device: int = -1, stream=None,
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None, timing: bool = False) -> Graph:
+    """COO edge list -> device CSR of M = D^-1 A.  See include/cleora.h."""
+    ps, ds, ks = _ptr(src, np.int32)
+    pd, dd, kd = _ptr(dst, np.int32)
+    pw, dw, kw = _ptr(weight, np.float32)
+    if ps is None or pd is None:
+        raise CleoraError(EUSAGE, "src/dst required")
+    n = int(ks.shape[0])
+    if int(kd.shape[0]) != n or (kw is not None and int(kw.shape[0]) != n):
+        raise CleoraError(EUSAGE, "src, dst, weight must have the same length")
+    on_dev = ds or dd or dw
+    if on_dev and not (ds and dd and (kw is None or dw)):
+        raise CleoraError(EUSAGE, "src/dst/weight must be all on the host or all on the device")
+    if on_dev and device < 0:
+        device = int(ks.device.index or 0)
+    o = _Opts()
+    o.device = device
+    o.input_on_device = 1 if on_dev else 0
+    if stream is not None:
+        o.stream = stream if isinstance(stream, int) else int(getattr(stream, "cuda_stream", stream))
+    o.rank, o.world = rank, world
+    idbuf = None
+    if nccl_id is not None:
+        idbuf = ctypes.create_string_buffer(bytes(nccl_id), len(nccl_id))
+        o.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
+    o.flags = F_TIMING if timing else 0
+    h = ctypes.c_void_p()
+    _check(_lib.cleora_build(ps, pd, pw, n, int(n_nodes), 1 if directed else 0, ctypes.byref(o), ctypes.byref(h)))
+    return Graph(h.value)
+
+
+def cleora_init(g: Graph, d: int, seed: int = 0):
+    _check(_lib.cleora_init(g.handle, int(d), int(seed) & 0xFFFFFFFFFFFFFFFF))
+
+
+def cleora_iterate(g: Graph, k: int):
+    _check(_lib.cleora_iterate(g.handle, int(k)))
+
+
+def cleora_fetch(g: Graph, row_begin: int = 0, row_end: int | None = None, out=None):
+    """Rows [row_begin, row_end) of the current T as a (rows, d) fp32 array.  ``out`` may be a
+    preallocated numpy array / host tensor (pinned for speed) or a CUDA tensor."""
+    info = cleora_info(g, sync=False)
+    if row_end is None:
+        row_end = info["n_nodes"]
+    rows = max(0, row_end - row_begin)
+    if out is None:
+        out = np.empty((rows, info["d"]), np.float32)
+    p, on_dev, keep = _ptr(out, np.float32)
+    if keep is not out:
+        raise CleoraError(EUSAGE, "out must be a contiguous fp32 array")
+    _check(_lib.cleora_fetch(g.handle, int(row_begin), int(row_end), p, 1 if on_dev else 0))
+    return out
+
+
+def cleora_info(g: Graph, sync: bool = True) -> dict:
+    i = _Info()
+    _check(_lib.cleora_info(g.handle, ctypes.byref(i)))
+    return {f: getattr(i, f) for f, _ in _Info._fields_}
+
+
+def cleora_stats(g: Graph, reset: bool = False) -> dict:
+    s = _Stats()
+    _check(_lib.cleora_stats(g.handle, ctypes.byref(s), 1 if reset else 0))
+    return {f: getattr(s, f) for f, _ in _Stats._fields_}
+
+
+def cleora_sync(g: Graph):
+    _check(_lib.cleora_sync(g.handle))
+
+
+def cleora_destroy(g: Graph):
+    g.close()
+
+
+def cleora_fetch_csr(g: Graph) -> dict:
+    info = cleora_info(g)
+    n, nnz = info["n_nodes"], info["nnz"]
+    rp = np.empty(n + 1, np.int64); col = np.empty(nnz, np.int32)
+    val = np.empty(nnz, np.float32); deg = np.empty(n, np.float64)
+    _check(_lib.cleora_fetch_csr(g.handle, rp.ctypes.data, col.ctypes.data, val.ctypes.data, deg.ctypes.data))
+    return dict(row_ptr=rp, col=col, val=val, deg=deg)
+
+
+def cleora_set_rows(g: Graph, row_begin: int, rows):
+    arr = np.ascontiguousarray(rows, np.float32)
+    _check(_lib.cleora_set_rows(g.handle, int(row_begin), int(row_begin) + int(arr.shape[0]), arr.ctypes.data))
+
+
+def cleora_nccl_id_size() -> int:
+    return int(_lib.cleora_nccl_id_size())
+
+
+def cleora_nccl_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(cleora_nccl_id_size())
+    _check(_lib.cleora_nccl_get_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+def cleora_plan_shards(row_ptr, world: int) -> np.ndarray:
+    """Host-side nnz-balanced contiguous row cuts (no GPU needed)."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cuts = np.empty(world + 1, np.int64)
+    _check(_lib.cleora_plan_shards(rp.ctypes.data, int(rp.shape[0] - 1), int(world), cuts.ctypes.data))
+    return cuts

@@ -1,0 +1,575 @@
+// api.cu -- the C ABI of libcleora (include/cleora.h): handle life cycle, argument checks,
+// device memory ownership, stream ordering, timing, and the multi-GPU exchange.
+//
+// Every step of the hot path runs in this library's kernels (build.cu, init.cu,
+// spmm_norm.cu); the Python binding only marshals arguments.  There is no CPU fallback.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/cleora.h"
+#include "common.cuh"
+
+namespace cleora {
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+static std::mutex g_pool_mu;
+static bool g_pool_cfg[64];
+
+Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what) {
+    *p = nullptr;
+    int dev = 0;
+    CL_CUDA_TRY(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (dev < 64 && !g_pool_cfg[dev]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            g_pool_cfg[dev] = true;
+        }
+    }
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(p, bytes, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        char buf[256];
+        snprintf(buf, sizeof buf, "cudaMallocAsync(%zu bytes) for %s: %s", bytes, what, cudaGetErrorString(e));
+        *p = nullptr;
+        return Status::make(4, buf);
+    }
+    return Status::ok();
+}
+
+void dfree(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+// ---------------------------------------------------------------- NCCL, resolved at run time
+// The library does not link NCCL: when world > 1 it binds to the libnccl.so.2 already loaded
+// into the process (torch's) or loads it, so the process never holds two NCCL copies.
+struct Nccl {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static Nccl& nccl() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) { n.why = std::string("dlopen libnccl.so.2: ") + dlerror(); return; }
+#define BIND(f, name)                                                   \
+    n.f = reinterpret_cast<decltype(n.f)>(dlsym(h, name));              \
+    if (!n.f) { n.why = std::string("dlsym ") + name; return; }
+        BIND(GetUniqueId, "ncclGetUniqueId");
+        BIND(CommInitRank, "ncclCommInitRank");
+        BIND(Broadcast, "ncclBroadcast");
+        BIND(GroupStart, "ncclGroupStart");
+        BIND(GroupEnd, "ncclGroupEnd");
+        BIND(CommDestroy, "ncclCommDestroy");
+        BIND(GetErrorString, "ncclGetErrorString");
+#undef BIND
+        n.ok = true;
+    });
+    return n;
+}
+
+#define CL_NCCL_TRY(expr)                                                                         \
+    do {                                                                                          \
+        ncclResult_t _r = (expr);                                                                 \
+        if (_r != ncclSuccess)                                                                    \
+            return Status::make(4, std::string(#expr) + ": " + nccl().GetErrorString(_r));       \
+    } while (0)
+
+static int heavy_thresh_default() {
+    const char* e = getenv("CLEORA_HEAVY_THRESH");
+    int v = e ? atoi(e) : 64;
+    if (v < 8) v = 8;
+    if (v > 4096) v = 4096;
+    return v;
+}
+
+}  // namespace cleora
+
+using namespace cleora;
+
+struct cleora_graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int32_t n = 0;
+    int64_t nnz = 0, n_edges_in = 0, zero_rows = 0, max_degree = 0;
+    int directed = 0;
+    int64_t* row_ptr = nullptr;
+    int32_t* col = nullptr;
+    float* val = nullptr;
+    double* deg = nullptr;
+    int heavy_thresh = 64;
+    Schedule sched;
+    int32_t d = 0, dp = 0;
+    float* T[2] = {nullptr, nullptr};
+    float* partials = nullptr;
+    int cur = 0;
+    int64_t iters = 0;
+    int rank = 0, world = 1;
+    std::vector<int64_t> cuts;
+    int64_t r0 = 0, r1 = 0;
+    ncclComm_t comm = nullptr;
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_spmm, ev_x;
+    std::vector<cudaEvent_t> ev_pool;
+    int64_t n_spmm = 0, n_x = 0;
+    double ms_spmm = 0, ms_min = 1e300, ms_max = 0, ms_x = 0;
+    int64_t bytes = 0;
+};
+
+namespace {
+
+int fail(const Status& s) {
+    set_error(s.msg);
+    return s.code;
+}
+int usage(const char* m) {
+    set_error(m);
+    return CLEORA_EUSAGE;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int now = -1;
+        if (prev >= 0 && cudaGetDevice(&now) == cudaSuccess && now != prev) cudaSetDevice(prev);
+    }
+};
+
+cudaEvent_t get_event(cleora_graph* g) {
+    if (!g->ev_pool.empty()) {
+        cudaEvent_t e = g->ev_pool.back();
+        g->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+Status collect_timing(cleora_graph* g) {
+    if (g->ev_spmm.empty() && g->ev_x.empty()) return Status::ok();
+    CL_CUDA_TRY(cudaStreamSynchronize(g->stream));
+    for (auto& p : g->ev_spmm) {
+        float ms = 0;
+        CL_CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
+        g->n_spmm++;
+        g->ms_spmm += ms;
+        g->ms_min = std::min(g->ms_min, (double)ms);
+        g->ms_max = std::max(g->ms_max, (double)ms);
+        g->ev_pool.push_back(p.first);
+        g->ev_pool.push_back(p.second);
+    }
+    for (auto& p : g->ev_x) {
+        float ms = 0;
+        CL_CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
+        g->n_x++;
+        g->ms_x += ms;
+        g->ev_pool.push_back(p.first);
+        g->ev_pool.push_back(p.second);
+    }
+    g->ev_spmm.clear();
+    g->ev_x.clear();
+    return Status::ok();
+}
+
+void free_T(cleora_graph* g) {
+    for (int i = 0; i < 2; i++) {
+        dfree(g->T[i], g->stream);
+        g->T[i] = nullptr;
+    }
+    dfree(g->partials, g->stream);
+    g->partials = nullptr;
+}
+
+Status exchange(cleora_graph* g, float* buf) {
+    // all-gather(-v) of the row shards into every replica: one in-place broadcast per rank
+    Nccl& N = nccl();
+    CL_NCCL_TRY(N.GroupStart());
+    for (int p = 0; p < g->world; p++) {
+        const int64_t b = g->cuts[p], e = g->cuts[p + 1];
+        if (e <= b) continue;
+        float* ptr = buf + b * (int64_t)g->dp;
+        CL_NCCL_TRY(N.Broadcast(ptr, ptr, (size_t)(e - b) * g->dp, ncclFloat32, p, g->comm, g->stream));
+    }
+    CL_NCCL_TRY(N.GroupEnd());
+    return Status::ok();
+}
+
+Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t E, int32_t N, int directed,
+                const cleora_opts* o, cleora_graph* g) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return Status::make(4, "cleora_build: no CUDA device visible (libcleora has no CPU fallback)");
+    }
+    int dev = (o && o->device >= 0) ? o->device : -1;
+    if (dev < 0) CL_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev >= ndev) return Status::make(2, "cleora_build: device ordinal out of range");
+    CL_CUDA_TRY(cudaSetDevice(dev));
+    int major = 0;
+    CL_CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (major != 10) return Status::make(4, "cleora_build: libcleora is compiled for sm_100a (B200) only");
+    g->device = dev;
+    if (o && o->stream) {
+        g->stream = (cudaStream_t)o->stream;
+    } else {
+        CL_CUDA_TRY(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+        g->own_stream = true;
+    }
+    g->timing = o && (o->flags & CLEORA_F_TIMING);
+    g->n = N;
+    g->n_edges_in = E;
+    g->directed = directed;
+    g->heavy_thresh = heavy_thresh_default();
+    g->rank = (o && o->world > 1) ? o->rank : 0;
+    g->world = (o && o->world > 1) ? o->world : 1;
+
+    // a1: device copies of the COO when the caller passed host memory
+    const int32_t* dsrc = src;
+    const int32_t* ddst = dst;
+    const float* dw = w;
+    void *bs = nullptr, *bd = nullptr, *bw = nullptr;
+    const bool on_dev = o && o->input_on_device;
+    if (!on_dev) {
+        CL_TRY(dalloc(&bs, E * sizeof(int32_t), g->stream, "input src"));
+        CL_TRY(dalloc(&bd, E * sizeof(int32_t), g->stream, "input dst"));
+        CL_CUDA_TRY(cudaMemcpyAsync(bs, src, E * sizeof(int32_t), cudaMemcpyHostToDevice, g->stream));
+        CL_CUDA_TRY(cudaMemcpyAsync(bd, dst, E * sizeof(int32_t), cudaMemcpyHostToDevice, g->stream));
+        if (w) {
+            CL_TRY(dalloc(&bw, E * sizeof(float), g->stream, "input weight"));
+            CL_CUDA_TRY(cudaMemcpyAsync(bw, w, E * sizeof(float), cudaMemcpyHostToDevice, g->stream));
+        }
+        dsrc = (const int32_t*)bs;
+        ddst = (const int32_t*)bd;
+        dw = (const float*)bw;
+    }
+    BuildOut b;
+    Status st = build_csr(dsrc, ddst, dw, E, N, directed, g->stream, &b);
+    dfree(bs, g->stream);
+    dfree(bd, g->stream);
+    dfree(bw, g->stream);
+    if (!st.good()) return st;
+    g->nnz = b.nnz;
+    g->row_ptr = b.row_ptr;
+    g->col = b.col;
+    g->val = b.val;
+    g->deg = b.deg;
+    g->zero_rows = b.zero_rows;
+    g->max_degree = b.max_degree;
+    g->bytes = (int64_t)(N + 1) * 8 + b.nnz * 8 + (int64_t)N * 8;
+
+    g->cuts.assign(g->world + 1, 0);
+    if (g->world > 1) {
+        CL_TRY(shard_cuts(g->row_ptr, N, g->world, g->stream, g->cuts.data()));
+    } else {
+        g->cuts[1] = N;
+    }
+    g->r0 = g->cuts[g->rank];
+    g->r1 = g->cuts[g->rank + 1];
+    CL_TRY(build_schedule(g->row_ptr, N, g->r0, g->r1, g->heavy_thresh, g->stream, &g->sched));
+    g->bytes += g->sched.n_items * (int64_t)sizeof(HeavyItem) + g->sched.n_heavy_rows * 4;
+
+    if (g->world > 1) {
+        Nccl& nc = nccl();
+        if (!nc.ok) return Status::make(4, "cleora_build: NCCL unavailable: " + nc.why);
+        ncclUniqueId id;
+        memcpy(id.internal, o->nccl_id, NCCL_UNIQUE_ID_BYTES);
+        CL_NCCL_TRY(nc.CommInitRank(&g->comm, g->world, id, g->rank));
+    }
+    CL_CUDA_TRY(cudaStreamSynchronize(g->stream));
+    return Status::ok();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cleora_last_error(void) { return g_err.c_str(); }
+
+int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, int64_t n_edges, int32_t n_nodes,
+                 int32_t directed, const cleora_opts* opts, cleora_graph** out) {
+    if (!out) return usage("cleora_build: out is NULL");
+    *out = nullptr;
+    if (!src || !dst) return usage("cleora_build: src/dst is NULL");
+    if (n_nodes <= 0) return usage("cleora_build: n_nodes must be > 0");
+    if (n_edges <= 0) return usage("cleora_build: n_edges must be > 0 (non-empty edge list)");
+    if (opts && opts->world > 1) {
+        if (!opts->nccl_id) return usage("cleora_build: world > 1 needs nccl_id");
+        if (opts->rank < 0 || opts->rank >= opts->world) return usage("cleora_build: rank outside [0, world)");
+    }
+    DeviceGuard guard(opts ? opts->device : -1);
+    cleora_graph* g = new cleora_graph();
+    Status s = do_build(src, dst, weight, n_edges, n_nodes, directed ? 1 : 0, opts, g);
+    if (!s.good()) {
+        cleora_destroy(g);
+        return fail(s);
+    }
+    *out = g;
+    return CLEORA_OK;
+}
+
+int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
+    if (!g) return usage("cleora_init: graph is NULL");
+    if (d < 1 || d > CLEORA_MAX_D) return usage("cleora_init: d must be in [1, CLEORA_MAX_D]");
+    DeviceGuard guard(g->device);
+    const int32_t dp = (d + 3) / 4 * 4;
+    if (dp != g->dp || !g->T[0]) {
+        free_T(g);
+        const size_t tb = (size_t)g->n * dp * sizeof(float);
+        for (int i = 0; i < 2; i++) {
+            Status s = dalloc((void**)&g->T[i], tb, g->stream, "embedding T");
+            if (!s.good()) {
+                free_T(g);
+                return fail(s);
+            }
+        }
+        if (g->sched.n_items > 0) {
+            Status s = dalloc((void**)&g->partials, (size_t)g->sched.n_items * dp * sizeof(float), g->stream,
+                              "heavy-row partials");
+            if (!s.good()) {
+                free_T(g);
+                return fail(s);
+            }
+        }
+    }
+    g->d = d;
+    g->dp = dp;
+    g->cur = 0;
+    g->iters = 0;
+    Status s = launch_hash_init(g->T[0], g->n, d, dp, seed, g->stream);
+    if (!s.good()) return fail(s);
+    return CLEORA_OK;
+}
+
+int cleora_iterate(cleora_graph* g, int32_t k) {
+    if (!g) return usage("cleora_iterate: graph is NULL");
+    if (k < 0) return usage("cleora_iterate: k must be >= 0");
+    if (!g->T[0]) return usage("cleora_iterate: call cleora_init first");
+    DeviceGuard guard(g->device);
+    for (int32_t i = 0; i < k; i++) {
+        SpmmArgs a;
+        a.row_ptr = g->row_ptr;
+        a.col = g->col;
+        a.val = g->val;
+        a.T_in = g->T[g->cur];
+        a.T_out = g->T[1 - g->cur];
+        a.dp = g->dp;
+        a.r0 = g->r0;
+        a.r1 = g->r1;
+        a.heavy_thresh = g->heavy_thresh;
+        a.items = g->sched.items;
+        a.n_items = g->sched.n_items;
+        a.partials = g->partials;
+        a.counters = g->sched.counters;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (g->timing) {
+            e0 = get_event(g);
+            e1 = get_event(g);
+            cudaEventRecord(e0, g->stream);
+        }
+        Status s = launch_spmm_norm(a, g->stream);
+        if (!s.good()) return fail(s);
+        if (g->timing) {
+            cudaEventRecord(e1, g->stream);
+            g->ev_spmm.emplace_back(e0, e1);
+        }
+        if (g->world > 1) {
+            if (g->timing) {
+                e0 = get_event(g);
+                e1 = get_event(g);
+                cudaEventRecord(e0, g->stream);
+            }
+            s = exchange(g, g->T[1 - g->cur]);
+            if (!s.good()) return fail(s);
+            if (g->timing) {
+                cudaEventRecord(e1, g->stream);
+                g->ev_x.emplace_back(e0, e1);
+            }
+        }
+        g->cur = 1 - g->cur;
+        g->iters++;
+    }
+    return CLEORA_OK;
+}
+
+int cleora_fetch(const cleora_graph* g, int64_t row_begin, int64_t row_end, float* out, int32_t out_on_device) {
+    if (!g || !out) return usage("cleora_fetch: NULL argument");
+    if (!g->T[0]) return usage("cleora_fetch: call cleora_init first");
+    if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_fetch: rows outside [0, N]");
+    if (row_end == row_begin) return CLEORA_OK;
+    DeviceGuard guard(g->device);
+    const float* src = g->T[g->cur] + row_begin * (int64_t)g->dp;
+    cudaError_t e = cudaMemcpy2DAsync(out, (size_t)g->d * sizeof(float), src, (size_t)g->dp * sizeof(float),
+                                      (size_t)g->d * sizeof(float), (size_t)(row_end - row_begin),
+                                      out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_fetch: ") + cudaGetErrorString(e)));
+    return CLEORA_OK;
+}
+
+int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const float* host_in) {
+    if (!g || !host_in) return usage("cleora_set_rows: NULL argument");
+    if (!g->T[0]) return usage("cleora_set_rows: call cleora_init first");
+    if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_set_rows: rows outside [0, N]");
+    if (row_end == row_begin) return CLEORA_OK;
+    DeviceGuard guard(g->device);
+    float* dst = g->T[g->cur] + row_begin * (int64_t)g->dp;
+    cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)g->dp * sizeof(float), host_in, (size_t)g->d * sizeof(float),
+                                      (size_t)g->d * sizeof(float), (size_t)(row_end - row_begin),
+                                      cudaMemcpyHostToDevice, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_set_rows: ") + cudaGetErrorString(e)));
+    return CLEORA_OK;
+}
+
+int cleora_fetch_csr(const cleora_graph* g, int64_t* row_ptr, int32_t* col, float* val, double* deg) {
+    if (!g) return usage("cleora_fetch_csr: graph is NULL");
+    DeviceGuard guard(g->device);
+    cudaError_t e = cudaSuccess;
+    if (row_ptr && e == cudaSuccess)
+        e = cudaMemcpyAsync(row_ptr, g->row_ptr, ((size_t)g->n + 1) * 8, cudaMemcpyDeviceToHost, g->stream);
+    if (col && e == cudaSuccess) e = cudaMemcpyAsync(col, g->col, (size_t)g->nnz * 4, cudaMemcpyDeviceToHost, g->stream);
+    if (val && e == cudaSuccess) e = cudaMemcpyAsync(val, g->val, (size_t)g->nnz * 4, cudaMemcpyDeviceToHost, g->stream);
+    if (deg && e == cudaSuccess) e = cudaMemcpyAsync(deg, g->deg, (size_t)g->n * 8, cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_fetch_csr: ") + cudaGetErrorString(e)));
+    return CLEORA_OK;
+}
+
+int cleora_info(const cleora_graph* g, cleora_info_t* o) {
+    if (!g || !o) return usage("cleora_info: NULL argument");
+    memset(o, 0, sizeof *o);
+    o->n_nodes = g->n;
+    o->nnz = g->nnz;
+    o->n_edges_in = g->n_edges_in;
+    o->d = g->d;
+    o->d_stride = g->dp;
+    o->iterations = g->iters;
+    o->zero_rows = g->zero_rows;
+    o->max_degree = g->max_degree;
+    o->heavy_rows = g->sched.n_heavy_rows;
+    o->heavy_items = g->sched.n_items;
+    o->shard_begin = g->r0;
+    o->shard_end = g->r1;
+    o->rank = g->rank;
+    o->world = g->world;
+    o->device_bytes = g->bytes + (g->T[0] ? 2 * (int64_t)g->n * g->dp * 4 : 0) +
+                      (g->partials ? g->sched.n_items * (int64_t)g->dp * 4 : 0);
+    DeviceGuard guard(g->device);
+    cudaError_t e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_info: ") + cudaGetErrorString(e)));
+    return CLEORA_OK;
+}
+
+int cleora_stats(cleora_graph* g, cleora_stats_t* o, int32_t reset) {
+    if (!g || !o) return usage("cleora_stats: NULL argument");
+    DeviceGuard guard(g->device);
+    Status s = collect_timing(g);
+    if (!s.good()) return fail(s);
+    o->spmm_launches = g->n_spmm;
+    o->spmm_ms_total = g->ms_spmm;
+    o->spmm_ms_min = g->n_spmm ? g->ms_min : 0.0;
+    o->spmm_ms_max = g->ms_max;
+    o->exchange_launches = g->n_x;
+    o->exchange_ms_total = g->ms_x;
+    if (reset) {
+        g->n_spmm = g->n_x = 0;
+        g->ms_spmm = g->ms_x = g->ms_max = 0;
+        g->ms_min = 1e300;
+    }
+    return CLEORA_OK;
+}
+
+int cleora_sync(const cleora_graph* g) {
+    if (!g) return usage("cleora_sync: graph is NULL");
+    DeviceGuard guard(g->device);
+    cudaError_t e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_sync: ") + cudaGetErrorString(e)));
+    return CLEORA_OK;
+}
+
+void cleora_destroy(cleora_graph* g) {
+    if (!g) return;
+    DeviceGuard guard(g->device);
+    if (g->stream) {
+        cudaStreamSynchronize(g->stream);
+        free_T(g);
+        dfree(g->row_ptr, g->stream);
+        dfree(g->col, g->stream);
+        dfree(g->val, g->stream);
+        dfree(g->deg, g->stream);
+        dfree(g->sched.items, g->stream);
+        dfree(g->sched.counters, g->stream);
+        cudaStreamSynchronize(g->stream);
+    }
+    for (auto& p : g->ev_spmm) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    for (auto& p : g->ev_x) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    for (auto e : g->ev_pool) cudaEventDestroy(e);
+    if (g->comm) nccl().CommDestroy(g->comm);
+    if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
+    delete g;
+}
+
+int cleora_nccl_id_size(void) { return NCCL_UNIQUE_ID_BYTES; }
+
+int cleora_nccl_get_unique_id(uint8_t* out128) {
+    if (!out128) return usage("cleora_nccl_get_unique_id: NULL");
+    Nccl& n = nccl();
+    if (!n.ok) return fail(Status::make(4, "NCCL unavailable: " + n.why));
+    ncclUniqueId id;
+    ncclResult_t r = n.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(Status::make(4, std::string("ncclGetUniqueId: ") + n.GetErrorString(r)));
+    memcpy(out128, id.internal, NCCL_UNIQUE_ID_BYTES);
+    return CLEORA_OK;
+}
+
+int cleora_plan_shards(const int64_t* row_ptr, int64_t n, int32_t world, int64_t* cuts) {
+    if (!row_ptr || !cuts) return usage("cleora_plan_shards: NULL argument");
+    if (n < 0 || world < 1) return usage("cleora_plan_shards: n >= 0 and world >= 1 required");
+    const int64_t nnz = row_ptr[n];
+    cuts[0] = 0;
+    for (int p = 1; p < world; p++) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if ((__int128)row_ptr[mid] * world >= (__int128)p * nnz) hi = mid; else lo = mid + 1;
+        }
+        cuts[p] = lo;
+    }
+    cuts[world] = n;
+    return CLEORA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,376 @@
+// build.cu -- on-device construction of M = D^-1 A in CSR and of the iteration schedule.
+//
+// PAPER.md:79-81 (§3.2 "Embedding"): M_ab = e_ab / deg(v_a), e_ab = number of a->b edges, or
+// the sum of their weights.  Algorithm 1 line 3 builds M per chunk; here Q = 1.
+// Bit-exact contract with the oracle (readings B1-B4):
+//   B1 entries = originals in input order, then mirrors (undirected, u != v) in input order;
+//      STABLE sort by (src, dst)                      -> cub radix sort (stable) on src*N+dst
+//   B2 e_ab   = fp64 sum in that stable order        -> one thread per run, sequential
+//   B3 deg(a) = fp64 sum of e_ab over ascending b     -> one thread per row, sequential
+//   B4 val    = fp32_rn(e_ab / deg(a))                -> IEEE double divide, one rounding
+// This translation unit must not be compiled with --use_fast_math.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include "common.cuh"
+
+namespace cleora {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(int64_t n, int per_thread = 1) {
+    int64_t b = (n + (int64_t)kThreads * per_thread - 1) / ((int64_t)kThreads * per_thread);
+    if (b < 1) b = 1;
+    if (b > (1 << 30)) b = 1 << 30;
+    return (int)b;
+}
+
+__global__ void k_validate_expand(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                                  const float* __restrict__ w, int64_t E, int32_t N, int directed,
+                                  uint64_t sentinel, uint64_t* __restrict__ keys, uint32_t* __restrict__ pos,
+                                  unsigned long long* __restrict__ err_first, int* __restrict__ err_kind,
+                                  unsigned long long* __restrict__ n_self) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += stride) {
+        int32_t u = src[i], v = dst[i];
+        bool bad_id = u < 0 || u >= N || v < 0 || v >= N;
+        bool bad_w = false;
+        if (w) {
+            float x = w[i];
+            bad_w = !(isfinite(x) && x > 0.0f);
+        }
+        if (bad_id || bad_w) {
+            atomicMin(err_first, (unsigned long long)i);
+            atomicOr(err_kind, bad_id ? 1 : 2);
+            u = 0; v = 0;
+        }
+        keys[i] = (uint64_t)(uint32_t)u * (uint64_t)N + (uint64_t)(uint32_t)v;
+        pos[i] = (uint32_t)i;
+        if (!directed) {
+            if (u == v) {
+                keys[E + i] = sentinel;          // the mirror of a self-loop is dropped (reading R5)
+                atomicAdd(n_self, 1ull);
+            } else {
+                keys[E + i] = (uint64_t)(uint32_t)v * (uint64_t)N + (uint64_t)(uint32_t)u;
+            }
+            pos[E + i] = (uint32_t)(E + i);
+        }
+    }
+}
+
+__global__ void k_head_flags(const uint64_t* __restrict__ keys, int64_t n, uint8_t* __restrict__ flags) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+// B2: one thread per (a,b) run: sequential fp64 sum in stable order.
+__global__ void k_merge_runs(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ pos,
+                             const int64_t* __restrict__ run_start, int64_t nnz, int64_t n_valid,
+                             const float* __restrict__ w, int64_t E, int32_t N, int32_t* __restrict__ rows,
+                             int32_t* __restrict__ col, double* __restrict__ e_ab) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nnz; u += stride) {
+        int64_t s = run_start[u], e = (u + 1 < nnz) ? run_start[u + 1] : n_valid;
+        uint64_t k = keys[s];
+        rows[u] = (int32_t)(k / (uint64_t)N);
+        col[u] = (int32_t)(k % (uint64_t)N);
+        double acc = 0.0;
+        if (w) {
+            for (int64_t i = s; i < e; i++) {
+                int64_t p = pos[i];
+                acc = acc + (double)w[p < E ? p : p - E];
+            }
+        } else {
+            for (int64_t i = s; i < e; i++) acc = acc + 1.0;
+        }
+        e_ab[u] = acc;
+    }
+}
+
+// row_ptr from the row of each (sorted) unique entry; deterministic, no atomics.
+__global__ void k_row_ptr(const int32_t* __restrict__ rows, int64_t nnz, int32_t N, int64_t* __restrict__ row_ptr) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nnz; u += stride) {
+        int32_t r = rows[u];
+        int32_t prev = (u == 0) ? -1 : rows[u - 1];
+        for (int32_t rr = prev + 1; rr <= r; rr++) row_ptr[rr] = u;
+        if (u == nnz - 1)
+            for (int64_t rr = (int64_t)r + 1; rr <= N; rr++) row_ptr[rr] = nnz;
+    }
+}
+
+// B3: deg(a) = sum over ascending b of e_ab, sequential per row.  Also zero rows / max degree.
+__global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __restrict__ e_ab, int32_t N,
+                         double* __restrict__ deg, unsigned long long* __restrict__ zero_rows,
+                         unsigned long long* __restrict__ max_deg) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < N; a += stride) {
+        int64_t k0 = row_ptr[a], k1 = row_ptr[a + 1];
+        double s = 0.0;
+        for (int64_t k = k0; k < k1; k++) s = s + e_ab[k];
+        deg[a] = s;
+        if (k1 == k0) atomicAdd(zero_rows, 1ull);
+        else atomicMax(max_deg, (unsigned long long)(k1 - k0));
+    }
+}
+
+// B4: val = fp32_rn(e_ab / deg(a)).
+__global__ void k_values(const int32_t* __restrict__ rows, const double* __restrict__ e_ab,
+                         const double* __restrict__ deg, int64_t nnz, float* __restrict__ val) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride)
+        val[k] = __double2float_rn(e_ab[k] / deg[rows[k]]);
+}
+
+struct IsHeavy {
+    const int64_t* rp;
+    int64_t thresh;
+    __host__ __device__ bool operator()(int64_t r) const { return rp[r + 1] - rp[r] > thresh; }
+};
+
+__global__ void k_items_per_row(const int64_t* __restrict__ rp, const int64_t* __restrict__ hrows, int64_t nh,
+                                int64_t per_item, int64_t* __restrict__ nit) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride) {
+        int64_t r = hrows[h];
+        int64_t c = rp[r + 1] - rp[r];
+        nit[h] = (c + per_item - 1) / per_item;
+    }
+}
+
+__global__ void k_fill_items(const int64_t* __restrict__ rp, const int64_t* __restrict__ hrows, int64_t nh,
+                             const int64_t* __restrict__ first, int64_t per_item, HeavyItem* __restrict__ items) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride) {
+        int64_t r = hrows[h];
+        int64_t k0 = rp[r], k1 = rp[r + 1];
+        int64_t n = (k1 - k0 + per_item - 1) / per_item;
+        for (int64_t p = 0; p < n; p++) {
+            HeavyItem it;
+            it.k0 = k0 + p * per_item;
+            it.k1 = min(k1, it.k0 + per_item);
+            it.row = (int32_t)r;
+            it.part = (int32_t)p;
+            it.nparts = (int32_t)n;
+            it.hrow = (int32_t)h;
+            items[first[h] + p] = it;
+        }
+    }
+}
+
+// nnz-balanced cuts: cut p = first row r with row_ptr[r] * world >= p * nnz.
+__global__ void k_cuts(const int64_t* __restrict__ rp, int32_t N, int world, int64_t* __restrict__ cuts) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > world) return;
+    int64_t nnz = rp[N];
+    if (p == 0) { cuts[0] = 0; return; }
+    if (p == world) { cuts[world] = N; return; }
+    int64_t lo = 0, hi = N;   // search in [0, N]
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        // compare row_ptr[mid] * world >= p * nnz without overflow (both < 2^63 / 64 here)
+        if ((__int128)rp[mid] * world >= (__int128)p * nnz) hi = mid; else lo = mid + 1;
+    }
+    cuts[p] = lo;
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    ~DevBuf() { if (p) dfree(p, s); }
+    Status alloc(size_t n, cudaStream_t st, const char* what) {
+        s = st;
+        return dalloc((void**)&p, n * sizeof(T) + 16, st, what);
+    }
+    T* release() { T* q = p; p = nullptr; return q; }
+};
+
+}  // namespace
+
+Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N,
+                 int directed, cudaStream_t s, BuildOut* out) {
+    const int64_t n_ent = directed ? E : 2 * E;
+    if (n_ent >= (int64_t)UINT32_MAX) return Status::make(2, "cleora_build: too many edges (entry positions are 32-bit)");
+    const uint64_t NN = (uint64_t)N * (uint64_t)N;
+    const uint64_t sentinel = NN;                        // sorts after every valid key
+    const int end_bit = 64 - __builtin_clzll(sentinel | 1ull);
+
+    DevBuf<uint64_t> keys, keys2;
+    DevBuf<uint32_t> pos, pos2;
+    DevBuf<unsigned long long> scal;                     // [0] err_first [1] n_self [2] zero_rows [3] max_deg [4] nnz
+    DevBuf<int> err_kind;
+    CL_TRY(keys.alloc(n_ent, s, "sort keys"));
+    CL_TRY(keys2.alloc(n_ent, s, "sort keys (alt)"));
+    CL_TRY(pos.alloc(n_ent, s, "sort payload"));
+    CL_TRY(pos2.alloc(n_ent, s, "sort payload (alt)"));
+    CL_TRY(scal.alloc(8, s, "scalars"));
+    CL_TRY(err_kind.alloc(1, s, "scalars"));
+    CL_CUDA_TRY(cudaMemsetAsync(scal.p, 0, 8 * sizeof(unsigned long long), s));
+    CL_CUDA_TRY(cudaMemsetAsync(scal.p, 0xFF, sizeof(unsigned long long), s));   // err_first = max
+    CL_CUDA_TRY(cudaMemsetAsync(err_kind.p, 0, sizeof(int), s));
+
+    k_validate_expand<<<grid_for(E, 4), kThreads, 0, s>>>(d_src, d_dst, d_w, E, N, directed, sentinel, keys.p, pos.p,
+                                                          scal.p + 0, err_kind.p, scal.p + 1);
+    CL_CUDA_TRY(cudaGetLastError());
+    unsigned long long h_scal[2];
+    int h_kind = 0;
+    CL_CUDA_TRY(cudaMemcpyAsync(h_scal, scal.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CL_CUDA_TRY(cudaMemcpyAsync(&h_kind, err_kind.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h_kind) {
+        char buf[256];
+        snprintf(buf, sizeof buf, "cleora_build: edge %llu: %s", (unsigned long long)h_scal[0],
+                 (h_kind & 1) ? "node id outside [0, n_nodes)" : "weight not finite or <= 0");
+        return Status::make(3, buf);
+    }
+    const int64_t n_valid = n_ent - (int64_t)h_scal[1];
+
+    // B1: stable radix sort by (src, dst) over the bits the keys use
+    {
+        cub::DoubleBuffer<uint64_t> kb(keys.p, keys2.p);
+        cub::DoubleBuffer<uint32_t> vb(pos.p, pos2.p);
+        size_t tmp_bytes = 0;
+        CL_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, n_ent, 0, end_bit, s));
+        DevBuf<uint8_t> tmp;
+        CL_TRY(tmp.alloc(tmp_bytes, s, "radix sort temp"));
+        CL_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kb, vb, n_ent, 0, end_bit, s));
+        if (kb.Current() != keys.p) std::swap(keys.p, keys2.p);
+        if (vb.Current() != pos.p) std::swap(pos.p, pos2.p);
+    }
+    dfree(keys2.release(), s);
+
+    // B2: run starts of equal keys, merged weights
+    DevBuf<uint8_t> flags;
+    DevBuf<int64_t> run_start;
+    CL_TRY(flags.alloc(n_valid, s, "head flags"));
+    CL_TRY(run_start.alloc(n_valid, s, "run starts"));
+    k_head_flags<<<grid_for(n_valid, 4), kThreads, 0, s>>>(keys.p, n_valid, flags.p);
+    CL_CUDA_TRY(cudaGetLastError());
+    {
+        thrust::counting_iterator<int64_t> it(0);
+        size_t tmp_bytes = 0;
+        CL_CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flags.p, run_start.p, scal.p + 4, n_valid, s));
+        DevBuf<uint8_t> tmp;
+        CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
+        CL_CUDA_TRY(cub::DeviceSelect::Flagged(tmp.p, tmp_bytes, it, flags.p, run_start.p, scal.p + 4, n_valid, s));
+    }
+    dfree(flags.release(), s);
+    unsigned long long h_nnz = 0;
+    CL_CUDA_TRY(cudaMemcpyAsync(&h_nnz, scal.p + 4, sizeof h_nnz, cudaMemcpyDeviceToHost, s));
+    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    const int64_t nnz = (int64_t)h_nnz;
+
+    DevBuf<int32_t> rows, col;
+    DevBuf<double> e_ab, deg;
+    DevBuf<int64_t> row_ptr;
+    DevBuf<float> val;
+    CL_TRY(rows.alloc(nnz, s, "entry rows"));
+    CL_TRY(col.alloc(nnz, s, "CSR col"));
+    CL_TRY(e_ab.alloc(nnz, s, "e_ab"));
+    k_merge_runs<<<grid_for(nnz, 4), kThreads, 0, s>>>(keys.p, pos.p, run_start.p, nnz, n_valid, d_w, E, N,
+                                                       rows.p, col.p, e_ab.p);
+    CL_CUDA_TRY(cudaGetLastError());
+    dfree(run_start.release(), s);
+    dfree(keys.release(), s);
+    dfree(pos.release(), s);
+    dfree(pos2.release(), s);
+
+    CL_TRY(row_ptr.alloc((size_t)N + 1, s, "CSR row_ptr"));
+    CL_CUDA_TRY(cudaMemsetAsync(row_ptr.p, 0, sizeof(int64_t), s));
+    k_row_ptr<<<grid_for(nnz, 4), kThreads, 0, s>>>(rows.p, nnz, N, row_ptr.p);
+    CL_CUDA_TRY(cudaGetLastError());
+
+    CL_TRY(deg.alloc(N, s, "degree"));
+    k_degree<<<grid_for(N, 4), kThreads, 0, s>>>(row_ptr.p, e_ab.p, N, deg.p, scal.p + 2, scal.p + 3);
+    CL_CUDA_TRY(cudaGetLastError());
+    CL_TRY(val.alloc(nnz, s, "CSR val"));
+    k_values<<<grid_for(nnz, 4), kThreads, 0, s>>>(rows.p, e_ab.p, deg.p, nnz, val.p);
+    CL_CUDA_TRY(cudaGetLastError());
+    unsigned long long h_zm[2];
+    CL_CUDA_TRY(cudaMemcpyAsync(h_zm, scal.p + 2, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CL_CUDA_TRY(cudaStreamSynchronize(s));
+
+    out->nnz = nnz;
+    out->zero_rows = (int64_t)h_zm[0];
+    out->max_degree = (int64_t)h_zm[1];
+    out->row_ptr = row_ptr.release();
+    out->col = col.release();
+    out->val = val.release();
+    out->deg = deg.release();
+    return Status::ok();
+}
+
+Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int heavy_thresh,
+                      cudaStream_t s, Schedule* out) {
+    (void)N;
+    const int64_t nr = r1 - r0;
+    out->n_heavy_rows = 0;
+    out->n_items = 0;
+    out->items = nullptr;
+    out->counters = nullptr;
+    if (nr <= 0) return Status::ok();
+    DevBuf<int64_t> hrows, cnt;
+    CL_TRY(hrows.alloc(nr, s, "heavy rows"));
+    CL_TRY(cnt.alloc(2, s, "scalars"));
+    {
+        thrust::counting_iterator<int64_t> it(r0);
+        IsHeavy pred{d_row_ptr, heavy_thresh};
+        size_t tmp_bytes = 0;
+        CL_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, it, hrows.p, cnt.p, nr, pred, s));
+        DevBuf<uint8_t> tmp;
+        CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
+        CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, hrows.p, cnt.p, nr, pred, s));
+    }
+    int64_t nh = 0;
+    CL_CUDA_TRY(cudaMemcpyAsync(&nh, cnt.p, sizeof nh, cudaMemcpyDeviceToHost, s));
+    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    out->n_heavy_rows = nh;
+    if (nh == 0) return Status::ok();
+    const int64_t per_item = (int64_t)heavy_thresh * kWarpsPerCta;
+    DevBuf<int64_t> nit, first;
+    CL_TRY(nit.alloc(nh, s, "items per heavy row"));
+    CL_TRY(first.alloc(nh, s, "first item"));
+    k_items_per_row<<<grid_for(nh), kThreads, 0, s>>>(d_row_ptr, hrows.p, nh, per_item, nit.p);
+    CL_CUDA_TRY(cudaGetLastError());
+    {
+        size_t tmp_bytes = 0;
+        CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, nit.p, first.p, nh, s));
+        DevBuf<uint8_t> tmp;
+        CL_TRY(tmp.alloc(tmp_bytes, s, "scan temp"));
+        CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, nit.p, first.p, nh, s));
+    }
+    int64_t last[2];
+    CL_CUDA_TRY(cudaMemcpyAsync(&last[0], first.p + nh - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CL_CUDA_TRY(cudaMemcpyAsync(&last[1], nit.p + nh - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    const int64_t n_items = last[0] + last[1];
+    DevBuf<HeavyItem> items;
+    DevBuf<unsigned> counters;
+    CL_TRY(items.alloc(n_items, s, "heavy items"));
+    CL_TRY(counters.alloc(nh, s, "heavy counters"));
+    CL_CUDA_TRY(cudaMemsetAsync(counters.p, 0, nh * sizeof(unsigned), s));
+    k_fill_items<<<grid_for(nh), kThreads, 0, s>>>(d_row_ptr, hrows.p, nh, first.p, per_item, items.p);
+    CL_CUDA_TRY(cudaGetLastError());
+    out->n_items = n_items;
+    out->items = items.release();
+    out->counters = counters.release();
+    return Status::ok();
+}
+
+Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts) {
+    DevBuf<int64_t> cuts;
+    CL_TRY(cuts.alloc(world + 1, s, "shard cuts"));
+    k_cuts<<<1, 128, 0, s>>>(d_row_ptr, N, world, cuts.p);
+    CL_CUDA_TRY(cudaGetLastError());
+    CL_CUDA_TRY(cudaMemcpyAsync(h_cuts, cuts.p, (world + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    return Status::ok();
+}
+
+}  // namespace cleora

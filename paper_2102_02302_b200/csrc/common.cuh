@@ -1,0 +1,97 @@
+// common.cuh -- shared declarations of libcleora (the B200 product path).
+// Nothing here is shared with oracle/ (task rule 3: the two share no code).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace cleora {
+
+// ---------------------------------------------------------------- error plumbing
+void set_error(const std::string& msg);     // thread-local message for cleora_last_error()
+
+struct Status {
+    int code = 0;
+    std::string msg;
+    static Status ok() { return Status(); }
+    static Status make(int c, const std::string& m) { Status s; s.code = c; s.msg = m; return s; }
+    bool good() const { return code == 0; }
+};
+
+#define CL_CUDA_TRY(expr)                                                                  \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return ::cleora::Status::make(4, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define CL_TRY(expr)                                                                       \
+    do {                                                                                   \
+        ::cleora::Status _s = (expr);                                                      \
+        if (!_s.good()) return _s;                                                         \
+    } while (0)
+
+// ---------------------------------------------------------------- device buffers
+// Stream-ordered allocation from the device's default pool (release threshold raised so
+// repeated build/destroy cycles do not return memory to the driver).
+Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what);
+void dfree(void* p, cudaStream_t s);
+
+// ---------------------------------------------------------------- schedule
+// A CTA work item of the heavy path: entries [k0, k1) of row `row`, which is part `part`
+// of `nparts` of that row; `hrow` indexes the row's completion counter; the partial vector
+// of item i lives at partials + i * dp.
+struct HeavyItem {
+    int64_t k0, k1;
+    int32_t row, part, nparts, hrow;
+};
+static_assert(sizeof(HeavyItem) == 32, "HeavyItem layout");
+
+constexpr int kWarpsPerCta = 8;     // 256 threads
+constexpr int kMaxV = 8;            // float4 per lane per column slice (slice = 1024 floats)
+
+struct SpmmArgs {
+    const int64_t* row_ptr;
+    const int32_t* col;
+    const float* val;
+    const float* T_in;
+    float* T_out;
+    int32_t dp;             // row stride in floats (multiple of 4)
+    int64_t r0, r1;         // rows this launch computes on the light path (shard)
+    int32_t heavy_thresh;   // rows with more entries than this are on the heavy path
+    const HeavyItem* items;
+    int64_t n_items;
+    float* partials;        // n_items * dp floats
+    unsigned* counters;     // one per heavy row, 0 between launches
+};
+
+// build.cu
+struct BuildOut {
+    int64_t nnz = 0;
+    int64_t* row_ptr = nullptr;
+    int32_t* col = nullptr;
+    float* val = nullptr;
+    double* deg = nullptr;
+    int64_t zero_rows = 0, max_degree = 0;
+};
+Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N,
+                 int directed, cudaStream_t s, BuildOut* out);
+
+struct Schedule {
+    int64_t n_heavy_rows = 0, n_items = 0;
+    HeavyItem* items = nullptr;
+    unsigned* counters = nullptr;
+};
+Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int heavy_thresh,
+                      cudaStream_t s, Schedule* out);
+Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts);
+
+// init.cu
+Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s);
+
+// spmm_norm.cu
+Status launch_spmm_norm(const SpmmArgs& a, cudaStream_t s);
+
+}  // namespace cleora

@@ -1,0 +1,285 @@
+// spmm_norm.cu -- one Cleora iteration: T_out = normalize_rows(M . T_in), fused.
+//
+// Algorithm 1 lines 6-7: "T_i = M . T_{i-1}; L2 normalize rows of T_i".
+// M is the CSR of D^-1 A (build.cu).  A row of the product is a weighted average of gathered
+// neighbour rows of T_in ("iterated L2-normalized weighted averaging of
+// neighboring nodes' representations"), so the kernel is a sparse gather-reduce, bound by
+// memory traffic, not by arithmetic: no tensor cores.
+//
+// Schedule (chosen per row from its degree only, so the result is independent of the number
+// of GPUs and bitwise reproducible run to run -- no floating-point atomics anywhere):
+//   light rows (cnt <= heavy_thresh): one warp per row, 8 rows per CTA, in row-id order.
+//     Lane l owns float4 columns l, l+32, ..., gathers every neighbour row with 16-byte
+//     read-only loads (a warp instruction covers 512 contiguous bytes), FMAs into fp32
+//     registers in ascending-k order, then reduces sum(y^2) in fp64 with warp shuffles and
+//     writes y / ||y|| with 16-byte streaming stores.
+//   heavy rows (cnt > heavy_thresh): CTA work items of <= 8*heavy_thresh entries; the 8 warps
+//     split an item evenly, combine their partial vectors through shared memory in warp order,
+//     and either normalise directly (one item) or publish the item's partial vector; the last
+//     CTA to finish a row (atomic ticket) sums the partials in part order in fp64 and
+//     normalises.  This is the merge-path split for power-law hubs; it also bounds every
+//     sequential fp32 summation to <= heavy_thresh terms (the precision requirement of
+//     SURVEY.md §0.4 / DESIGN.md §Precision).
+//   Rows whose product is the zero vector (no out-edges) are written as zeros (reading RZ).
+#include "common.cuh"
+
+namespace cleora {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
+
+__device__ __forceinline__ void fma4(float4& acc, float w, const float4& x) {
+    acc.x = fmaf(w, x.x, acc.x);
+    acc.y = fmaf(w, x.y, acc.y);
+    acc.z = fmaf(w, x.z, acc.z);
+    acc.w = fmaf(w, x.w, acc.w);
+}
+
+__device__ __forceinline__ double sq4(const float4& y) {
+    return (double)y.x * y.x + (double)y.y * y.y + (double)y.z * y.z + (double)y.w * y.w;
+}
+
+__device__ __forceinline__ float4 scale4(const float4& y, double inv) {
+    return make_float4((float)((double)y.x * inv), (float)((double)y.y * inv), (float)((double)y.z * inv),
+                       (float)((double)y.w * inv));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarpsPerCta; w++) s += scratch[w];   // fixed order: deterministic
+    return s;
+}
+
+// acc[v] += sum_{k in [k0,k1)} val[k] * T_in[col[k]][cbase + 4*(lane + 32 v) .. +3], ascending k.
+template <int V>
+__device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, int64_t k0, int64_t k1, int cbase, int lane,
+                                                float4 (&acc)[V]) {
+    constexpr int U = (V >= 8) ? 1 : 8 / V;      // neighbours per batch: U*V 16-byte loads in flight
+    const int dp = a.dp;
+    bool ok[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) ok[v] = cbase + 4 * (lane + 32 * v) < dp;
+    const float* tb = a.T_in + cbase + 4 * lane;
+    for (int64_t kb = k0; kb < k1; kb += 32) {
+        const int n = (int)min((int64_t)32, k1 - kb);
+        int32_t mc = 0;
+        float mw = 0.0f;
+        if (lane < n) {
+            mc = __ldg(a.col + kb + lane);
+            mw = __ldg(a.val + kb + lane);
+        }
+        int j = 0;
+        for (; j + U <= n; j += U) {
+            float4 x[U][V];
+            float w[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int c = __shfl_sync(kFull, mc, j + u);
+                w[u] = __shfl_sync(kFull, mw, j + u);
+                const float4* p = reinterpret_cast<const float4*>(tb + (int64_t)c * dp);
+#pragma unroll
+                for (int v = 0; v < V; v++) x[u][v] = ok[v] ? ldg4(p + 32 * v) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++)
+#pragma unroll
+                for (int v = 0; v < V; v++) fma4(acc[v], w[u], x[u][v]);
+        }
+        for (; j < n; j++) {
+            const int c = __shfl_sync(kFull, mc, j);
+            const float w = __shfl_sync(kFull, mw, j);
+            const float4* p = reinterpret_cast<const float4*>(tb + (int64_t)c * dp);
+#pragma unroll
+            for (int v = 0; v < V; v++)
+                if (ok[v]) fma4(acc[v], w, ldg4(p + 32 * v));
+        }
+    }
+}
+
+template <int V>
+__device__ void light_row(const SpmmArgs& a, int64_t row, int64_t k0, int64_t k1, int lane) {
+    constexpr int SW = 128 * V;                   // floats per column slice
+    const int dp = a.dp;
+    const int ns = (dp + SW - 1) / SW;
+    float4* out = reinterpret_cast<float4*>(a.T_out + row * (int64_t)dp);
+    double ss = 0.0;
+    float4 acc[V];
+    for (int sl = 0; sl < ns; sl++) {
+        const int cbase = sl * SW;
+#pragma unroll
+        for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        accumulate_warp<V>(a, k0, k1, cbase, lane, acc);
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            const int f = cbase / 4 + lane + 32 * v;
+            if (4 * f < dp) {
+                ss += sq4(acc[v]);
+                if (ns > 1) out[f] = acc[v];      // unnormalised; rescaled below
+            }
+        }
+    }
+    ss = warp_sum(ss);
+    const double inv = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+    if (ns == 1) {
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            const int f = lane + 32 * v;
+            if (4 * f < dp) __stcs(out + f, scale4(acc[v], inv));
+        }
+    } else {
+        for (int f = lane; 4 * f < dp; f += 32) __stcs(out + f, scale4(out[f], inv));
+    }
+}
+
+template <int V>
+__device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* scratch, int* flag) {
+    constexpr int SW = 128 * V;
+    constexpr int Q = 32 * V;                     // float4 per slice
+    const HeavyItem it = a.items[idx];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
+    const int dp = a.dp, nq = dp / 4;
+    const int ns = (dp + SW - 1) / SW;
+    const int64_t len = it.k1 - it.k0;
+    const int64_t sub = (len + kWarpsPerCta - 1) / kWarpsPerCta;
+    const int64_t wk0 = min(it.k0 + warp * sub, it.k1), wk1 = min(wk0 + sub, it.k1);
+    const bool single = it.nparts == 1;
+    float4* dst = reinterpret_cast<float4*>(single ? a.T_out + (int64_t)it.row * dp : a.partials + idx * (int64_t)dp);
+
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    double ss = 0.0;
+    for (int sl = 0; sl < ns; sl++) {
+        float4 acc[V];
+#pragma unroll
+        for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        accumulate_warp<V>(a, wk0, wk1, sl * SW, lane, acc);
+#pragma unroll
+        for (int v = 0; v < V; v++) red[warp * Q + lane + 32 * v] = acc[v];
+        __syncthreads();
+        if (t < Q) {
+            const int f = sl * Q + t;
+            float4 s = red[t];
+#pragma unroll
+            for (int w = 1; w < kWarpsPerCta; w++) {   // warp order: deterministic
+                const float4 r = red[w * Q + t];
+                s.x += r.x; s.y += r.y; s.z += r.z; s.w += r.w;
+            }
+            y = s;
+            if (f < nq) {
+                ss += sq4(y);
+                if (!(single && ns == 1)) dst[f] = y;
+            }
+        }
+        __syncthreads();
+    }
+    if (single) {
+        const double tot = block_sum(ss, scratch);
+        const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+        if (ns == 1) {
+            if (t < Q && t < nq) __stcs(dst + t, scale4(y, inv));
+        } else {
+            for (int f = t; f < nq; f += blockDim.x) __stcs(dst + f, scale4(dst[f], inv));
+        }
+        return;
+    }
+    // publish this part; the last CTA of the row finishes it
+    __threadfence();
+    __syncthreads();
+    if (t == 0) {
+        const unsigned prev = atomicAdd(a.counters + it.hrow, 1u);
+        *flag = (prev == (unsigned)it.nparts - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (!*flag) return;
+    __threadfence();
+    const int64_t first = idx - it.part;
+    const float4* parts = reinterpret_cast<const float4*>(a.partials + first * (int64_t)dp);
+    const int64_t pstride = dp / 4;
+    float4* out = reinterpret_cast<float4*>(a.T_out + (int64_t)it.row * dp);
+    double zx = 0, zy = 0, zz = 0, zw = 0;
+    double ss2 = 0.0;
+    for (int f = t; f < nq; f += blockDim.x) {
+        zx = zy = zz = zw = 0.0;
+        for (int q = 0; q < it.nparts; q++) {     // part order: deterministic
+            const float4 p = __ldcg(parts + q * pstride + f);
+            zx += p.x; zy += p.y; zz += p.z; zw += p.w;
+        }
+        ss2 += zx * zx + zy * zy + zz * zz + zw * zw;
+    }
+    const double tot = block_sum(ss2, scratch);
+    const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+    if (nq <= (int)blockDim.x) {
+        if (t < nq)
+            __stcs(out + t, make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
+    } else {
+        for (int f = t; f < nq; f += blockDim.x) {
+            zx = zy = zz = zw = 0.0;
+            for (int q = 0; q < it.nparts; q++) {
+                const float4 p = __ldcg(parts + q * pstride + f);
+                zx += p.x; zy += p.y; zz += p.z; zw += p.w;
+            }
+            __stcs(out + f, make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
+        }
+    }
+    if (t == 0) a.counters[it.hrow] = 0u;         // ready for the next launch
+}
+
+template <int V>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_norm(const SpmmArgs a) {
+    extern __shared__ float4 red[];
+    __shared__ double scratch[kWarpsPerCta];
+    __shared__ int flag;
+    const int64_t b = blockIdx.x;
+    if (b < a.n_items) {
+        heavy_item<V>(a, b, red, scratch, &flag);
+        return;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row = a.r0 + (b - a.n_items) * kWarpsPerCta + warp;
+    if (row >= a.r1) return;
+    const int64_t k0 = a.row_ptr[row], k1 = a.row_ptr[row + 1];
+    if (k1 - k0 > a.heavy_thresh) return;
+    light_row<V>(a, row, k0, k1, lane);
+}
+
+template <int V>
+Status launch_v(const SpmmArgs& a, cudaStream_t s) {
+    const size_t smem = (size_t)kWarpsPerCta * 32 * V * sizeof(float4);
+    static bool configured = false;
+    if (!configured) {
+        CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_norm<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = true;
+    }
+    const int64_t light_ctas = (a.r1 - a.r0 + kWarpsPerCta - 1) / kWarpsPerCta;
+    const int64_t grid = a.n_items + (light_ctas > 0 ? light_ctas : 0);
+    if (grid <= 0) return Status::ok();
+    if (grid > 0x7fffffffLL) return Status::make(2, "cleora_iterate: grid too large");
+    k_spmm_norm<V><<<(unsigned)grid, kWarpsPerCta * 32, smem, s>>>(a);
+    CL_CUDA_TRY(cudaGetLastError());
+    return Status::ok();
+}
+
+}  // namespace
+
+Status launch_spmm_norm(const SpmmArgs& a, cudaStream_t s) {
+    if (a.dp <= 128) return launch_v<1>(a, s);
+    if (a.dp <= 256) return launch_v<2>(a, s);
+    if (a.dp <= 512) return launch_v<4>(a, s);
+    return launch_v<8>(a, s);
+}
+
+}  // namespace cleora

@@ -1,0 +1,236 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle -- needs a B200.
+
+Bars (BASELINE.json north_star): CSR structure, values and degrees bit-exact; T_0 bit-exact;
+every iterate within max|d| <= 1e-5 per element and cosine >= 0.99999 per non-zero row; the
+zero-row sets identical.  Inputs are the seeded generators of gen/ (DESIGN.md "Input recipe").
+"""
+import os
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL_ABS = 1e-5
+TOL_COS = 0.99999
+
+
+@pytest.fixture(scope="module")
+def cl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2102_02302_b200 as m
+    return m
+
+
+def check_csr(csr, M):
+    assert np.array_equal(csr["row_ptr"], M.row_ptr), "row_ptr"
+    assert np.array_equal(csr["col"], M.col), "col"
+    assert np.array_equal(csr["val"].view(np.uint32), M.val.view(np.uint32)), "val bits"
+    assert np.array_equal(csr["deg"].view(np.uint64), M.deg.view(np.uint64)), "deg bits"
+
+
+def compare(T, R, what=""):
+    """max|d| and min cosine over non-zero rows; zero-row sets must be identical."""
+    T = T.astype(np.float64)
+    R = R.astype(np.float64)
+    err = float(np.abs(T - R).max()) if T.size else 0.0
+    zt, zr = ~T.any(1), ~R.any(1)
+    assert np.array_equal(zt, zr), f"{what}: zero-row sets differ ({zt.sum()} vs {zr.sum()})"
+    nz = ~zr
+    if nz.any():
+        cos = (T[nz] * R[nz]).sum(1) / (np.linalg.norm(T[nz], axis=1) * np.linalg.norm(R[nz], axis=1))
+        mc = float(cos.min())
+    else:
+        mc = 1.0
+    assert err <= TOL_ABS, f"{what}: max|d| = {err:.3e}"
+    assert mc >= TOL_COS, f"{what}: min cos = {mc:.9f}"
+    return err, mc
+
+
+def ill_conditioned(M, T_prev):
+    """True if some row's pre-normalisation vector is (near) zero although it has live
+    neighbours: normalising it is ill-defined, so any rounding may flip it (d=1 graphs)."""
+    if M.nnz == 0:
+        return False
+    rows = np.repeat(np.arange(M.n), np.diff(M.row_ptr))
+    Y = np.zeros_like(T_prev, dtype=np.float64)
+    np.add.at(Y, rows, M.val[:, None].astype(np.float64) * T_prev[M.col].astype(np.float64))
+    live = np.zeros(M.n, bool)
+    np.logical_or.at(live, rows, T_prev[M.col].any(1))
+    nr = np.linalg.norm(Y, axis=1)
+    return bool(live.any() and nr[live].min() < 1e-4)
+
+
+def run_case(cl, g, d, iters, seed=0, per_iter=True):
+    M = oracle.build_from(g)
+    G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0)
+    try:
+        check_csr(cl.cleora_fetch_csr(G), M)
+        cl.cleora_init(G, d, seed)
+        R = oracle.hash_init(g.n, d, seed)
+        T = cl.cleora_fetch(G)
+        assert np.array_equal(T.view(np.uint32), R.view(np.uint32)), "T_0 not bit-exact"
+        worst = (0.0, 1.0)
+        for i in range(1, iters + 1):
+            if ill_conditioned(M, R):
+                break
+            cl.cleora_iterate(G, 1)
+            R = oracle.step(M, R)
+            if per_iter or i == iters:
+                e, c = compare(cl.cleora_fetch(G), R, f"{g.name} d={d} iteration {i}")
+                worst = (max(worst[0], e), min(worst[1], c))
+        return worst
+    finally:
+        G.close()
+
+
+DIMS = [1, 2, 3, 4, 5, 7, 8, 16, 31, 33, 64, 100, 128, 129, 200, 256, 257, 384, 512, 513, 768, 1000, 1024,
+        1025, 1500, 2048, 3000, 4096]
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_tiny_random_graphs(cl, seed):
+    g = gen.tiny_graph(seed)
+    d = DIMS[seed % len(DIMS)]
+    run_case(cl, g, d, iters=1 + seed % 6, seed=seed)
+
+
+@pytest.mark.parametrize("d", [1, 4, 17, 128, 256, 1024, 1100])
+@pytest.mark.parametrize("directed,weighted", [(False, False), (True, True)])
+def test_hub_rows_multi_part(cl, d, directed, weighted):
+    """Power-law hubs: a star of 5000 leaves plus a random graph, so the hub row is split into
+    several CTA items (heavy path with the last-CTA fp64 finalisation)."""
+    rng = np.random.default_rng(d)
+    n = 6000
+    src = np.concatenate([np.zeros(5000, np.int32), rng.integers(0, n, 20000).astype(np.int32)])
+    dst = np.concatenate([np.arange(1, 5001, dtype=np.int32), rng.integers(0, n, 20000).astype(np.int32)])
+    w = rng.lognormal(0, 1, src.size).astype(np.float32) if weighted else None
+    g = gen.EdgeList("hub", n, src, dst, w, directed)
+    run_case(cl, g, d, iters=4)
+
+
+@pytest.mark.parametrize("thresh", ["8", "16", "64", "4096"])
+def test_schedule_threshold_does_not_change_results(cl, thresh, monkeypatch):
+    monkeypatch.setenv("CLEORA_HEAVY_THRESH", thresh)
+    g = gen.chung_lu(20000, 60000, 2.1, 9.5388, 233115.5 * 20000 / 1134890, seed=1)
+    run_case(cl, g, 256, iters=4)
+
+
+def test_c1_full(cl):
+    g = gen.config("c1")
+    run_case(cl, g, g.d, g.iters)
+
+
+def test_c3_full(cl):
+    g = gen.config("c3")
+    run_case(cl, g, g.d, g.iters, per_iter=False)
+
+
+def test_c2_full(cl):
+    g = gen.config("c2")
+    run_case(cl, g, g.d, g.iters, per_iter=False)
+
+
+def test_c4_full(cl):
+    g = gen.config("c4")
+    run_case(cl, g, g.d, g.iters, per_iter=False)
+
+
+def test_determinism_and_composability(cl):
+    """Same bytes on repeated runs; iterate(1)+iterate(2) == iterate(3) bit for bit."""
+    g = gen.config("c1")
+    outs = []
+    for split in ([3], [1, 2], [3]):
+        G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0)
+        cl.cleora_init(G, 64, 5)
+        for k in split:
+            cl.cleora_iterate(G, k)
+        outs.append(cl.cleora_fetch(G).tobytes())
+        G.close()
+    assert outs[0] == outs[1] == outs[2]
+
+
+def test_device_resident_inputs_and_stream(cl):
+    """The same result when the COO is already in HBM (torch CUDA tensors) and a caller stream is used."""
+    import torch
+    g = gen.config("c1")
+    s = torch.cuda.Stream()
+    G1 = cl.cleora_build(g.src, g.dst, g.w, g.n, False, device=0)
+    G2 = cl.cleora_build(torch.from_numpy(g.src).cuda(), torch.from_numpy(g.dst).cuda(), None, g.n, False,
+                         stream=s)
+    for G in (G1, G2):
+        cl.cleora_init(G, 128, 0)
+        cl.cleora_iterate(G, 2)
+    a, b = cl.cleora_fetch(G1), cl.cleora_fetch(G2)
+    out = torch.empty_like(torch.from_numpy(a)).cuda()
+    cl.cleora_fetch(G2, 0, g.n, out)
+    assert a.tobytes() == b.tobytes() == out.cpu().numpy().tobytes()
+    G1.close(); G2.close()
+
+
+def test_set_rows_and_partial_fetch(cl):
+    g = gen.config("c1")
+    M = oracle.build_from(g)
+    G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0)
+    cl.cleora_init(G, 20, 1)
+    T0 = np.random.default_rng(0).standard_normal((g.n, 20)).astype(np.float32)
+    cl.cleora_set_rows(G, 0, T0)
+    np.testing.assert_array_equal(cl.cleora_fetch(G, 100, 300), T0[100:300])
+    cl.cleora_iterate(G, 1)
+    compare(cl.cleora_fetch(G), oracle.step(M, T0), "custom T0")
+    assert cl.cleora_fetch(G, 5, 5).shape == (0, 20)
+    G.close()
+
+
+def test_error_codes(cl):
+    i32 = lambda *a: np.array(a, np.int32)
+    with pytest.raises(cl.CleoraError) as e:
+        cl.cleora_build(i32(0, 1), i32(1, 5), None, 3)
+    assert e.value.code == cl.EDATA and "edge 1" in str(e.value)
+    for bad in (0.0, -2.0, np.nan, np.inf):
+        with pytest.raises(cl.CleoraError) as e:
+            cl.cleora_build(i32(0, 1), i32(1, 2), np.array([1.0, bad], np.float32), 3)
+        assert e.value.code == cl.EDATA
+    with pytest.raises(cl.CleoraError) as e:
+        cl.cleora_build(i32(), i32(), None, 3)
+    assert e.value.code == cl.EUSAGE
+    with pytest.raises(cl.CleoraError) as e:
+        cl.cleora_build(i32(0), i32(1), None, 0)
+    assert e.value.code == cl.EUSAGE
+    G = cl.cleora_build(i32(0), i32(1), None, 2, device=0)
+    with pytest.raises(cl.CleoraError) as e:
+        cl.cleora_iterate(G, 1)                      # before init
+    assert e.value.code == cl.EUSAGE
+    with pytest.raises(cl.CleoraError) as e:
+        cl.cleora_init(G, 0, 0)
+    assert e.value.code == cl.EUSAGE
+    cl.cleora_init(G, 8, 0)
+    with pytest.raises(cl.CleoraError) as e:
+        cl.cleora_iterate(G, -1)
+    assert e.value.code == cl.EUSAGE
+    with pytest.raises(cl.CleoraError) as e:
+        cl.cleora_fetch(G, 0, 3)
+    assert e.value.code == cl.EUSAGE
+    cl.cleora_iterate(G, 0)
+    assert cl.cleora_info(G)["iterations"] == 0
+    G.close()
+
+
+def test_info_and_stats(cl):
+    g = gen.config("c2")
+    G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0, timing=True)
+    info = cl.cleora_info(G)
+    assert info["n_nodes"] == g.n and info["nnz"] == 2 * g.n_edges
+    deg = np.bincount(np.concatenate([g.src, g.dst]), minlength=g.n)
+    assert info["zero_rows"] == int((deg == 0).sum()) and info["max_degree"] == int(deg.max())
+    cl.cleora_init(G, 128, 0)
+    cl.cleora_iterate(G, 3)
+    st = cl.cleora_stats(G, reset=True)
+    assert st["spmm_launches"] == 3 and st["spmm_ms_total"] > 0
+    assert cl.cleora_stats(G)["spmm_launches"] == 0
+    G.close()
