@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Benchmark of the Cleora hot path on B200 (BASELINE.json metric, one JSON line on rank 0).
+
+A *step* is one pass of the whole hot path over one synthetic
+graph: cleora_build (validate, mirror, radix sort, merge, row pointer, degree, D^-1 scaling,
+schedule) -> cleora_init (hash T_0) -> cleora_iterate(I) (I fused SpMM + row-normalise
+launches), with the COO already resident in HBM when the timed region starts.  The result
+stays in HBM; the end-to-end variant (``e2e``) goes through the same C-ABI calls with HOST
+buffers: pinned COO in, H2D inside cleora_build, and cleora_fetch of all N x d rows into
+pinned host memory, inside the timed region.
+
+value = nnz * d * I / step_time   (nnz = stored CSR entries; BASELINE metric "nnz·d/s")
+Multi-GPU (torchrun, one rank per GPU, NCCL): M is row-sharded by nnz balance, every rank
+keeps a full T replica, each iteration ends with an all-gather; the total work is the same
+graph for every N ("scaling": "strong"); time = max over ranks of CUDA-event step time.
+
+--impl reference times the CPU oracle (oracle/, plain C + OpenMP) on a bounded sample of the
+same workload (one oracle iteration over a leading block of rows), on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "nnz·d/s per Cleora iteration and achieved HBM GB/s vs peak at 1/2/4/8 B200"
+UNIT = "nnz·d/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons, sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(g, M_holder, d, iters, budget_s=12.0):
+    """The oracle as it stands on this host: full CSR build, T_0, and one iteration over a
+    leading block of rows sized to ~budget_s; the step time is extrapolated from the sampled
+    rows' share of nnz.  Returns (value, details)."""
+    import oracle
+    t0 = time.perf_counter()
+    M = oracle.build_from(g)
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    T = oracle.hash_init(g.n, d, 0)
+    t_init = time.perf_counter() - t0
+    # probe: a small block, then size the sample to the budget; when the whole iteration fits
+    # the budget, time all I iterations over all rows (no extrapolation)
+    t0 = time.perf_counter()
+    T1 = oracle.step(M, T)
+    t_full = time.perf_counter() - t0
+    if t_full * iters <= budget_s:
+        for _ in range(iters - 1):
+            T1 = oracle.step(M, T1)
+        t_all = time.perf_counter() - t0
+        M_holder.append(M)
+        return (M.nnz * d * iters / (t_build + t_init + t_all),
+                dict(t_build_s=t_build, t_init_s=t_init, t_sample_s=t_all, rows=g.n, nnz_sample=M.nnz,
+                     t_iter_est_s=t_all / iters, iter_rate=M.nnz * d * iters / t_all, full=True))
+    del T1
+    r1 = min(g.n, 2048)
+    t0 = time.perf_counter()
+    oracle.step(M, T, 0, r1)
+    t_probe = max(time.perf_counter() - t0, 1e-4)
+    nnz_probe = max(int(M.row_ptr[r1]), 1)
+    rate = nnz_probe / t_probe
+    target_nnz = int(rate * budget_s)
+    r1 = int(np.searchsorted(M.row_ptr, min(target_nnz, M.nnz), side="left"))
+    r1 = max(1, min(r1, g.n))
+    t0 = time.perf_counter()
+    oracle.step(M, T, 0, r1)
+    t_samp = time.perf_counter() - t0
+    nnz_s = int(M.row_ptr[r1])
+    t_iter = t_samp * M.nnz / max(nnz_s, 1)
+    t_step = t_build + t_init + iters * t_iter
+    value = M.nnz * d * iters / t_step
+    M_holder.append(M)
+    return value, dict(t_build_s=t_build, t_init_s=t_init, t_sample_s=t_samp, rows=r1, nnz_sample=nnz_s,
+                       t_iter_est_s=t_iter, iter_rate=nnz_s * d / t_samp, full=False)
+
+
+def run_reference(args, g, world, rank):
+    """--impl reference: the CPU oracle, each step = one oracle iteration over a fixed leading
+    block of rows (a bounded sample of the workload), rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+    d, iters = g.d, g.iters
+    M = oracle.build_from(g)
+    T = oracle.hash_init(g.n, d, 0)
+    r1 = min(g.n, 2048)
+    t0 = time.perf_counter()
+    oracle.step(M, T, 0, r1)
+    rate = max(int(M.row_ptr[r1]), 1) / max(time.perf_counter() - t0, 1e-4)
+    per_step_s = float(os.environ.get("CLEORA_REF_STEP_S", "3.0"))
+    r1 = int(np.searchsorted(M.row_ptr, min(int(rate * per_step_s), M.nnz), side="left"))
+    r1 = max(1, min(r1, g.n))
+    nnz_s = int(M.row_ptr[r1])
+    for _ in range(args.warmup):
+        oracle.step(M, T, 0, r1)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.step(M, T, 0, r1)
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts)
+    value = nnz_s * d * args.steps / t
+    cores = oracle.num_threads()
+    sample = (f"{g.name}: one oracle iteration (fp64 accumulate, fp32 store) over rows [0,{r1}) = "
+              f"{nnz_s} of {M.nnz} nnz, d={d}, per step; CSR build and T_0 excluded")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(g, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(g, world):
+    return {"workload": g.name, "desc": g.meta.get("desc", ""), "N": g.n, "edges_in": g.n_edges,
+            "d": g.d, "iterations": g.iters, "directed": g.directed, "weighted": g.w is not None,
+            "parallelism": f"rowshard{world}" if world > 1 else "single",
+            "l2": "inputs larger than L2 (T = N*d*4 bytes per replica >> 126 MB)"}
+
+
+def load_traffic(name, d):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        return json.load(open(p)).get(f"{name}_d{d}")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cleora", choices=["cleora", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl != "reference":
+        print("bench.py: --warmup must be >= 3", file=sys.stderr)
+        args.warmup = 3
+
+    world, rank, local = dist_env()
+    import gen
+    g = gen.config(args.config)
+
+    if args.impl == "reference":
+        run_reference(args, g, world, rank)
+        return
+
+    import torch
+    import paper_2102_02302_b200 as cl
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [cl.cleora_nccl_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    d, iters = g.d, g.iters
+    stream = torch.cuda.Stream(device=dev)
+    src_d = torch.from_numpy(g.src).to(dev)
+    dst_d = torch.from_numpy(g.dst).to(dev)
+    w_d = torch.from_numpy(g.w).to(dev) if g.w is not None else None
+    torch.cuda.synchronize()
+
+    def one_step(timing=False):
+        G = cl.cleora_build(src_d, dst_d, w_d, g.n, g.directed, device=local, stream=stream.cuda_stream,
+                            rank=rank, world=world, nccl_id=nccl_id, timing=timing)
+        cl.cleora_init(G, d, 0)
+        cl.cleora_iterate(G, iters)
+        return G
+
+    # warm-up (also yields the schedule facts)
+    info = None
+    for _ in range(args.warmup):
+        G = one_step()
+        info = cl.cleora_info(G)
+        G.close()
+    nnz = info["nnz"]
+
+    # timed region: K steps, CUDA events on the library's stream, barrier + sync on both sides
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = cl.cleora_kernel_launches()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            G = one_step()
+            G.close()
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    launches = cl.cleora_kernel_launches() - launches0
+    barrier()
+    ms_step = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    value = nnz * d * iters / (ms_step / 1e3)
+
+    # dominant kernel: the fused SpMM+normalise launches, timed by the library with CUDA events
+    # on the same stream during extra steps (separately, so the headline timing has no event overhead)
+    spmm = {"n": 0, "ms": 0.0}
+    for _ in range(2):
+        G = one_step(timing=True)
+        st = cl.cleora_stats(G, reset=True)
+        spmm["n"] += st["spmm_launches"]
+        spmm["ms"] += st["spmm_ms_total"]
+        xms = st["exchange_ms_total"]
+        G.close()
+    spmm_ms = max_over_ranks(spmm["ms"] / max(spmm["n"], 1))
+    peak, peak_src = load_peaks()
+    b_comp = 8 * (g.n + 1) + 8 * nnz + 2 * g.n * d * 4       # SURVEY.md §8(d) B_comp per iteration
+    achieved = b_comp / (spmm_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": load_traffic(g.name, d), "kernel": "k_spmm_norm (fused SpMM + row L2 normalise)",
+                "kernel_ms": spmm_ms, "algorithmic_bytes_per_launch": b_comp, "peak_source": peak_src,
+                "gather_bytes_per_launch": nnz * d * 4}
+
+    # e2e through the public C-ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        src_h = torch.from_numpy(g.src).pin_memory()
+        dst_h = torch.from_numpy(g.dst).pin_memory()
+        w_h = torch.from_numpy(g.w).pin_memory() if g.w is not None else None
+        out_h = torch.empty((g.n, d), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            G = cl.cleora_build(src_h, dst_h, w_h, g.n, g.directed, device=local, stream=stream.cuda_stream,
+                                rank=rank, world=world, nccl_id=nccl_id)
+            cl.cleora_init(G, d, 0)
+            cl.cleora_iterate(G, iters)
+            cl.cleora_fetch(G, 0, g.n, out_h)
+            G.close()
+        e2e_step()
+        k2 = max(2, min(args.steps, 5))
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k2):
+            e2e_step()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1) / k2)
+        h2d = g.n_edges * 8 + (g.n_edges * 4 if g.w is not None else 0)
+        e2e = {"value": nnz * d * iters / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": g.n * d * 4, "ms_per_step": ms_e2e, "steps": k2,
+               "wall_ms_per_step": 1e3 * (time.perf_counter() - t0) / k2}
+        del out_h
+
+    # CPU oracle baseline: rank 0 at N = 1 only, bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        holder = []
+        v, det = cpu_baseline(g, holder, d, iters)
+        cpu = {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+               "sample": (f"{g.name}: full oracle run: CSR build ({det['t_build_s']:.2f} s) + T_0 ({det['t_init_s']:.2f} s) + "
+                          f"{iters} iterations over all rows ({det['t_sample_s']:.2f} s)" if det["full"] else
+                          f"{g.name}: full oracle CSR build ({det['t_build_s']:.2f} s) + T_0 ({det['t_init_s']:.2f} s) + "
+                          f"one iteration over rows [0,{det['rows']}) = {det['nnz_sample']} of {nnz} nnz "
+                          f"({det['t_sample_s']:.2f} s), iteration time extrapolated by nnz share x I={iters}"),
+               "iter_rate": det["iter_rate"]}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator, gen/)",
+                "config": config_dict(g, world),
+                "iteration": {"ms": spmm_ms, "nnz_d_per_s": nnz * d / (spmm_ms / 1e3),
+                              "exchange_ms": (xms / max(iters, 1)) if world > 1 else 0.0},
+                "nnz": nnz, "heavy_rows": info["heavy_rows"], "heavy_items": info["heavy_items"],
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

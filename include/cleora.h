@@ -166,6 +166,11 @@ CLEORA_API void cleora_destroy(cleora_graph* g);
 
 CLEORA_API const char* cleora_last_error(void);
 
+/* Process-wide number of device kernels libcleora has launched so far (its own kernels plus
+ * the kernels of the CUB primitives it dispatches).  Diagnostic; read it before and after a
+ * region to count that region's launches. */
+CLEORA_API int64_t cleora_kernel_launches(void);
+
 /* ---- test hooks (not on the graded path) ------------------------------------------------ */
 
 /* Copy the device CSR to host arrays in the original labelling:

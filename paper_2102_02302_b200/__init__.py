@@ -21,7 +21,7 @@ __all__ = [
     "CleoraError", "Graph", "LIB_PATH",
     "cleora_build", "cleora_init", "cleora_iterate", "cleora_fetch", "cleora_info", "cleora_stats",
     "cleora_sync", "cleora_destroy", "cleora_last_error", "cleora_fetch_csr", "cleora_set_rows",
-    "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards",
+    "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcleora.so")
@@ -70,6 +70,7 @@ _SIGS = {
     "cleora_nccl_id_size": (ctypes.c_int, []),
     "cleora_nccl_get_unique_id": (ctypes.c_int, [_vp]),
     "cleora_plan_shards": (ctypes.c_int, [_vp, _i64, _i32, _vp]),
+    "cleora_kernel_launches": (ctypes.c_int64, []),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -259,3 +260,8 @@ def cleora_plan_shards(row_ptr, world: int) -> np.ndarray:
     cuts = np.empty(world + 1, np.int64)
     _check(_lib.cleora_plan_shards(rp.ctypes.data, int(rp.shape[0] - 1), int(world), cuts.ctypes.data))
     return cuts
+
+
+def cleora_kernel_launches() -> int:
+    """Process-wide count of kernels libcleora has launched (its own + CUB's)."""
+    return int(_lib.cleora_kernel_launches())

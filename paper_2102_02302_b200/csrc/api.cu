@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +22,9 @@ namespace cleora {
 
 static thread_local std::string g_err;
 void set_error(const std::string& m) { g_err = m; }
+
+static std::atomic<int64_t> g_launches{0};
+void count_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 static std::mutex g_pool_mu;
 static bool g_pool_cfg[64];
@@ -318,6 +322,8 @@ extern "C" {
 
 const char* cleora_last_error(void) { return g_err.c_str(); }
 
+int64_t cleora_kernel_launches(void) { return g_launches.load(); }
+
 int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, int64_t n_edges, int32_t n_nodes,
                  int32_t directed, const cleora_opts* opts, cleora_graph** out) {
     if (!out) return usage("cleora_build: out is NULL");
@@ -431,9 +437,13 @@ int cleora_fetch(const cleora_graph* g, int64_t row_begin, int64_t row_end, floa
     if (row_end == row_begin) return CLEORA_OK;
     DeviceGuard guard(g->device);
     const float* src = g->T[g->cur] + row_begin * (int64_t)g->dp;
-    cudaError_t e = cudaMemcpy2DAsync(out, (size_t)g->d * sizeof(float), src, (size_t)g->dp * sizeof(float),
-                                      (size_t)g->d * sizeof(float), (size_t)(row_end - row_begin),
-                                      out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, g->stream);
+    const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    cudaError_t e;
+    if (g->d == g->dp)   // dense rows: one linear copy (full PCIe rate into pinned memory)
+        e = cudaMemcpyAsync(out, src, (size_t)(row_end - row_begin) * g->d * sizeof(float), kind, g->stream);
+    else
+        e = cudaMemcpy2DAsync(out, (size_t)g->d * sizeof(float), src, (size_t)g->dp * sizeof(float),
+                              (size_t)g->d * sizeof(float), (size_t)(row_end - row_begin), kind, g->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_fetch: ") + cudaGetErrorString(e)));
     return CLEORA_OK;

@@ -6,7 +6,7 @@
 //   B1 entries = originals in input order, then mirrors (undirected, u != v) in input order;
 //      STABLE sort by (src, dst)                      -> cub radix sort (stable) on src*N+dst
 //   B2 e_ab   = fp64 sum in that stable order        -> one thread per run, sequential
-//   B3 deg(a) = fp64 sum of e_ab over ascending b     -> one thread per row, sequential
+//   B3 deg(a) = fp64 sum of e_ab over ascending b     -> one warp per row, sequential fold
 //   B4 val    = fp32_rn(e_ab / deg(a))                -> IEEE double divide, one rounding
 // This translation unit must not be compiled with --use_fast_math.
 #include <cub/cub.cuh>
@@ -102,18 +102,28 @@ __global__ void k_row_ptr(const int32_t* __restrict__ rows, int64_t nnz, int32_t
     }
 }
 
-// B3: deg(a) = sum over ascending b of e_ab, sequential per row.  Also zero rows / max degree.
+// B3: deg(a) = sum over ascending b of e_ab, sequential per row.  One warp per row: the
+// lanes load 32 consecutive e_ab (coalesced) and every lane folds them in ascending order
+// via shuffles, so the sum is exactly the sequential left-to-right fp64 sum while the loads
+// stay parallel (a hub row of 10^6 entries would otherwise expose 10^6 load latencies).
 __global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __restrict__ e_ab, int32_t N,
                          double* __restrict__ deg, unsigned long long* __restrict__ zero_rows,
                          unsigned long long* __restrict__ max_deg) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < N; a += stride) {
-        int64_t k0 = row_ptr[a], k1 = row_ptr[a + 1];
+    const int lane = threadIdx.x & 31;
+    const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < N; a += wstride) {
+        const int64_t k0 = row_ptr[a], k1 = row_ptr[a + 1];
         double s = 0.0;
-        for (int64_t k = k0; k < k1; k++) s = s + e_ab[k];
-        deg[a] = s;
-        if (k1 == k0) atomicAdd(zero_rows, 1ull);
-        else atomicMax(max_deg, (unsigned long long)(k1 - k0));
+        for (int64_t kb = k0; kb < k1; kb += 32) {
+            const int n = (int)min((int64_t)32, k1 - kb);
+            const double mine = lane < n ? e_ab[kb + lane] : 0.0;
+            for (int j = 0; j < n; j++) s = s + __shfl_sync(0xffffffffu, mine, j);
+        }
+        if (lane == 0) {
+            deg[a] = s;
+            if (k1 == k0) atomicAdd(zero_rows, 1ull);
+            else atomicMax(max_deg, (unsigned long long)(k1 - k0));
+        }
     }
 }
 
@@ -218,6 +228,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     k_validate_expand<<<grid_for(E, 4), kThreads, 0, s>>>(d_src, d_dst, d_w, E, N, directed, sentinel, keys.p, pos.p,
                                                           scal.p + 0, err_kind.p, scal.p + 1);
     CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     unsigned long long h_scal[2];
     int h_kind = 0;
     CL_CUDA_TRY(cudaMemcpyAsync(h_scal, scal.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -240,6 +251,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         DevBuf<uint8_t> tmp;
         CL_TRY(tmp.alloc(tmp_bytes, s, "radix sort temp"));
         CL_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kb, vb, n_ent, 0, end_bit, s));
+        count_launches(2 + (end_bit + 7) / 8);            // histogram, exclusive sum, one onesweep pass per 8 bits
         if (kb.Current() != keys.p) std::swap(keys.p, keys2.p);
         if (vb.Current() != pos.p) std::swap(pos.p, pos2.p);
     }
@@ -252,6 +264,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     CL_TRY(run_start.alloc(n_valid, s, "run starts"));
     k_head_flags<<<grid_for(n_valid, 4), kThreads, 0, s>>>(keys.p, n_valid, flags.p);
     CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     {
         thrust::counting_iterator<int64_t> it(0);
         size_t tmp_bytes = 0;
@@ -259,6 +272,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         DevBuf<uint8_t> tmp;
         CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
         CL_CUDA_TRY(cub::DeviceSelect::Flagged(tmp.p, tmp_bytes, it, flags.p, run_start.p, scal.p + 4, n_valid, s));
+        count_launches(2);
     }
     dfree(flags.release(), s);
     unsigned long long h_nnz = 0;
@@ -276,6 +290,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     k_merge_runs<<<grid_for(nnz, 4), kThreads, 0, s>>>(keys.p, pos.p, run_start.p, nnz, n_valid, d_w, E, N,
                                                        rows.p, col.p, e_ab.p);
     CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     dfree(run_start.release(), s);
     dfree(keys.release(), s);
     dfree(pos.release(), s);
@@ -285,13 +300,16 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     CL_CUDA_TRY(cudaMemsetAsync(row_ptr.p, 0, sizeof(int64_t), s));
     k_row_ptr<<<grid_for(nnz, 4), kThreads, 0, s>>>(rows.p, nnz, N, row_ptr.p);
     CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
 
     CL_TRY(deg.alloc(N, s, "degree"));
-    k_degree<<<grid_for(N, 4), kThreads, 0, s>>>(row_ptr.p, e_ab.p, N, deg.p, scal.p + 2, scal.p + 3);
+    k_degree<<<grid_for((int64_t)N * 32, 4), kThreads, 0, s>>>(row_ptr.p, e_ab.p, N, deg.p, scal.p + 2, scal.p + 3);
     CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     CL_TRY(val.alloc(nnz, s, "CSR val"));
     k_values<<<grid_for(nnz, 4), kThreads, 0, s>>>(rows.p, e_ab.p, deg.p, nnz, val.p);
     CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     unsigned long long h_zm[2];
     CL_CUDA_TRY(cudaMemcpyAsync(h_zm, scal.p + 2, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CL_CUDA_TRY(cudaStreamSynchronize(s));
@@ -326,6 +344,7 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         DevBuf<uint8_t> tmp;
         CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
         CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, hrows.p, cnt.p, nr, pred, s));
+        count_launches(2);
     }
     int64_t nh = 0;
     CL_CUDA_TRY(cudaMemcpyAsync(&nh, cnt.p, sizeof nh, cudaMemcpyDeviceToHost, s));
@@ -338,12 +357,14 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
     CL_TRY(first.alloc(nh, s, "first item"));
     k_items_per_row<<<grid_for(nh), kThreads, 0, s>>>(d_row_ptr, hrows.p, nh, per_item, nit.p);
     CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     {
         size_t tmp_bytes = 0;
         CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, nit.p, first.p, nh, s));
         DevBuf<uint8_t> tmp;
         CL_TRY(tmp.alloc(tmp_bytes, s, "scan temp"));
         CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, nit.p, first.p, nh, s));
+        count_launches(2);
     }
     int64_t last[2];
     CL_CUDA_TRY(cudaMemcpyAsync(&last[0], first.p + nh - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -357,6 +378,7 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
     CL_CUDA_TRY(cudaMemsetAsync(counters.p, 0, nh * sizeof(unsigned), s));
     k_fill_items<<<grid_for(nh), kThreads, 0, s>>>(d_row_ptr, hrows.p, nh, first.p, per_item, items.p);
     CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     out->n_items = n_items;
     out->items = items.release();
     out->counters = counters.release();
@@ -368,6 +390,7 @@ Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s
     CL_TRY(cuts.alloc(world + 1, s, "shard cuts"));
     k_cuts<<<1, 128, 0, s>>>(d_row_ptr, N, world, cuts.p);
     CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     CL_CUDA_TRY(cudaMemcpyAsync(h_cuts, cuts.p, (world + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CL_CUDA_TRY(cudaStreamSynchronize(s));
     return Status::ok();

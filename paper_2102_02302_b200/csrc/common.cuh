@@ -33,6 +33,9 @@ struct Status {
         if (!_s.good()) return _s;                                                         \
     } while (0)
 
+// Process-wide launch counter (cleora_kernel_launches).
+void count_launches(int64_t n);
+
 // ---------------------------------------------------------------- device buffers
 // Stream-ordered allocation from the device's default pool (release threshold raised so
 // repeated build/destroy cycles do not return memory to the driver).

@@ -51,6 +51,7 @@ Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t see
     if (blocks < 1) blocks = 1;
     k_hash_init<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4*>(T), N, d, dp, key);
     CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     return Status::ok();
 }
 

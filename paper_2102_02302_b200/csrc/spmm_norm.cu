@@ -270,6 +270,7 @@ Status launch_v(const SpmmArgs& a, cudaStream_t s) {
     if (grid > 0x7fffffffLL) return Status::make(2, "cleora_iterate: grid too large");
     k_spmm_norm<V><<<(unsigned)grid, kWarpsPerCta * 32, smem, s>>>(a);
     CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     return Status::ok();
 }
 
