@@ -399,6 +399,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
         a.n_items = g->sched.n_items;
         a.partials = g->partials;
         a.counters = g->sched.counters;
+        a.work = g->sched.work;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (g->timing) {
             e0 = get_event(g);
@@ -542,6 +543,7 @@ void cleora_destroy(cleora_graph* g) {
         dfree(g->deg, g->stream);
         dfree(g->sched.items, g->stream);
         dfree(g->sched.counters, g->stream);
+        dfree(g->sched.work, g->stream);
         cudaStreamSynchronize(g->stream);
     }
     for (auto& p : g->ev_spmm) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }

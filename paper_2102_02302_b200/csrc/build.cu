@@ -332,6 +332,12 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
     out->n_items = 0;
     out->items = nullptr;
     out->counters = nullptr;
+    {
+        DevBuf<unsigned> work;
+        CL_TRY(work.alloc(4, s, "work tickets"));
+        CL_CUDA_TRY(cudaMemsetAsync(work.p, 0, 4 * sizeof(unsigned), s));
+        out->work = work.release();
+    }
     if (nr <= 0) return Status::ok();
     DevBuf<int64_t> hrows, cnt;
     CL_TRY(hrows.alloc(nr, s, "heavy rows"));

@@ -68,6 +68,7 @@ struct SpmmArgs {
     int64_t n_items;
     float* partials;        // n_items * dp floats
     unsigned* counters;     // one per heavy row, 0 between launches
+    unsigned* work;         // 3 work tickets of the persistent kernel, 0 between launches
 };
 
 // build.cu
@@ -86,6 +87,7 @@ struct Schedule {
     int64_t n_heavy_rows = 0, n_items = 0;
     HeavyItem* items = nullptr;
     unsigned* counters = nullptr;
+    unsigned* work = nullptr;   // [4] persistent-kernel tickets
 };
 Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int heavy_thresh,
                       cudaStream_t s, Schedule* out);

@@ -69,7 +69,7 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
 template <int V>
 __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, int64_t k0, int64_t k1, int cbase, int lane,
                                                 float4 (&acc)[V]) {
-    constexpr int U = (V >= 8) ? 1 : 8 / V;      // neighbours per batch: U*V 16-byte loads in flight
+    constexpr int U = (16 / V > 8) ? 8 : 16 / V;  // neighbours per batch: U*V 16-byte loads in flight
     const int dp = a.dp;
     bool ok[V];
 #pragma unroll
@@ -238,37 +238,74 @@ __device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* 
     if (t == 0) a.counters[it.hrow] = 0u;         // ready for the next launch
 }
 
+// Persistent kernel: one wave of CTAs (SM count x resident CTAs per SM).  Work is handed out
+// dynamically through global tickets so that no warp waits for another: CTAs first take heavy
+// items one at a time (a.work[0]); then every warp takes chunks of kChunk consecutive light rows
+// (a.work[1]).  The last warp to finish resets the tickets (a.work[2] counts finished warps), so
+// the counters are 0 again at the next launch.  Which warp computes a row never changes its
+// arithmetic, so results stay bitwise deterministic.
+constexpr int kChunk = 16;
+
 template <int V>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_norm(const SpmmArgs a) {
     extern __shared__ float4 red[];
     __shared__ double scratch[kWarpsPerCta];
     __shared__ int flag;
-    const int64_t b = blockIdx.x;
-    if (b < a.n_items) {
-        heavy_item<V>(a, b, red, scratch, &flag);
-        return;
-    }
+    __shared__ unsigned s_item;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t row = a.r0 + (b - a.n_items) * kWarpsPerCta + warp;
-    if (row >= a.r1) return;
-    const int64_t k0 = a.row_ptr[row], k1 = a.row_ptr[row + 1];
-    if (k1 - k0 > a.heavy_thresh) return;
-    light_row<V>(a, row, k0, k1, lane);
+    if (a.n_items > 0) {
+        for (;;) {
+            if (threadIdx.x == 0) s_item = atomicAdd(a.work + 0, 1u);
+            __syncthreads();
+            const int64_t it = s_item;
+            __syncthreads();
+            if (it >= a.n_items) break;
+            heavy_item<V>(a, it, red, scratch, &flag);
+        }
+    }
+    const int64_t nchunks = (a.r1 - a.r0 + kChunk - 1) / kChunk;
+    for (;;) {
+        unsigned c = 0;
+        if (lane == 0) c = atomicAdd(a.work + 1, 1u);
+        c = __shfl_sync(kFull, c, 0);
+        if ((int64_t)c >= nchunks) break;
+        const int64_t rb = a.r0 + (int64_t)c * kChunk;
+        const int64_t re = min(rb + kChunk, a.r1);
+        const int64_t rpl = (lane <= re - rb) ? a.row_ptr[rb + lane] : 0;
+        for (int64_t r = rb; r < re; r++) {
+            const int64_t k0 = __shfl_sync(kFull, rpl, (int)(r - rb));
+            const int64_t k1 = __shfl_sync(kFull, rpl, (int)(r - rb + 1));
+            if (k1 - k0 > a.heavy_thresh) continue;
+            light_row<V>(a, r, k0, k1, lane);
+        }
+    }
+    if (lane == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(a.work + 2, 1u);
+        if (done == gridDim.x * kWarpsPerCta - 1) {
+            a.work[0] = 0u;
+            a.work[1] = 0u;
+            a.work[2] = 0u;
+        }
+    }
 }
 
 template <int V>
 Status launch_v(const SpmmArgs& a, cudaStream_t s) {
     const size_t smem = (size_t)kWarpsPerCta * 32 * V * sizeof(float4);
-    static bool configured = false;
-    if (!configured) {
+    static int blocks_per_sm = 0, sms = 0;
+    if (!blocks_per_sm) {
         CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_norm<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = true;
+        int dev = 0;
+        CL_CUDA_TRY(cudaGetDevice(&dev));
+        CL_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm_norm<V>,
+                                                                  kWarpsPerCta * 32, smem));
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
-    const int64_t light_ctas = (a.r1 - a.r0 + kWarpsPerCta - 1) / kWarpsPerCta;
-    const int64_t grid = a.n_items + (light_ctas > 0 ? light_ctas : 0);
-    if (grid <= 0) return Status::ok();
-    if (grid > 0x7fffffffLL) return Status::make(2, "cleora_iterate: grid too large");
-    k_spmm_norm<V><<<(unsigned)grid, kWarpsPerCta * 32, smem, s>>>(a);
+    if (a.r1 <= a.r0 && a.n_items == 0) return Status::ok();
+    const int grid = sms * blocks_per_sm;                // one persistent wave
+    k_spmm_norm<V><<<grid, kWarpsPerCta * 32, smem, s>>>(a);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     return Status::ok();
