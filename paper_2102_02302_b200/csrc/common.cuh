@@ -96,7 +96,9 @@ Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s
 // init.cu
 Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s);
 
-// spmm_norm.cu
+// spmm_norm.cu (register gathers; any d) and spmm_tma.cu (TMA bulk gathers; dp <= 1024)
 Status launch_spmm_norm(const SpmmArgs& a, cudaStream_t s);
+bool tma_path_supported(int dp);
+Status launch_spmm_tma(const SpmmArgs& a, cudaStream_t s);
 
 }  // namespace cleora

@@ -1,0 +1,368 @@
+// spmm_tma.cu -- one Cleora iteration T_out = normalize_rows(M . T_in) with TMA bulk gathers.
+//
+// Algorithm 1 lines 6-7.  Same schedule and arithmetic as spmm_norm.cu (which
+// remains the path for d > 1024), but the neighbour rows are not loaded through registers:
+// each warp owns a ring of S shared-memory slots, one row of T_in (dp*4 bytes) per slot, filled
+// by 1-D TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx) that lane 0 issues S entries
+// ahead of the consumer.  Bytes in flight are therefore bounded by shared memory (~190 KB per
+// SM) instead of the register file, which is what a latency-bound gather needs; registers only
+// hold the fp32 accumulator (dp/32 floats per lane).
+//
+// Light rows (<= heavy_thresh entries): a warp takes a ticket for kChunk consecutive rows and
+// streams their entries flat through its ring -- the pipeline keeps running across row
+// boundaries, where the finished row is reduced (fp64 sum of squares, warp shuffles), scaled
+// and written with 16-byte streaming stores.  Heavy rows: CTA work items; each warp streams a
+// contiguous sub-range, the 8 partial vectors are combined through shared memory in warp order,
+// and multi-item rows finish in the last CTA (atomic ticket) with an fp64 sum in part order.
+// Each row accumulates its entries in ascending order from 0, exactly as spmm_norm.cu does, so
+// both kernels produce bitwise identical results.
+#include <cstdlib>
+
+#include "common.cuh"
+#include "spmm_common.cuh"
+
+namespace cleora {
+
+namespace {
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(saddr(dst)),
+        "l"(src), "r"(bytes), "r"(saddr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(saddr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+constexpr int kChunk = 31;    // rows per light ticket: their 32 row pointers fit one register per lane
+
+struct Ring {
+    float4* buf;       // S slots of slot_f4 float4
+    uint64_t* bar;     // S mbarriers (arrival count 1: lane 0's arrive.expect_tx)
+    int S;
+    int slot_f4;
+    uint32_t bytes;    // dp * 4
+    int cs;            // next slot to consume
+    uint32_t ph;       // parity bit of each slot
+};
+
+__device__ __forceinline__ void ring_issue(const SpmmArgs& a, Ring& r, int slot, int32_t c, int lane) {
+    if (lane == 0) {
+        mbar_expect_tx(r.bar + slot, r.bytes);
+        bulk_g2s(r.buf + (size_t)slot * r.slot_f4, a.T_in + (int64_t)c * a.dp, r.bytes, r.bar + slot);
+    }
+}
+
+template <int V, bool FULL>
+__device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, float4 (&acc)[V], int lane) {
+    const int dp = FULL ? 128 * V : a.dp;
+    double ss = 0.0;
+#pragma unroll
+    for (int v = 0; v < V; v++)
+        if (FULL || 4 * (lane + 32 * v) < dp) ss += sq4(acc[v]);
+    ss = warp_sum(ss);
+    const double inv = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+    float4* out = reinterpret_cast<float4*>(a.T_out + row * (int64_t)dp);
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        const int f = lane + 32 * v;
+        if (FULL || 4 * f < dp) __stcs(out + f, scale4(acc[v], inv));
+        acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// Stream CSR entries [E0, E1) through the warp's ring into acc.  ROWS: the entries belong to
+// rows [ra, rz) whose bounds are in rpl (lane i holds row_ptr[rb + i]); rows are finalised at
+// their boundaries (zero rows included).  On return every issued copy has been consumed.
+template <int V, bool FULL, bool ROWS>
+__device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E1, float4 (&acc)[V], int64_t rb,
+                               int64_t rpl, int64_t ra, int64_t rz, int lane) {
+    const int dp = FULL ? 128 * V : a.dp;
+    int64_t row = ra;
+    int64_t kend = ROWS ? __shfl_sync(kFull, rpl, (int)(ra - rb + 1)) : E1;
+    int32_t mc0 = 0, mc1 = 0;
+    float mw0 = 0.f, mw1 = 0.f;
+    if (E0 + lane < E1) {
+        mc0 = __ldg(a.col + E0 + lane);
+        mw0 = __ldg(a.val + E0 + lane);
+    }
+    if (E0 + 32 + lane < E1) {
+        mc1 = __ldg(a.col + E0 + 32 + lane);
+        mw1 = __ldg(a.val + E0 + 32 + lane);
+    }
+    // prologue: the first min(S, n) entries
+    {
+        const int pro = (int)min((int64_t)r.S, E1 - E0);
+        int sl = r.cs;
+        for (int i = 0; i < pro; i++) {
+            const int32_t c = __shfl_sync(kFull, mc0, i);
+            ring_issue(a, r, sl, c, lane);
+            sl = (sl + 1 == r.S) ? 0 : sl + 1;
+        }
+    }
+    for (int64_t kb = E0; kb < E1; kb += 32) {
+        const int n = (int)min((int64_t)32, E1 - kb);
+        for (int j = 0; j < n; j++) {
+            const int64_t e = kb + j;
+            if (ROWS) {
+                while (e >= kend) {                       // row boundary (warp-uniform)
+                    finalize_row_t<V, FULL>(a, row, acc, lane);
+                    row++;
+                    kend = __shfl_sync(kFull, rpl, (int)(row - rb + 1));
+                }
+            }
+            const float w = __shfl_sync(kFull, mw0, j);
+            const int sl = r.cs;
+            mbar_wait(r.bar + sl, (r.ph >> sl) & 1u);
+            r.ph ^= 1u << sl;
+            const float4* src = r.buf + (size_t)sl * r.slot_f4 + lane;
+#pragma unroll
+            for (int v = 0; v < V; v++)
+                if (FULL || 4 * (lane + 32 * v) < dp) fma4(acc[v], w, src[32 * v]);
+            __syncwarp();
+            // refill the slot just consumed with entry e + S (S <= 32, so it is in block 0 or 1)
+            const int jp = j + r.S;
+            const int32_t cp = (jp < 32) ? __shfl_sync(kFull, mc0, jp) : __shfl_sync(kFull, mc1, jp - 32);
+            if (e + r.S < E1) ring_issue(a, r, sl, cp, lane);
+            r.cs = (sl + 1 == r.S) ? 0 : sl + 1;
+        }
+        mc0 = mc1;
+        mw0 = mw1;
+        mc1 = 0;
+        mw1 = 0.f;
+        if (kb + 64 + lane < E1) {
+            mc1 = __ldg(a.col + kb + 64 + lane);
+            mw1 = __ldg(a.val + kb + 64 + lane);
+        }
+    }
+    if (ROWS) {
+        while (row < rz) {                                // last row and trailing zero rows
+            finalize_row_t<V, FULL>(a, row, acc, lane);
+            row++;
+        }
+    }
+}
+
+template <int V, bool FULL>
+__device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* smem, int ring_f4, double* scratch,
+                             int* flag) {
+    const HeavyItem it = a.items[idx];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
+    const int dp = FULL ? 128 * V : a.dp;
+    const int nq = dp / 4;
+    const int64_t len = it.k1 - it.k0;
+    const int64_t sub = (len + kWarpsPerCta - 1) / kWarpsPerCta;
+    const int64_t wk0 = min(it.k0 + warp * sub, it.k1), wk1 = min(wk0 + sub, it.k1);
+    float4 acc[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    stream_entries<V, FULL, false>(a, r, wk0, wk1, acc, 0, 0, 0, 0, lane);
+    // this warp's partial vector -> slot 0 of its ring (drained), combined in warp order
+    float4* red = r.buf;
+#pragma unroll
+    for (int v = 0; v < V; v++)
+        if (FULL || 4 * (lane + 32 * v) < dp) red[lane + 32 * v] = acc[v];
+    __syncthreads();
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    double ss = 0.0;
+    if (t < nq) {
+        y = smem[t];
+#pragma unroll
+        for (int w = 1; w < kWarpsPerCta; w++) {
+            const float4 q = smem[(size_t)w * ring_f4 + t];
+            y.x += q.x; y.y += q.y; y.z += q.z; y.w += q.w;
+        }
+        ss = sq4(y);
+    }
+    if (it.nparts == 1) {
+        const double tot = block_sum(ss, scratch);
+        const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+        if (t < nq) __stcs(reinterpret_cast<float4*>(a.T_out + (int64_t)it.row * dp) + t, scale4(y, inv));
+    } else {
+        float4* part = reinterpret_cast<float4*>(a.partials + idx * (int64_t)dp);
+        if (t < nq) part[t] = y;
+        __threadfence();
+        __syncthreads();
+        if (t == 0) {
+            const unsigned prev = atomicAdd(a.counters + it.hrow, 1u);
+            *flag = (prev == (unsigned)it.nparts - 1) ? 1 : 0;
+        }
+        __syncthreads();
+        if (*flag) {
+            __threadfence();
+            const float4* parts = reinterpret_cast<const float4*>(a.partials + (idx - it.part) * (int64_t)dp);
+            double zx = 0, zy = 0, zz = 0, zw = 0;
+            if (t < nq) {
+                for (int q = 0; q < it.nparts; q++) {     // part order: deterministic
+                    const float4 p = __ldcg(parts + (int64_t)q * nq + t);
+                    zx += p.x; zy += p.y; zz += p.z; zw += p.w;
+                }
+            }
+            const double tot = block_sum(zx * zx + zy * zy + zz * zz + zw * zw, scratch);
+            const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+            if (t < nq)
+                __stcs(reinterpret_cast<float4*>(a.T_out + (int64_t)it.row * dp) + t,
+                       make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
+            if (t == 0) a.counters[it.hrow] = 0u;
+        }
+    }
+    __syncthreads();              // red (ring slot 0) is refilled by TMA next: order the generic
+    fence_proxy_async_smem();     // accesses before the async-proxy writes
+}
+
+template <int V, bool FULL>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArgs a, int S) {
+    extern __shared__ __align__(128) float4 smem[];
+    __shared__ double scratch[kWarpsPerCta];
+    __shared__ int flag;
+    __shared__ unsigned s_item;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int dp = FULL ? 128 * V : a.dp;
+    const int slot_f4 = dp / 4;
+    const int ring_f4 = S * slot_f4;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarpsPerCta * ring_f4);
+    Ring r;
+    r.buf = smem + (size_t)warp * ring_f4;
+    r.bar = bars + warp * S;
+    r.S = S;
+    r.slot_f4 = slot_f4;
+    r.bytes = (uint32_t)dp * 4u;
+    r.cs = 0;
+    r.ph = 0u;
+    if (lane == 0)
+        for (int i = 0; i < S; i++) mbar_init(r.bar + i, 1);
+    mbar_fence_init();
+    __syncthreads();
+
+    if (a.n_items > 0) {
+        for (;;) {
+            if (threadIdx.x == 0) s_item = atomicAdd(a.work + 0, 1u);
+            __syncthreads();
+            const int64_t it = s_item;
+            __syncthreads();
+            if (it >= a.n_items) break;
+            heavy_item_t<V, FULL>(a, it, r, smem, ring_f4, scratch, &flag);
+        }
+    }
+    const int64_t nchunks = (a.r1 - a.r0 + kChunk - 1) / kChunk;
+    float4 acc[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (;;) {
+        unsigned c = 0;
+        if (lane == 0) c = atomicAdd(a.work + 1, 1u);
+        c = __shfl_sync(kFull, c, 0);
+        if ((int64_t)c >= nchunks) break;
+        const int64_t rb = a.r0 + (int64_t)c * kChunk;
+        const int64_t re = min(rb + kChunk, a.r1);
+        const int64_t rpl = (lane <= re - rb) ? a.row_ptr[rb + lane] : 0;
+        int64_t row = rb;
+        while (row < re) {   // segments of consecutive light rows; heavy rows are skipped
+            int64_t k0 = __shfl_sync(kFull, rpl, (int)(row - rb));
+            int64_t k1 = __shfl_sync(kFull, rpl, (int)(row - rb + 1));
+            if (k1 - k0 > a.heavy_thresh) {
+                row++;
+                continue;
+            }
+            const int64_t E0 = k0;
+            int64_t z = row + 1;
+            while (z < re) {
+                k0 = k1;
+                k1 = __shfl_sync(kFull, rpl, (int)(z - rb + 1));
+                if (k1 - k0 > a.heavy_thresh) break;
+                z++;
+            }
+            const int64_t E1 = __shfl_sync(kFull, rpl, (int)(z - rb));
+            stream_entries<V, FULL, true>(a, r, E0, E1, acc, rb, rpl, row, z, lane);
+            row = z;
+        }
+    }
+    if (lane == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(a.work + 2, 1u);
+        if (done == gridDim.x * kWarpsPerCta - 1) {
+            a.work[0] = 0u;
+            a.work[1] = 0u;
+            a.work[2] = 0u;
+        }
+    }
+}
+
+struct TmaCfg {
+    int blocks_per_sm = 0, sms = 0, S = 0;
+    size_t smem = 0;
+};
+
+template <int V, bool FULL>
+Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
+    static TmaCfg cfg[2];   // [0]: default, keyed by dp below
+    static int cfg_dp = -1;
+    TmaCfg& c = cfg[0];
+    if (cfg_dp != a.dp) {
+        const int slot = a.dp * 4;
+        // per-CTA ring budget ~96 KB so that two CTAs (16 warps) share an SM
+        int S = (96 * 1024) / (kWarpsPerCta * slot);
+        if (S > 16) S = 16;
+        if (S < 2) S = 2;
+        c.S = S;
+        c.smem = (size_t)kWarpsPerCta * S * slot + (size_t)kWarpsPerCta * S * sizeof(uint64_t);
+        CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_tma<V, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+        int dev = 0;
+        CL_CUDA_TRY(cudaGetDevice(&dev));
+        CL_CUDA_TRY(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
+        CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.blocks_per_sm, k_spmm_tma<V, FULL>,
+                                                                  kWarpsPerCta * 32, c.smem));
+        if (c.blocks_per_sm < 1) c.blocks_per_sm = 1;
+        cfg_dp = a.dp;
+    }
+    if (a.r1 <= a.r0 && a.n_items == 0) return Status::ok();
+    k_spmm_tma<V, FULL><<<c.sms * c.blocks_per_sm, kWarpsPerCta * 32, c.smem, s>>>(a, c.S);
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    return Status::ok();
+}
+
+}  // namespace
+
+bool tma_path_supported(int dp) { return dp <= 1024 && getenv("CLEORA_NO_TMA") == nullptr; }
+
+Status launch_spmm_tma(const SpmmArgs& a, cudaStream_t s) {
+    if (a.dp == 1024) return launch_tma_v<8, true>(a, s);
+    if (a.dp == 512) return launch_tma_v<4, true>(a, s);
+    if (a.dp == 256) return launch_tma_v<2, true>(a, s);
+    if (a.dp == 128) return launch_tma_v<1, true>(a, s);
+    if (a.dp < 128) return launch_tma_v<1, false>(a, s);
+    if (a.dp < 256) return launch_tma_v<2, false>(a, s);
+    if (a.dp < 512) return launch_tma_v<4, false>(a, s);
+    return launch_tma_v<8, false>(a, s);
+}
+
+}  // namespace cleora

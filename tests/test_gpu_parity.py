@@ -238,3 +238,20 @@ def test_info_and_stats(cl):
     assert st["spmm_launches"] == 3 and st["spmm_ms_total"] > 0
     assert cl.cleora_stats(G)["spmm_launches"] == 0
     G.close()
+
+
+@pytest.mark.parametrize("d", [100, 256, 1024])
+def test_tma_and_register_kernels_bitwise_equal(cl, d, monkeypatch):
+    """The TMA-gather kernel (spmm_tma.cu) and the register-gather kernel (spmm_norm.cu) run the
+    same per-row arithmetic in the same order, so their outputs are bitwise identical."""
+    g = gen.chung_lu(30000, 90000, 2.1, 9.5388, 233115.5 * 30000 / 1134890, seed=3)
+    outs = []
+    for no_tma in (False, True):
+        if no_tma:
+            monkeypatch.setenv("CLEORA_NO_TMA", "1")
+        G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0)
+        cl.cleora_init(G, d, 0)
+        cl.cleora_iterate(G, 3)
+        outs.append(cl.cleora_fetch(G))
+        G.close()
+    assert outs[0].tobytes() == outs[1].tobytes()
