@@ -134,6 +134,8 @@ struct cleora_graph {
     int32_t d = 0, dp = 0;
     float* T[2] = {nullptr, nullptr};
     float* partials = nullptr;
+    int32_t* col_tag = nullptr;     // col with the hot bit (TMA path L2 hints), built by cleora_init
+    int64_t n_hot = 0;
     int cur = 0;
     int64_t iters = 0;
     int rank = 0, world = 1;
@@ -215,6 +217,9 @@ void free_T(cleora_graph* g) {
     }
     dfree(g->partials, g->stream);
     g->partials = nullptr;
+    dfree(g->col_tag, g->stream);
+    g->col_tag = nullptr;
+    g->n_hot = 0;
 }
 
 Status exchange(cleora_graph* g, float* buf) {
@@ -374,6 +379,18 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     g->dp = dp;
     g->cur = 0;
     g->iters = 0;
+    if (!g->col_tag && tma_path_supported(dp) && !getenv("CLEORA_NO_HOT") && g->nnz > 0) {
+        // L2 residency hints: tag the columns whose rows are re-read most (highest in-degree) so
+        // that their gathers use an evict_last policy, within a budget of the 126 MB L2
+        const char* e = getenv("CLEORA_HOT_MB");
+        const int64_t budget = (int64_t)(e ? atof(e) : 72.0) * 1024 * 1024;
+        Status s = dalloc((void**)&g->col_tag, (size_t)g->nnz * sizeof(int32_t), g->stream, "hot-tagged col");
+        if (s.good()) s = hot_tag(g->col, g->nnz, g->n, (int64_t)dp * 4, budget, g->stream, g->col_tag, &g->n_hot);
+        if (!s.good()) {
+            free_T(g);
+            return fail(s);
+        }
+    }
     Status s = launch_hash_init(g->T[0], g->n, d, dp, seed, g->stream);
     if (!s.good()) return fail(s);
     return CLEORA_OK;
@@ -388,6 +405,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
         SpmmArgs a;
         a.row_ptr = g->row_ptr;
         a.col = g->col;
+        a.col_tag = nullptr;
         a.val = g->val;
         a.T_in = g->T[g->cur];
         a.T_out = g->T[1 - g->cur];
@@ -399,6 +417,10 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
         a.n_items = g->sched.n_items;
         a.partials = g->partials;
         a.counters = g->sched.counters;
+        a.col_tag = g->col_tag;
+        // with hot rows pinned (power-law graphs) the other gathers are evicted first; without
+        // (e.g. lattices, whose re-reads are local) they keep the normal policy (measured: c2, c4, c3)
+        a.cold_first = getenv("CLEORA_COLD_FIRST") ? atoi(getenv("CLEORA_COLD_FIRST")) : (g->n_hot > 0 ? 1 : 0);
         a.work = g->sched.work;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (g->timing) {

@@ -391,6 +391,68 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
     return Status::ok();
 }
 
+namespace {
+__global__ void k_indegree(const int32_t* __restrict__ col, int64_t nnz, int32_t* __restrict__ indeg) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) atomicAdd(indeg + col[k], 1);
+}
+__global__ void k_indeg_hist(const int32_t* __restrict__ indeg, int32_t N, unsigned long long* __restrict__ hist) {
+    __shared__ unsigned long long h[33];
+    if (threadIdx.x < 33) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < N; v += stride) {
+        const int x = indeg[v];
+        atomicAdd(&h[x > 0 ? 32 - __clz(x) : 0], 1ull);        // bin b >= 1: 2^(b-1) <= x < 2^b
+    }
+    __syncthreads();
+    if (threadIdx.x < 33) atomicAdd(hist + threadIdx.x, h[threadIdx.x]);
+}
+__global__ void k_tag(const int32_t* __restrict__ col, int64_t nnz, const int32_t* __restrict__ indeg, int32_t t,
+                      int32_t* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
+        const int32_t c = col[k];
+        out[k] = indeg[c] >= t ? (int32_t)((uint32_t)c | 0x80000000u) : c;
+    }
+}
+}  // namespace
+
+Status hot_tag(const int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes, cudaStream_t s,
+               int32_t* d_col_tag, int64_t* n_hot) {
+    DevBuf<int32_t> indeg;
+    DevBuf<unsigned long long> hist;
+    CL_TRY(indeg.alloc(N, s, "in-degree"));
+    CL_TRY(hist.alloc(33, s, "in-degree histogram"));
+    CL_CUDA_TRY(cudaMemsetAsync(indeg.p, 0, (size_t)N * 4, s));
+    CL_CUDA_TRY(cudaMemsetAsync(hist.p, 0, 33 * 8, s));
+    k_indegree<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p);
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    k_indeg_hist<<<grid_for(N, 8), kThreads, 0, s>>>(indeg.p, N, hist.p);
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    unsigned long long h[33];
+    CL_CUDA_TRY(cudaMemcpyAsync(h, hist.p, sizeof h, cudaMemcpyDeviceToHost, s));
+    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    // rows with in-degree >= 2^(b-1) are those in bins >= b; take the lowest b that fits the budget
+    int64_t cum = 0;
+    int best = 33;
+    for (int b = 32; b >= 2; b--) {
+        cum += (int64_t)h[b];
+        if (cum * row_bytes > budget_bytes) break;
+        best = b;
+    }
+    int64_t nh = 0;
+    for (int b = best; b <= 32; b++) nh += (int64_t)h[b];
+    *n_hot = nh;
+    const int32_t t = best >= 32 ? INT32_MAX : (int32_t)(1u << (best - 1));
+    k_tag<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p, t, d_col_tag);
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    return Status::ok();
+}
+
 Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts) {
     DevBuf<int64_t> cuts;
     CL_TRY(cuts.alloc(world + 1, s, "shard cuts"));

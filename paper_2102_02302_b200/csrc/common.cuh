@@ -58,6 +58,7 @@ constexpr int kMaxV = 8;            // float4 per lane per column slice (slice =
 struct SpmmArgs {
     const int64_t* row_ptr;
     const int32_t* col;
+    const int32_t* col_tag; // optional: col with bit 31 set for hot columns (TMA path), or NULL
     const float* val;
     const float* T_in;
     float* T_out;
@@ -69,6 +70,7 @@ struct SpmmArgs {
     float* partials;        // n_items * dp floats
     unsigned* counters;     // one per heavy row, 0 between launches
     unsigned* work;         // 3 work tickets of the persistent kernel, 0 between launches
+    int32_t cold_first;     // TMA path: gathers of non-hot rows with evict_first (else evict_normal)
 };
 
 // build.cu
@@ -92,6 +94,12 @@ struct Schedule {
 Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int heavy_thresh,
                       cudaStream_t s, Schedule* out);
 Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts);
+
+// Hot-row tagging for L2 residency hints: col_tag[k] = col[k] | (indeg(col[k]) >= 2^b) << 31,
+// b the smallest power of two such that the hot rows' bytes fit `budget_bytes`.  Returns the
+// number of hot rows in *n_hot (0 => no tagging was useful).
+Status hot_tag(const int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes,
+               cudaStream_t s, int32_t* d_col_tag, int64_t* n_hot);
 
 // init.cu
 Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s);

@@ -50,6 +50,44 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            saddr(dst)),
+        "l"(src), "r"(bytes), "r"(saddr(bar)), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// streamed-once CSR words: no L1 allocation, first out of L2
+__device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p, uint64_t pol) {
+    int32_t x;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(x) : "l"(p), "l"(pol));
+    return x;
+}
+__device__ __forceinline__ float ld_stream_f32(const float* p, uint64_t pol) {
+    float x;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(x) : "l"(p), "l"(pol));
+    return x;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -72,12 +110,18 @@ struct Ring {
     uint32_t bytes;    // dp * 4
     int cs;            // next slot to consume
     uint32_t ph;       // parity bit of each slot
+    uint64_t pol_hot;  // L2 policy for gathers of hot rows (evict_last)
+    uint64_t pol_cold; // ... of all other rows (evict_normal; evict_first with a.cold_first)
+    uint64_t pol_csr;  // streamed-once CSR words (evict_first)
 };
 
+// c: column index, bit 31 set when the row is "hot" (high in-degree, see hot_tag in build.cu):
+// hot rows are gathered with an evict_last L2 policy so the most re-read rows stay resident.
 __device__ __forceinline__ void ring_issue(const SpmmArgs& a, Ring& r, int slot, int32_t c, int lane) {
     if (lane == 0) {
         mbar_expect_tx(r.bar + slot, r.bytes);
-        bulk_g2s(r.buf + (size_t)slot * r.slot_f4, a.T_in + (int64_t)c * a.dp, r.bytes, r.bar + slot);
+        bulk_g2s_hint(r.buf + (size_t)slot * r.slot_f4, a.T_in + (int64_t)(c & 0x7fffffff) * a.dp, r.bytes,
+                      r.bar + slot, c < 0 ? r.pol_hot : r.pol_cold);
     }
 }
 
@@ -108,15 +152,16 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
     const int dp = FULL ? 128 * V : a.dp;
     int64_t row = ra;
     int64_t kend = ROWS ? __shfl_sync(kFull, rpl, (int)(ra - rb + 1)) : E1;
+    const int32_t* colp = a.col_tag ? a.col_tag : a.col;
     int32_t mc0 = 0, mc1 = 0;
     float mw0 = 0.f, mw1 = 0.f;
     if (E0 + lane < E1) {
-        mc0 = __ldg(a.col + E0 + lane);
-        mw0 = __ldg(a.val + E0 + lane);
+        mc0 = ld_stream_i32(colp + E0 + lane, r.pol_csr);
+        mw0 = ld_stream_f32(a.val + E0 + lane, r.pol_csr);
     }
     if (E0 + 32 + lane < E1) {
-        mc1 = __ldg(a.col + E0 + 32 + lane);
-        mw1 = __ldg(a.val + E0 + 32 + lane);
+        mc1 = ld_stream_i32(colp + E0 + 32 + lane, r.pol_csr);
+        mw1 = ld_stream_f32(a.val + E0 + 32 + lane, r.pol_csr);
     }
     // prologue: the first min(S, n) entries
     {
@@ -159,8 +204,8 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
         mc1 = 0;
         mw1 = 0.f;
         if (kb + 64 + lane < E1) {
-            mc1 = __ldg(a.col + kb + 64 + lane);
-            mw1 = __ldg(a.val + kb + 64 + lane);
+            mc1 = ld_stream_i32(colp + kb + 64 + lane, r.pol_csr);
+            mw1 = ld_stream_f32(a.val + kb + 64 + lane, r.pol_csr);
         }
     }
     if (ROWS) {
@@ -257,6 +302,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
     r.bytes = (uint32_t)dp * 4u;
     r.cs = 0;
     r.ph = 0u;
+    r.pol_hot = policy_evict_last();
+    r.pol_cold = a.cold_first ? policy_evict_first() : policy_evict_normal();
+    r.pol_csr = policy_evict_first();
     if (lane == 0)
         for (int i = 0; i < S; i++) mbar_init(r.bar + i, 1);
     mbar_fence_init();
