@@ -23,7 +23,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -46,57 +45,73 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons, sampled every 200 ms during the timed region."""
+    """SM clocks and throttle reasons sampled every 100 ms by a thread through NVML (the library
+    nvidia-smi reads; spawning nvidia-smi itself inside the timed region stalled CUDA calls for
+    tens of ms).  Start it before the warm-up; mark() the timed window; summary() uses only the
+    samples taken inside marked windows."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.proc = None
-        self.lines = []
-
-    def __enter__(self):
+        self.samples = []
+        self.windows = []
+        self._stop = threading.Event()
+        self.ok = False
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            idx = gpu
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                try:
+                    idx = int(vis.split(",")[gpu])
+                except ValueError:
+                    pass
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _reasons(self):
+        f = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            self.nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        return int(f(self.h))
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append((time.perf_counter(), float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)),
+                                     self._reasons()))
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def start(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def stop(self):
+        self._stop.set()
 
-    def __exit__(self, *exc):
-        if self.proc:
-            time.sleep(0.25)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+    def mark(self, t0, t1):
+        self.windows.append((t0, t1))
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in self.lines:
-            parts = [p.strip() for p in l.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        inside = [s for s in self.samples if any(a - 0.05 <= s[0] <= b + 0.05 for a, b in self.windows)]
+        mhz = [s[1] for s in inside]
+        reasons = set()
+        for _, _, r in inside:
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(mhz), "source": "nvml"}
 
 
 def dist_env():
@@ -269,6 +284,7 @@ def main():
         cl.cleora_iterate(G, iters)
         return G
 
+    clk = ClockSampler(local).start()
     # warm-up (also yields the schedule facts)
     info = None
     for _ in range(args.warmup):
@@ -282,13 +298,19 @@ def main():
     barrier()
     torch.cuda.synchronize()
     launches0 = cl.cleora_kernel_launches()
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            G = one_step()
-            G.close()
-        ev1.record(stream)
-        ev1.synchronize()
+    per_step = []
+    t_w0 = time.perf_counter()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        e_a = torch.cuda.Event(enable_timing=True)
+        e_a.record(stream)
+        G = one_step()
+        G.close()
+        per_step.append(e_a)
+    ev1.record(stream)
+    ev1.synchronize()
+    clk.mark(t_w0, time.perf_counter())
+    step_ms = [a.elapsed_time(b) for a, b in zip(per_step, per_step[1:] + [ev1])]
     torch.cuda.synchronize()
     launches = cl.cleora_kernel_launches() - launches0
     barrier()
@@ -340,6 +362,7 @@ def main():
             e2e_step()
         e1.record(stream)
         e1.synchronize()
+        clk.mark(t0, time.perf_counter())
         torch.cuda.synchronize()
         barrier()
         ms_e2e = max_over_ranks(e0.elapsed_time(e1) / k2)
@@ -371,9 +394,11 @@ def main():
                 "iteration": {"ms": spmm_ms, "nnz_d_per_s": nnz * d / (spmm_ms / 1e3),
                               "exchange_ms": (xms / max(iters, 1)) if world > 1 else 0.0},
                 "nnz": nnz, "heavy_rows": info["heavy_rows"], "heavy_items": info["heavy_items"],
+                "step_ms_each": [round(x, 3) for x in step_ms],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches,
                 "clocks": clk.summary()}
+        clk.stop()
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

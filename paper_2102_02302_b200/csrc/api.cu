@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -25,6 +26,17 @@ void set_error(const std::string& m) { g_err = m; }
 
 static std::atomic<int64_t> g_launches{0};
 void count_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void trace(const char* what, cudaStream_t s, bool sync) {
+    static const bool on = getenv("CLEORA_TRACE") != nullptr;
+    if (!on) return;
+    static thread_local std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    if (sync) cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[cleora trace] %-28s %8.3f ms%s\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(), sync ? " (synced)" : "");
+    last = now;
+}
 
 static std::mutex g_pool_mu;
 static bool g_pool_cfg[64];
@@ -284,8 +296,10 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
         ddst = (const int32_t*)bd;
         dw = (const float*)bw;
     }
+    trace("build: inputs staged", g->stream, true);
     BuildOut b;
     Status st = build_csr(dsrc, ddst, dw, E, N, directed, g->stream, &b);
+    trace("build: csr", g->stream, true);
     dfree(bs, g->stream);
     dfree(bd, g->stream);
     dfree(bw, g->stream);
@@ -308,6 +322,7 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
     g->r0 = g->cuts[g->rank];
     g->r1 = g->cuts[g->rank + 1];
     CL_TRY(build_schedule(g->row_ptr, N, g->r0, g->r1, g->heavy_thresh, g->stream, &g->sched));
+    trace("build: schedule", g->stream, true);
     g->bytes += g->sched.n_items * (int64_t)sizeof(HeavyItem) + g->sched.n_heavy_rows * 4;
 
     if (g->world > 1) {

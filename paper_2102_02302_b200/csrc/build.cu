@@ -102,10 +102,11 @@ __global__ void k_row_ptr(const int32_t* __restrict__ rows, int64_t nnz, int32_t
     }
 }
 
-// B3: deg(a) = sum over ascending b of e_ab, sequential per row.  One warp per row: the
-// lanes load 32 consecutive e_ab (coalesced) and every lane folds them in ascending order
-// via shuffles, so the sum is exactly the sequential left-to-right fp64 sum while the loads
-// stay parallel (a hub row of 10^6 entries would otherwise expose 10^6 load latencies).
+// B3: deg(a) = sum over ascending b of e_ab, the sequential left-to-right fp64 sum.  One warp
+// per row.  Fast path: when every e_ab of the row is an integer and the total is below 2^52, every
+// partial sum is exact, so a warp tree reduction returns exactly the sequential result (unit-weight
+// graphs always take it).  Otherwise the lanes load 32 consecutive e_ab (coalesced) and every
+// lane folds them in ascending order via shuffles -- literally the sequential sum.
 __global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __restrict__ e_ab, int32_t N,
                          double* __restrict__ deg, unsigned long long* __restrict__ zero_rows,
                          unsigned long long* __restrict__ max_deg) {
@@ -113,11 +114,23 @@ __global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __re
     const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < N; a += wstride) {
         const int64_t k0 = row_ptr[a], k1 = row_ptr[a + 1];
-        double s = 0.0;
-        for (int64_t kb = k0; kb < k1; kb += 32) {
-            const int n = (int)min((int64_t)32, k1 - kb);
-            const double mine = lane < n ? e_ab[kb + lane] : 0.0;
-            for (int j = 0; j < n; j++) s = s + __shfl_sync(0xffffffffu, mine, j);
+        double part = 0.0;
+        bool integral = true;
+        for (int64_t k = k0 + lane; k < k1; k += 32) {
+            const double x = e_ab[k];
+            integral &= (x == trunc(x));
+            part += x;
+        }
+        double s = part;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (!__all_sync(0xffffffffu, integral) || !(s < 4503599627370496.0)) {
+            s = 0.0;                                   // general case: sequential fold
+            for (int64_t kb = k0; kb < k1; kb += 32) {
+                const int n = (int)min((int64_t)32, k1 - kb);
+                const double mine = lane < n ? e_ab[kb + lane] : 0.0;
+                for (int j = 0; j < n; j++) s = s + __shfl_sync(0xffffffffu, mine, j);
+            }
         }
         if (lane == 0) {
             deg[a] = s;
@@ -241,6 +254,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         return Status::make(3, buf);
     }
     const int64_t n_valid = n_ent - (int64_t)h_scal[1];
+    trace("csr: validate+expand", s, false);
 
     // B1: stable radix sort by (src, dst) over the bits the keys use
     {
@@ -256,6 +270,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         if (vb.Current() != pos.p) std::swap(pos.p, pos2.p);
     }
     dfree(keys2.release(), s);
+    trace("csr: radix sort", s, true);
 
     // B2: run starts of equal keys, merged weights
     DevBuf<uint8_t> flags;
@@ -279,6 +294,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     CL_CUDA_TRY(cudaMemcpyAsync(&h_nnz, scal.p + 4, sizeof h_nnz, cudaMemcpyDeviceToHost, s));
     CL_CUDA_TRY(cudaStreamSynchronize(s));
     const int64_t nnz = (int64_t)h_nnz;
+    trace("csr: run select", s, false);
 
     DevBuf<int32_t> rows, col;
     DevBuf<double> e_ab, deg;
@@ -291,6 +307,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
                                                        rows.p, col.p, e_ab.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
+    trace("csr: merge runs", s, true);
     dfree(run_start.release(), s);
     dfree(keys.release(), s);
     dfree(pos.release(), s);
@@ -302,10 +319,12 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
 
+    trace("csr: row_ptr", s, true);
     CL_TRY(deg.alloc(N, s, "degree"));
     k_degree<<<grid_for((int64_t)N * 32, 4), kThreads, 0, s>>>(row_ptr.p, e_ab.p, N, deg.p, scal.p + 2, scal.p + 3);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
+    trace("csr: degree", s, true);
     CL_TRY(val.alloc(nnz, s, "CSR val"));
     k_values<<<grid_for(nnz, 4), kThreads, 0, s>>>(rows.p, e_ab.p, deg.p, nnz, val.p);
     CL_CUDA_TRY(cudaGetLastError());

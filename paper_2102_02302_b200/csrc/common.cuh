@@ -33,6 +33,9 @@ struct Status {
         if (!_s.good()) return _s;                                                         \
     } while (0)
 
+// Host-side phase trace (stderr) when CLEORA_TRACE is set; `sync` waits for the stream first.
+void trace(const char* what, cudaStream_t s, bool sync);
+
 // Process-wide launch counter (cleora_kernel_launches).
 void count_launches(int64_t n);
 
