@@ -171,6 +171,14 @@ CLEORA_API const char* cleora_last_error(void);
  * region to count that region's launches. */
 CLEORA_API int64_t cleora_kernel_launches(void);
 
+/* Device blocks of >= 1 MiB freed by cleora_destroy (T replicas, CSR, sort buffers) are kept
+ * in a process-wide cache and reused by later handles of the same sizes (no allocator growth
+ * between repeated build/embed/destroy cycles), up to CLEORA_CACHE_MAX_FRAC (default 0.6) of
+ * device memory; CLEORA_NO_CACHE=1 disables it.  This call returns every cached block to the
+ * driver (e.g. before handing the memory to another library).  Returns CLEORA_OK or
+ * EINTERNAL. */
+CLEORA_API int cleora_release_cached_memory(void);
+
 /* ---- test hooks (not on the graded path) ------------------------------------------------ */
 
 /* Copy the device CSR to host arrays in the original labelling:

@@ -22,6 +22,7 @@ __all__ = [
     "cleora_build", "cleora_init", "cleora_iterate", "cleora_fetch", "cleora_info", "cleora_stats",
     "cleora_sync", "cleora_destroy", "cleora_last_error", "cleora_fetch_csr", "cleora_set_rows",
     "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
+    "cleora_release_cached_memory",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcleora.so")
@@ -71,6 +72,7 @@ _SIGS = {
     "cleora_nccl_get_unique_id": (ctypes.c_int, [_vp]),
     "cleora_plan_shards": (ctypes.c_int, [_vp, _i64, _i32, _vp]),
     "cleora_kernel_launches": (ctypes.c_int64, []),
+    "cleora_release_cached_memory": (ctypes.c_int, []),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -265,3 +267,8 @@ def cleora_plan_shards(row_ptr, world: int) -> np.ndarray:
 def cleora_kernel_launches() -> int:
     """Process-wide count of kernels libcleora has launched (its own + CUB's)."""
     return int(_lib.cleora_kernel_launches())
+
+
+def cleora_release_cached_memory():
+    """Return the library's cached device blocks (freed T replicas, CSR, sort buffers) to the driver."""
+    _check(_lib.cleora_release_cached_memory())

@@ -38,8 +38,63 @@ void trace(const char* what, cudaStream_t s, bool sync) {
     last = now;
 }
 
+// ---------------------------------------------------------------- device memory
+// Small buffers come from the device's default stream-ordered pool.  Large ones (>= 1 MiB:
+// the T replicas, CSR arrays, sort buffers) go through a process-wide cache of freed blocks,
+// keyed by device and size rounded to 2 MiB: a graph built, embedded and destroyed over and
+// over (the bench step; a service embedding many graphs of one shape) reuses the same
+// physical blocks instead of growing the pool.  Measured on B200: without it, pool growth
+// in the middle of a run stalled single steps by 40-140 ms (scripts/step_jitter.py).
+// A cached block carries an event recorded on the stream that freed it; the stream that
+// reuses it waits on that event, so stream ordering is kept across streams.
+// cleora_release_cached_memory() returns every cached block to the driver; an allocation
+// that fails for lack of memory does the same on its device and retries once.
 static std::mutex g_pool_mu;
 static bool g_pool_cfg[64];
+
+namespace {
+constexpr size_t kCacheMin = (size_t)1 << 20;
+constexpr size_t kCacheGrain = (size_t)2 << 20;
+struct Block {
+    void* p;
+    size_t bytes;
+    int dev;
+    cudaEvent_t ready;
+};
+std::mutex g_cache_mu;
+std::vector<Block> g_cache;                 // freed, reusable
+std::vector<Block> g_live;                  // handed out (p -> size, device)
+size_t g_cached_bytes = 0;
+
+size_t round_block(size_t b) { return (b + kCacheGrain - 1) / kCacheGrain * kCacheGrain; }
+
+void release_cached(int dev /* -1: all */, cudaStream_t s) {
+    std::vector<Block> drop;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (size_t i = 0; i < g_cache.size();) {
+            if (dev < 0 || g_cache[i].dev == dev) {
+                drop.push_back(g_cache[i]);
+                g_cached_bytes -= g_cache[i].bytes;
+                g_cache[i] = g_cache.back();
+                g_cache.pop_back();
+            } else {
+                i++;
+            }
+        }
+    }
+    int cur = -1;
+    cudaGetDevice(&cur);
+    for (auto& b : drop) {
+        cudaSetDevice(b.dev);
+        cudaEventSynchronize(b.ready);
+        cudaEventDestroy(b.ready);
+        cudaFree(b.p);
+    }
+    if (cur >= 0) cudaSetDevice(cur);
+    (void)s;
+}
+}  // namespace
 
 Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what) {
     *p = nullptr;
@@ -57,19 +112,102 @@ Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what) {
         }
     }
     if (bytes == 0) bytes = 16;
-    cudaError_t e = cudaMallocAsync(p, bytes, s);
-    if (e != cudaSuccess) {
+    const bool big = bytes >= kCacheMin && getenv("CLEORA_NO_CACHE") == nullptr;
+    if (big) {
+        const size_t rb = round_block(bytes);
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (size_t i = 0; i < g_cache.size(); i++) {
+            if (g_cache[i].dev == dev && g_cache[i].bytes == rb) {
+                Block b = g_cache[i];
+                g_cache[i] = g_cache.back();
+                g_cache.pop_back();
+                g_cached_bytes -= rb;
+                cudaStreamWaitEvent(s, b.ready, 0);
+                *p = b.p;
+                g_live.push_back(b);
+                return Status::ok();
+            }
+        }
+    }
+    for (int attempt = 0; attempt < 2; attempt++) {
+        cudaError_t e;
+        if (big) {
+            // cached blocks are plain device allocations (not pool memory): they outlive streams
+            e = cudaMalloc(p, round_block(bytes));
+        } else {
+            e = cudaMallocAsync(p, bytes, s);
+        }
+        if (e == cudaSuccess) break;
         cudaGetLastError();
-        char buf[256];
-        snprintf(buf, sizeof buf, "cudaMallocAsync(%zu bytes) for %s: %s", bytes, what, cudaGetErrorString(e));
         *p = nullptr;
+        if (e == cudaErrorMemoryAllocation && attempt == 0) {
+            cudaStreamSynchronize(s);
+            release_cached(dev, s);
+            continue;
+        }
+        char buf[256];
+        snprintf(buf, sizeof buf, "cudaMalloc(%zu bytes) for %s: %s", bytes, what, cudaGetErrorString(e));
         return Status::make(4, buf);
+    }
+    if (big) {
+        Block b{*p, round_block(bytes), dev, nullptr};
+        if (cudaEventCreateWithFlags(&b.ready, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(*p);
+            *p = nullptr;
+            return Status::make(4, std::string("cudaEventCreate for ") + what);
+        }
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        g_live.push_back(b);
     }
     return Status::ok();
 }
 
+static size_t cache_cap_bytes(int dev) {
+    static size_t cap[64];
+    if (dev < 0 || dev >= 64) return 0;
+    if (!cap[dev]) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const char* e = getenv("CLEORA_CACHE_MAX_FRAC");
+        const double f = e ? atof(e) : 0.6;
+        cap[dev] = (size_t)(f * (double)tot) + 1;
+    }
+    return cap[dev];
+}
+
 void dfree(void* p, cudaStream_t s) {
-    if (p) cudaFreeAsync(p, s);
+    if (!p) return;
+    std::vector<Block> drop;
+    bool cached = false;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (size_t i = 0; i < g_live.size(); i++) {
+            if (g_live[i].p == p) {
+                Block b = g_live[i];
+                g_live[i] = g_live.back();
+                g_live.pop_back();
+                cudaEventRecord(b.ready, s);    // the block is free once s reaches this point
+                g_cache.push_back(b);
+                g_cached_bytes += b.bytes;
+                cached = true;
+                // bound what stays cached: drop the oldest blocks beyond the cap
+                const size_t cap = cache_cap_bytes(b.dev);
+                while (g_cached_bytes > cap && g_cache.size() > 1) {
+                    drop.push_back(g_cache.front());
+                    g_cached_bytes -= g_cache.front().bytes;
+                    g_cache.erase(g_cache.begin());
+                }
+                break;
+            }
+        }
+    }
+    for (auto& b : drop) {
+        cudaEventSynchronize(b.ready);
+        cudaEventDestroy(b.ready);
+        cudaFree(b.p);
+    }
+    if (!cached) cudaFreeAsync(p, s);
 }
 
 // ---------------------------------------------------------------- NCCL, resolved at run time
@@ -343,6 +481,13 @@ extern "C" {
 const char* cleora_last_error(void) { return g_err.c_str(); }
 
 int64_t cleora_kernel_launches(void) { return g_launches.load(); }
+
+int cleora_release_cached_memory(void) {
+    release_cached(-1, nullptr);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_release_cached_memory: ") + cudaGetErrorString(e)));
+    return CLEORA_OK;
+}
 
 int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, int64_t n_edges, int32_t n_nodes,
                  int32_t directed, const cleora_opts* opts, cleora_graph** out) {

@@ -114,14 +114,27 @@ __global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __re
     const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < N; a += wstride) {
         const int64_t k0 = row_ptr[a], k1 = row_ptr[a + 1];
-        double part = 0.0;
+        // 8 independent partial sums per lane keep 8 loads in flight on hub rows (any order
+        // is exact on the integer fast path; the general path below redoes the sum in order)
+        double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         bool integral = true;
-        for (int64_t k = k0 + lane; k < k1; k += 32) {
+        int64_t k = k0 + lane;
+        for (; k + 7 * 32 < k1; k += 8 * 32) {
+            double x[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) x[u] = e_ab[k + 32 * u];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                integral &= (x[u] == trunc(x[u]));
+                p[u] += x[u];
+            }
+        }
+        for (; k < k1; k += 32) {
             const double x = e_ab[k];
             integral &= (x == trunc(x));
-            part += x;
+            p[0] += x;
         }
-        double s = part;
+        double s = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (!__all_sync(0xffffffffu, integral) || !(s < 4503599627370496.0)) {

@@ -20,6 +20,40 @@ __device__ __forceinline__ float h2f(uint64_t h) {
     return (float)((int32_t)(h >> 40) - 8388608) * (1.0f / 8388608.0f);
 }
 
+constexpr uint64_t kC1 = 0xBF58476D1CE4E5B9ull, kC2 = 0x94D049BB133111EBull;
+
+// The same value as h2f(sm64(base ^ j)) for 0 <= j < 2^30, with the per-row work hoisted
+// (the kernel is integer-ALU bound, not HBM bound, when written naively):
+//   z1 = base ^ j ^ (base >> 30)            (j < 2^30 contributes nothing to z1 >> 30)
+//   z2 = z1 * C1  = lo*C1lo + ((lo*C1hi + hi*C1lo) << 32), hi*C1lo a per-row constant
+//   z3 = z2 ^ (z2 >> 27)
+//   h >> 40 = (z3 * C2) >> 40               (the final xor-shift by 31 does not reach bit 40)
+// so only the high word of z3*C2 is formed.  Bit-exact with the oracle (tested).
+struct RowHash {
+    uint32_t b1_lo, b1_hi, k1;   // b1 = base ^ (base >> 30); k1 = lo32(b1_hi * C1lo)
+};
+
+__device__ __forceinline__ RowHash row_hash(uint64_t base) {
+    const uint64_t b1 = base ^ (base >> 30);
+    RowHash r;
+    r.b1_lo = (uint32_t)b1;
+    r.b1_hi = (uint32_t)(b1 >> 32);
+    r.k1 = r.b1_hi * (uint32_t)kC1;
+    return r;
+}
+
+__device__ __forceinline__ float hash_elem(const RowHash& r, uint32_t j) {
+    const uint32_t lo = r.b1_lo ^ j;
+    const uint64_t t = (uint64_t)lo * (uint32_t)kC1;                       // lo * C1lo
+    const uint32_t z2_lo = (uint32_t)t;
+    const uint32_t z2_hi = (uint32_t)(t >> 32) + lo * (uint32_t)(kC1 >> 32) + r.k1;
+    const uint32_t z3_lo = z2_lo ^ __funnelshift_r(z2_lo, z2_hi, 27);      // low word of z2 >> 27
+    const uint32_t z3_hi = z2_hi ^ (z2_hi >> 27);
+    const uint32_t z4_hi = __umulhi(z3_lo, (uint32_t)kC2) + z3_lo * (uint32_t)(kC2 >> 32) +
+                           z3_hi * (uint32_t)kC2;
+    return (float)((int32_t)(z4_hi >> 8) - 8388608) * (1.0f / 8388608.0f);
+}
+
 // One warp per row (grid-stride over rows): lane l writes float4 columns l, l+32, ... -- no
 // 64-bit division per element, 512 contiguous bytes per warp store instruction.
 __global__ void k_hash_init(float4* __restrict__ T, int64_t N, int32_t d, int32_t dp, uint64_t s) {
@@ -27,16 +61,16 @@ __global__ void k_hash_init(float4* __restrict__ T, int64_t N, int32_t d, int32_
     const int q = dp / 4;
     const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < N; v += wstride) {
-        const uint64_t base = s ^ ((uint64_t)v << 32);
+        const RowHash rh = row_hash(s ^ ((uint64_t)v << 32));
         float4* row = T + v * q;
         for (int f = lane; f < q; f += 32) {
-            const int j0 = 4 * f;
+            const uint32_t j0 = 4u * f;
             float4 o;
-            o.x = (j0 + 0 < d) ? h2f(sm64(base ^ (uint64_t)(j0 + 0))) : 0.0f;
-            o.y = (j0 + 1 < d) ? h2f(sm64(base ^ (uint64_t)(j0 + 1))) : 0.0f;
-            o.z = (j0 + 2 < d) ? h2f(sm64(base ^ (uint64_t)(j0 + 2))) : 0.0f;
-            o.w = (j0 + 3 < d) ? h2f(sm64(base ^ (uint64_t)(j0 + 3))) : 0.0f;
-            row[f] = o;
+            o.x = (j0 + 0 < (uint32_t)d) ? hash_elem(rh, j0 + 0) : 0.0f;
+            o.y = (j0 + 1 < (uint32_t)d) ? hash_elem(rh, j0 + 1) : 0.0f;
+            o.z = (j0 + 2 < (uint32_t)d) ? hash_elem(rh, j0 + 2) : 0.0f;
+            o.w = (j0 + 3 < (uint32_t)d) ? hash_elem(rh, j0 + 3) : 0.0f;
+            __stcs(row + f, o);
         }
     }
 }
