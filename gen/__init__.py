@@ -146,8 +146,36 @@ def rmat_undirected(n, scale, samples, abc, seed=0) -> EdgeList:
                     np.resize(dst, got) if got != samples else dst, None, False)
 
 
+def _cache_path(name: str, seed: int):
+    d = os.environ.get("CLEORA_GEN_CACHE")
+    return os.path.join(d, f"{name}_s{seed}.npz") if d else None
+
+
 def config(name: str, seed: int = 0) -> EdgeList:
-    """Generate BASELINE.json config ``name`` (c1..c5) with generator seed ``seed``."""
+    """Generate BASELINE.json config ``name`` (c1..c5) with generator seed ``seed``.
+
+    With ``CLEORA_GEN_CACHE=<dir>`` the edge arrays are kept in ``<dir>`` after the first
+    generation (c5 takes minutes of host time) and loaded from there afterwards."""
+    c = CONFIGS[name]
+    path = _cache_path(name, seed)
+    if path and os.path.exists(path):
+        z = np.load(path)
+        w = z["w"] if "w" in z.files else None
+        g = EdgeList(name, int(z["n"]), z["src"], z["dst"], w, bool(z["directed"]))
+        g.d, g.iters = c["d"], c["iters"]
+        g.meta = dict(desc=c["desc"], seed=seed)
+        return g
+    g = _generate(name, seed)
+    if path:
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        extra = {"w": g.w} if g.w is not None else {}
+        tmp = path + f".tmp{os.getpid()}.npz"
+        np.savez(tmp, n=g.n, src=g.src, dst=g.dst, directed=g.directed, **extra)
+        os.replace(tmp, path)
+    return g
+
+
+def _generate(name: str, seed: int) -> EdgeList:
     c = CONFIGS[name]
     k = c["kind"]
     if k == "er":

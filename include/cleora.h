@@ -51,8 +51,15 @@ enum {
 
 /* cleora_opts.flags */
 enum {
-    CLEORA_F_TIMING = 1    /* record CUDA events around every SpMM+normalise launch so that
+    CLEORA_F_TIMING = 1,   /* record CUDA events around every SpMM+normalise launch so that
                               cleora_stats() can report device time per launch            */
+    CLEORA_F_LOOPBACK = 2, /* world > 1 without NCCL: emulate all `world` ranks (<= 8) in this
+                              process on one GPU -- one replica pair per rank, the ranks'
+                              fused SpMM launches run one after another and store their rows
+                              into every replica.  For testing the multi-GPU path on one GPU;
+                              rank selects the replica cleora_fetch reads.                  */
+    CLEORA_F_EXCHANGE_NCCL = 4 /* world > 1: exchange the shards with an NCCL all-gather-v
+                              after each step instead of the fused peer stores            */
 };
 
 /* Build options.  Pass NULL to cleora_build for: current device, host inputs, a
@@ -115,7 +122,12 @@ CLEORA_API int cleora_init(cleora_graph* g, int32_t d, uint64_t seed);
  * product is the zero vector (no out-edges) is written as zeros (reading RZ).
  * iterate(a); iterate(b) is bit-identical to iterate(a + b).  Results do not depend on the
  * number of GPUs (the per-row schedule depends only on the row's degree).
- * Multi-GPU: collective; after each step the rank shards are all-gathered into every replica.
+ * Multi-GPU: collective.  Each rank computes the rows of its shard, and the kernel's epilogue
+ * stores every finished row into all ranks' replicas through NVLink (peer pointers opened with
+ * CUDA IPC during cleora_init), so the exchange overlaps the SpMM row by row; a 4-byte NCCL
+ * all-reduce then orders the steps across ranks.  When the GPUs cannot map each other's memory
+ * (or with CLEORA_F_EXCHANGE_NCCL) the shards are all-gathered with NCCL after each step.
+ * Rows without out-edges stay 0 and are not rewritten once both buffers hold their zeros.
  *   Errors: EUSAGE (g NULL, k < 0, called before cleora_init), EINTERNAL.
  */
 CLEORA_API int cleora_iterate(cleora_graph* g, int32_t k);
@@ -145,6 +157,8 @@ typedef struct cleora_info_t {
     int64_t shard_end;
     int32_t rank, world;
     int64_t device_bytes;   /* device memory currently owned by the handle              */
+    int64_t hot_rows;       /* rows whose gathers carry the L2 evict_last hint (0 = none) */
+    int32_t exchange;       /* 0 one GPU, 1 NCCL all-gather, 2 fused peer stores, 3 loopback */
 } cleora_info_t;
 CLEORA_API int cleora_info(const cleora_graph* g, cleora_info_t* out);
 
@@ -185,8 +199,14 @@ CLEORA_API int cleora_release_cached_memory(void);
  * row_ptr [N+1] int64, col [nnz] int32, val [nnz] fp32, deg [N] fp64 (any may be NULL). */
 CLEORA_API int cleora_fetch_csr(const cleora_graph* g, int64_t* row_ptr, int32_t* col, float* val, double* deg);
 
+/* Copy rows [row_begin, row_end) of rank `rank`'s replica of the current T into host memory
+ * (dense, d per row).  With CLEORA_F_LOOPBACK every emulated rank's replica is readable (the
+ * replicas must be identical); otherwise only this rank's. */
+CLEORA_API int cleora_fetch_replica(const cleora_graph* g, int32_t rank, int64_t row_begin, int64_t row_end,
+                                    float* host_out);
+
 /* Overwrite rows [row_begin, row_end) of the current T from host memory (dense, d per row):
- * resume from a checkpoint or start from a custom T_0. */
+ * resume from a checkpoint or start from a custom T_0.  (Loopback: every replica.) */
 CLEORA_API int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const float* host_in);
 
 /* Size of an ncclUniqueId (128) and a helper that fills one (rank 0 calls it and

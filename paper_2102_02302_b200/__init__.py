@@ -20,7 +20,7 @@ import numpy as np
 __all__ = [
     "CleoraError", "Graph", "LIB_PATH",
     "cleora_build", "cleora_init", "cleora_iterate", "cleora_fetch", "cleora_info", "cleora_stats",
-    "cleora_sync", "cleora_destroy", "cleora_last_error", "cleora_fetch_csr", "cleora_set_rows",
+    "cleora_sync", "cleora_destroy", "cleora_last_error", "cleora_fetch_csr", "cleora_set_rows", "cleora_fetch_replica",
     "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
     "cleora_release_cached_memory",
 ]
@@ -32,7 +32,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 OK, EUSAGE, EDATA, EINTERNAL = 0, 2, 3, 4
-F_TIMING = 1
+F_TIMING, F_LOOPBACK, F_EXCHANGE_NCCL = 1, 2, 4
 
 
 class _Opts(ctypes.Structure):
@@ -46,7 +46,8 @@ class _Info(ctypes.Structure):
                 ("d", ctypes.c_int32), ("d_stride", ctypes.c_int32), ("iterations", ctypes.c_int64),
                 ("zero_rows", ctypes.c_int64), ("max_degree", ctypes.c_int64), ("heavy_rows", ctypes.c_int64),
                 ("heavy_items", ctypes.c_int64), ("shard_begin", ctypes.c_int64), ("shard_end", ctypes.c_int64),
-                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device_bytes", ctypes.c_int64)]
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
+                ("hot_rows", ctypes.c_int64), ("exchange", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -68,6 +69,7 @@ _SIGS = {
     "cleora_last_error": (ctypes.c_char_p, []),
     "cleora_fetch_csr": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "cleora_set_rows": (ctypes.c_int, [_vp, _i64, _i64, _vp]),
+    "cleora_fetch_replica": (ctypes.c_int, [_vp, _i32, _i64, _i64, _vp]),
     "cleora_nccl_id_size": (ctypes.c_int, []),
     "cleora_nccl_get_unique_id": (ctypes.c_int, [_vp]),
     "cleora_plan_shards": (ctypes.c_int, [_vp, _i64, _i32, _vp]),
@@ -157,7 +159,8 @@ class Graph:
 
 
 def cleora_build(src, dst, weight, n_nodes: int, directed: bool = False, *, device: int = -1, stream=None,
-                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None, timing: bool = False) -> Graph:
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None, timing: bool = False,
+                 loopback: bool = False, exchange_nccl: bool = False) -> Graph:
     """COO edge list -> device CSR of M = D^-1 A.  See include/cleora.h."""
     ps, ds, ks = _ptr(src, np.int32)
     pd, dd, kd = _ptr(dst, np.int32)
@@ -182,7 +185,8 @@ def cleora_build(src, dst, weight, n_nodes: int, directed: bool = False, *, devi
     if nccl_id is not None:
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), len(nccl_id))
         o.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
-    o.flags = F_TIMING if timing else 0
+    o.flags = (F_TIMING if timing else 0) | (F_LOOPBACK if loopback else 0) | \
+        (F_EXCHANGE_NCCL if exchange_nccl else 0)
     h = ctypes.c_void_p()
     _check(_lib.cleora_build(ps, pd, pw, n, int(n_nodes), 1 if directed else 0, ctypes.byref(o), ctypes.byref(h)))
     return Graph(h.value)
@@ -239,6 +243,16 @@ def cleora_fetch_csr(g: Graph) -> dict:
     val = np.empty(nnz, np.float32); deg = np.empty(n, np.float64)
     _check(_lib.cleora_fetch_csr(g.handle, rp.ctypes.data, col.ctypes.data, val.ctypes.data, deg.ctypes.data))
     return dict(row_ptr=rp, col=col, val=val, deg=deg)
+
+
+def cleora_fetch_replica(g: Graph, rank: int, row_begin: int = 0, row_end: int | None = None) -> np.ndarray:
+    """Rows of rank ``rank``'s replica (every replica is local with ``loopback=True``)."""
+    info = cleora_info(g)
+    if row_end is None:
+        row_end = info["n_nodes"]
+    out = np.empty((max(0, row_end - row_begin), info["d"]), np.float32)
+    _check(_lib.cleora_fetch_replica(g.handle, int(rank), int(row_begin), int(row_end), out.ctypes.data))
+    return out
 
 
 def cleora_set_rows(g: Graph, row_begin: int, rows):

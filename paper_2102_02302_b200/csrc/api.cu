@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -219,6 +220,8 @@ struct Nccl {
     ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
@@ -239,6 +242,8 @@ static Nccl& nccl() {
         BIND(GetUniqueId, "ncclGetUniqueId");
         BIND(CommInitRank, "ncclCommInitRank");
         BIND(Broadcast, "ncclBroadcast");
+        BIND(AllGather, "ncclAllGather");
+        BIND(AllReduce, "ncclAllReduce");
         BIND(GroupStart, "ncclGroupStart");
         BIND(GroupEnd, "ncclGroupEnd");
         BIND(CommDestroy, "ncclCommDestroy");
@@ -284,7 +289,7 @@ struct cleora_graph {
     int32_t d = 0, dp = 0;
     float* T[2] = {nullptr, nullptr};
     float* partials = nullptr;
-    int32_t* col_tag = nullptr;     // col with the hot bit (TMA path L2 hints), built by cleora_init
+    int32_t tag_dp = 0;             // row stride the hot-row tags in col (bit 31) were chosen for
     int64_t n_hot = 0;
     int cur = 0;
     int64_t iters = 0;
@@ -292,6 +297,17 @@ struct cleora_graph {
     std::vector<int64_t> cuts;
     int64_t r0 = 0, r1 = 0;
     ncclComm_t comm = nullptr;
+    // exchange of the row shards after every step (world > 1), see exchange_mode below
+    int xmode = 0;
+    bool zclean[2] = {false, false};   // rows without entries are already 0 in T[b]
+    // X_PEER: the other ranks' T[0], T[1], opened through CUDA IPC (rank order, self skipped)
+    float* peer_T[2][kMaxPeers] = {};
+    int* d_flag = nullptr;             // 1 int: operand of the per-step NCCL barrier
+    // X_LOOPBACK: all `world` replicas live in this process; rep[p] = rank p's T pair
+    // (rep[rank] aliases T), sched_p[p] = rank p's schedule
+    std::vector<std::array<float*, 2>> rep;
+    std::vector<Schedule> sched_p;
+    int64_t max_items = 0;
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_spmm, ev_x;
     std::vector<cudaEvent_t> ev_pool;
@@ -360,16 +376,114 @@ Status collect_timing(cleora_graph* g) {
     return Status::ok();
 }
 
+// Exchange modes (world > 1).  X_PEER is the product path: the SpMM epilogue stores every
+// finished row into all replicas over NVLink (peer pointers from CUDA IPC), then one 4-byte NCCL
+// all-reduce per step orders the steps across ranks.  X_NCCL: the SpMM writes only the local
+// replica and an all-gather-v (grouped in-place ncclBroadcast) follows -- the fallback when the
+// GPUs cannot map each other's memory, or on request (CLEORA_F_EXCHANGE_NCCL).  X_LOOPBACK:
+// `world` ranks emulated in one process on one GPU (tests): the same fused kernel writes its
+// rows into the other ranks' replicas, which are local buffers; ranks run one after another.
+enum { X_NONE = 0, X_NCCL = 1, X_PEER = 2, X_LOOPBACK = 3 };
+
+void close_peers(cleora_graph* g) {
+    for (int b = 0; b < 2; b++)
+        for (int i = 0; i < kMaxPeers; i++)
+            if (g->peer_T[b][i]) {
+                cudaIpcCloseMemHandle(g->peer_T[b][i]);
+                g->peer_T[b][i] = nullptr;
+            }
+}
+
 void free_T(cleora_graph* g) {
+    close_peers(g);
+    for (size_t p = 0; p < g->rep.size(); p++)
+        if ((int)p != g->rank)
+            for (int i = 0; i < 2; i++) dfree(g->rep[p][i], g->stream);
+    if (!g->rep.empty()) g->rep.assign(g->rep.size(), {nullptr, nullptr});
     for (int i = 0; i < 2; i++) {
         dfree(g->T[i], g->stream);
         g->T[i] = nullptr;
     }
     dfree(g->partials, g->stream);
     g->partials = nullptr;
-    dfree(g->col_tag, g->stream);
-    g->col_tag = nullptr;
-    g->n_hot = 0;
+    g->zclean[0] = g->zclean[1] = false;
+}
+
+// Stream-ordered barrier over all ranks (a 1-int all-reduce): work enqueued after it on any rank
+// runs after every rank's work enqueued before it -- including the SpMM's peer stores.
+Status rank_barrier(cleora_graph* g) {
+    Nccl& N = nccl();
+    CL_NCCL_TRY(N.AllReduce(g->d_flag, g->d_flag, 1, ncclInt32, ncclMax, g->comm, g->stream));
+    return Status::ok();
+}
+
+// X_PEER set-up (collective, inside cleora_init): all-gather the IPC handles of every rank's
+// T[0], T[1] and open the others'.  Any rank that cannot open them makes all ranks fall back to
+// X_NCCL (the decision is all-reduced, so every rank takes the same path).
+Status open_peers(cleora_graph* g) {
+    Nccl& N = nccl();
+    const int W = g->world;
+    if (W - 1 > kMaxPeers) {
+        g->xmode = X_NCCL;
+        return Status::ok();
+    }
+    cudaIpcMemHandle_t mine[2];
+    int ok = 1;
+    for (int b = 0; b < 2; b++)
+        if (cudaIpcGetMemHandle(&mine[b], g->T[b]) != cudaSuccess) {
+            cudaGetLastError();
+            ok = 0;
+        }
+    const size_t hb = sizeof(mine);
+    void* d_all = nullptr;
+    CL_TRY(dalloc(&d_all, hb * W + 16, g->stream, "IPC handles"));
+    std::vector<char> all(hb * W);
+    Status st = Status::ok();
+    do {
+        if (cudaMemcpyAsync((char*)d_all + hb * g->rank, mine, hb, cudaMemcpyHostToDevice, g->stream) != cudaSuccess) {
+            st = Status::make(4, "IPC handle copy");
+            break;
+        }
+        ncclResult_t r = N.AllGather((char*)d_all + hb * g->rank, d_all, hb, ncclChar, g->comm, g->stream);
+        if (r != ncclSuccess) { st = Status::make(4, std::string("ncclAllGather: ") + N.GetErrorString(r)); break; }
+        if (cudaMemcpyAsync(all.data(), d_all, hb * W, cudaMemcpyDeviceToHost, g->stream) != cudaSuccess ||
+            cudaStreamSynchronize(g->stream) != cudaSuccess) {
+            st = Status::make(4, "IPC handle gather");
+            break;
+        }
+    } while (0);
+    dfree(d_all, g->stream);
+    CL_TRY(st);
+    int i = 0;
+    for (int p = 0; p < W && ok; p++) {
+        if (p == g->rank) continue;
+        for (int b = 0; b < 2 && ok; b++) {
+            cudaIpcMemHandle_t h;
+            memcpy(&h, all.data() + hb * p + sizeof(cudaIpcMemHandle_t) * b, sizeof h);
+            void* ptr = nullptr;
+            if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                ok = 0;
+            } else {
+                g->peer_T[b][i] = (float*)ptr;
+            }
+        }
+        i++;
+    }
+    // all ranks agree: peer stores only if every rank opened every peer
+    int h_ok = ok;
+    CL_CUDA_TRY(cudaMemcpyAsync(g->d_flag, &h_ok, sizeof(int), cudaMemcpyHostToDevice, g->stream));
+    {
+        ncclResult_t r = N.AllReduce(g->d_flag, g->d_flag, 1, ncclInt32, ncclMin, g->comm, g->stream);
+        if (r != ncclSuccess) return Status::make(4, std::string("ncclAllReduce: ") + N.GetErrorString(r));
+    }
+    CL_CUDA_TRY(cudaMemcpyAsync(&h_ok, g->d_flag, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+    CL_CUDA_TRY(cudaStreamSynchronize(g->stream));
+    if (!h_ok) {
+        close_peers(g);
+        g->xmode = X_NCCL;
+    }
+    return Status::ok();
 }
 
 Status exchange(cleora_graph* g, float* buf) {
@@ -459,11 +573,29 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
     }
     g->r0 = g->cuts[g->rank];
     g->r1 = g->cuts[g->rank + 1];
-    CL_TRY(build_schedule(g->row_ptr, N, g->r0, g->r1, g->heavy_thresh, g->stream, &g->sched));
+    const bool loopback = g->world > 1 && o && (o->flags & CLEORA_F_LOOPBACK);
+    if (loopback) {
+        // every rank's schedule lives here; g->sched aliases this rank's
+        g->sched_p.resize(g->world);
+        for (int p = 0; p < g->world; p++) {
+            CL_TRY(build_schedule(g->row_ptr, N, g->cuts[p], g->cuts[p + 1], g->heavy_thresh, g->stream,
+                                  &g->sched_p[p]));
+            g->max_items = std::max(g->max_items, g->sched_p[p].n_items);
+        }
+        g->sched = g->sched_p[g->rank];
+        g->rep.assign(g->world, {nullptr, nullptr});
+        g->xmode = X_LOOPBACK;
+    } else {
+        CL_TRY(build_schedule(g->row_ptr, N, g->r0, g->r1, g->heavy_thresh, g->stream, &g->sched));
+        g->max_items = g->sched.n_items;
+    }
     trace("build: schedule", g->stream, true);
     g->bytes += g->sched.n_items * (int64_t)sizeof(HeavyItem) + g->sched.n_heavy_rows * 4;
 
-    if (g->world > 1) {
+    if (g->world > 1 && !loopback) {
+        g->xmode = (o->flags & CLEORA_F_EXCHANGE_NCCL) ? X_NCCL : X_PEER;
+        CL_TRY(dalloc((void**)&g->d_flag, 16, g->stream, "barrier flag"));
+        CL_CUDA_TRY(cudaMemsetAsync(g->d_flag, 0, 16, g->stream));
         Nccl& nc = nccl();
         if (!nc.ok) return Status::make(4, "cleora_build: NCCL unavailable: " + nc.why);
         ncclUniqueId id;
@@ -497,7 +629,10 @@ int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, in
     if (n_nodes <= 0) return usage("cleora_build: n_nodes must be > 0");
     if (n_edges <= 0) return usage("cleora_build: n_edges must be > 0 (non-empty edge list)");
     if (opts && opts->world > 1) {
-        if (!opts->nccl_id) return usage("cleora_build: world > 1 needs nccl_id");
+        if (opts->world - 1 > kMaxPeers && (opts->flags & CLEORA_F_LOOPBACK))
+            return usage("cleora_build: loopback emulation supports at most 8 ranks");
+        if (!opts->nccl_id && !(opts->flags & CLEORA_F_LOOPBACK))
+            return usage("cleora_build: world > 1 needs nccl_id");
         if (opts->rank < 0 || opts->rank >= opts->world) return usage("cleora_build: rank outside [0, world)");
     }
     DeviceGuard guard(opts ? opts->device : -1);
@@ -526,9 +661,29 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
                 return fail(s);
             }
         }
-        if (g->sched.n_items > 0) {
-            Status s = dalloc((void**)&g->partials, (size_t)g->sched.n_items * dp * sizeof(float), g->stream,
+        if (g->max_items > 0) {
+            Status s = dalloc((void**)&g->partials, (size_t)g->max_items * dp * sizeof(float), g->stream,
                               "heavy-row partials");
+            if (!s.good()) {
+                free_T(g);
+                return fail(s);
+            }
+        }
+        if (g->xmode == X_LOOPBACK) {
+            g->rep[g->rank] = {g->T[0], g->T[1]};
+            for (int p = 0; p < g->world; p++) {
+                if (p == g->rank) continue;
+                for (int i = 0; i < 2; i++) {
+                    Status s = dalloc((void**)&g->rep[p][i], tb, g->stream, "loopback replica");
+                    if (!s.good()) {
+                        free_T(g);
+                        return fail(s);
+                    }
+                }
+            }
+        }
+        if (g->xmode == X_PEER) {
+            Status s = open_peers(g);          // collective; may switch every rank to X_NCCL
             if (!s.good()) {
                 free_T(g);
                 return fail(s);
@@ -539,20 +694,34 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     g->dp = dp;
     g->cur = 0;
     g->iters = 0;
-    if (!g->col_tag && tma_path_supported(dp) && !getenv("CLEORA_NO_HOT") && g->nnz > 0) {
-        // L2 residency hints: tag the columns whose rows are re-read most (highest in-degree) so
-        // that their gathers use an evict_last policy, within a budget of the 126 MB L2
+    g->zclean[0] = g->zclean[1] = false;
+    if (g->tag_dp != dp && tma_path_supported(dp) && !getenv("CLEORA_NO_HOT") && g->nnz > 0) {
+        // L2 residency hints: tag (bit 31 of col, in place) the columns whose rows are re-read
+        // most (highest in-degree) so that their gathers use an evict_last policy, within a
+        // budget of the 126 MB L2
         const char* e = getenv("CLEORA_HOT_MB");
         const int64_t budget = (int64_t)(e ? atof(e) : 72.0) * 1024 * 1024;
-        Status s = dalloc((void**)&g->col_tag, (size_t)g->nnz * sizeof(int32_t), g->stream, "hot-tagged col");
-        if (s.good()) s = hot_tag(g->col, g->nnz, g->n, (int64_t)dp * 4, budget, g->stream, g->col_tag, &g->n_hot);
+        Status s = hot_tag(g->col, g->nnz, g->n, (int64_t)dp * 4, budget, g->stream, &g->n_hot);
         if (!s.good()) {
             free_T(g);
             return fail(s);
         }
+        g->tag_dp = dp;
     }
     Status s = launch_hash_init(g->T[0], g->n, d, dp, seed, g->stream);
     if (!s.good()) return fail(s);
+    if (g->xmode == X_LOOPBACK)   // every emulated rank initialises its own replica
+        for (int p = 0; p < g->world; p++)
+            if (p != g->rank) {
+                s = launch_hash_init(g->rep[p][0], g->n, d, dp, seed, g->stream);
+                if (!s.good()) return fail(s);
+            }
+    if (g->xmode == X_PEER) {
+        // no rank may store into another's replicas before that rank is done with its
+        // previous steps and has re-initialised
+        s = rank_barrier(g);
+        if (!s.good()) return fail(s);
+    }
     return CLEORA_OK;
 }
 
@@ -561,53 +730,70 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
     if (k < 0) return usage("cleora_iterate: k must be >= 0");
     if (!g->T[0]) return usage("cleora_iterate: call cleora_init first");
     DeviceGuard guard(g->device);
+    const int nsh = g->xmode == X_LOOPBACK ? g->world : 1;
     for (int32_t i = 0; i < k; i++) {
-        SpmmArgs a;
-        a.row_ptr = g->row_ptr;
-        a.col = g->col;
-        a.col_tag = nullptr;
-        a.val = g->val;
-        a.T_in = g->T[g->cur];
-        a.T_out = g->T[1 - g->cur];
-        a.dp = g->dp;
-        a.r0 = g->r0;
-        a.r1 = g->r1;
-        a.heavy_thresh = g->heavy_thresh;
-        a.items = g->sched.items;
-        a.n_items = g->sched.n_items;
-        a.partials = g->partials;
-        a.counters = g->sched.counters;
-        a.col_tag = g->col_tag;
-        // with hot rows pinned (power-law graphs) the other gathers are evicted first; without
-        // (e.g. lattices, whose re-reads are local) they keep the normal policy (measured: c2, c4, c3)
-        a.cold_first = getenv("CLEORA_COLD_FIRST") ? atoi(getenv("CLEORA_COLD_FIRST")) : (g->n_hot > 0 ? 1 : 0);
-        a.work = g->sched.work;
+        const int in = g->cur, out = 1 - g->cur;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (g->timing) {
             e0 = get_event(g);
             e1 = get_event(g);
             cudaEventRecord(e0, g->stream);
         }
-        Status s = launch_spmm_norm(a, g->stream);
-        if (!s.good()) return fail(s);
+        for (int sh = 0; sh < nsh; sh++) {
+            // rank p's launch; outside loopback p is this rank and there is one launch
+            const int p = g->xmode == X_LOOPBACK ? sh : g->rank;
+            const Schedule& sc = g->xmode == X_LOOPBACK ? g->sched_p[p] : g->sched;
+            SpmmArgs a;
+            a.row_ptr = g->row_ptr;
+            a.col = g->col;
+            a.val = g->val;
+            a.T_in = g->xmode == X_LOOPBACK ? g->rep[p][in] : g->T[in];
+            a.T_out = g->xmode == X_LOOPBACK ? g->rep[p][out] : g->T[out];
+            a.dp = g->dp;
+            a.r0 = g->cuts[p];
+            a.r1 = g->cuts[p + 1];
+            a.heavy_thresh = g->heavy_thresh;
+            a.items = sc.items;
+            a.n_items = sc.n_items;
+            a.partials = g->partials;
+            a.counters = sc.counters;
+            // with hot rows pinned (power-law graphs) the other gathers are evicted first; without
+            // (e.g. lattices, whose re-reads are local) they keep the normal policy (measured: c2, c4, c3)
+            a.cold_first = getenv("CLEORA_COLD_FIRST") ? atoi(getenv("CLEORA_COLD_FIRST")) : (g->n_hot > 0 ? 1 : 0);
+            a.work = sc.work;
+            a.n_peers = 0;
+            for (int q = 0; q < kMaxPeers; q++) a.peer_out[q] = nullptr;
+            if (g->xmode == X_LOOPBACK) {
+                for (int q = 0; q < g->world; q++)
+                    if (q != p) a.peer_out[a.n_peers++] = g->rep[q][out];
+            } else if (g->xmode == X_PEER) {
+                for (int q = 0; q < g->world - 1; q++) a.peer_out[a.n_peers++] = g->peer_T[out][q];
+            }
+            a.skip_zero_rows = (g->zclean[out] && !getenv("CLEORA_WRITE_ZERO_ROWS")) ? 1 : 0;
+            Status s = launch_spmm_norm(a, g->stream);
+            if (!s.good()) return fail(s);
+        }
         if (g->timing) {
             cudaEventRecord(e1, g->stream);
             g->ev_spmm.emplace_back(e0, e1);
         }
-        if (g->world > 1) {
+        if (g->xmode == X_NCCL || g->xmode == X_PEER) {
             if (g->timing) {
                 e0 = get_event(g);
                 e1 = get_event(g);
                 cudaEventRecord(e0, g->stream);
             }
-            s = exchange(g, g->T[1 - g->cur]);
+            // X_NCCL: all-gather-v of the shards; X_PEER: the rows are already in every
+            // replica, only the step order across ranks is enforced
+            Status s = g->xmode == X_NCCL ? exchange(g, g->T[out]) : rank_barrier(g);
             if (!s.good()) return fail(s);
             if (g->timing) {
                 cudaEventRecord(e1, g->stream);
                 g->ev_x.emplace_back(e0, e1);
             }
         }
-        g->cur = 1 - g->cur;
+        g->zclean[out] = true;     // every row of T[out] was written (or was already 0)
+        g->cur = out;
         g->iters++;
     }
     return CLEORA_OK;
@@ -632,16 +818,42 @@ int cleora_fetch(const cleora_graph* g, int64_t row_begin, int64_t row_end, floa
     return CLEORA_OK;
 }
 
+int cleora_fetch_replica(const cleora_graph* g, int32_t rank, int64_t row_begin, int64_t row_end, float* host_out) {
+    if (!g || !host_out) return usage("cleora_fetch_replica: NULL argument");
+    if (!g->T[0]) return usage("cleora_fetch_replica: call cleora_init first");
+    if (g->xmode != X_LOOPBACK) {
+        if (rank != g->rank) return usage("cleora_fetch_replica: only this rank's replica is local");
+        return cleora_fetch(g, row_begin, row_end, host_out, 0);
+    }
+    if (rank < 0 || rank >= g->world) return usage("cleora_fetch_replica: rank outside [0, world)");
+    if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_fetch_replica: rows outside [0, N]");
+    if (row_end == row_begin) return CLEORA_OK;
+    DeviceGuard guard(g->device);
+    const float* src = g->rep[rank][g->cur] + row_begin * (int64_t)g->dp;
+    cudaError_t e = cudaMemcpy2DAsync(host_out, (size_t)g->d * sizeof(float), src, (size_t)g->dp * sizeof(float),
+                                      (size_t)g->d * sizeof(float), (size_t)(row_end - row_begin),
+                                      cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_fetch_replica: ") + cudaGetErrorString(e)));
+    return CLEORA_OK;
+}
+
 int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const float* host_in) {
     if (!g || !host_in) return usage("cleora_set_rows: NULL argument");
     if (!g->T[0]) return usage("cleora_set_rows: call cleora_init first");
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_set_rows: rows outside [0, N]");
     if (row_end == row_begin) return CLEORA_OK;
     DeviceGuard guard(g->device);
-    float* dst = g->T[g->cur] + row_begin * (int64_t)g->dp;
-    cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)g->dp * sizeof(float), host_in, (size_t)g->d * sizeof(float),
-                                      (size_t)g->d * sizeof(float), (size_t)(row_end - row_begin),
-                                      cudaMemcpyHostToDevice, g->stream);
+    // loopback: every emulated rank sets the same rows in its own replica
+    const int nrep = g->xmode == X_LOOPBACK ? g->world : 1;
+    cudaError_t e = cudaSuccess;
+    for (int p = 0; p < nrep && e == cudaSuccess; p++) {
+        float* base = g->xmode == X_LOOPBACK ? g->rep[p][g->cur] : g->T[g->cur];
+        e = cudaMemcpy2DAsync(base + row_begin * (int64_t)g->dp, (size_t)g->dp * sizeof(float), host_in,
+                              (size_t)g->d * sizeof(float), (size_t)g->d * sizeof(float),
+                              (size_t)(row_end - row_begin), cudaMemcpyHostToDevice, g->stream);
+    }
+    g->zclean[g->cur] = false;
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_set_rows: ") + cudaGetErrorString(e)));
     return CLEORA_OK;
@@ -654,6 +866,9 @@ int cleora_fetch_csr(const cleora_graph* g, int64_t* row_ptr, int32_t* col, floa
     if (row_ptr && e == cudaSuccess)
         e = cudaMemcpyAsync(row_ptr, g->row_ptr, ((size_t)g->n + 1) * 8, cudaMemcpyDeviceToHost, g->stream);
     if (col && e == cudaSuccess) e = cudaMemcpyAsync(col, g->col, (size_t)g->nnz * 4, cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    if (col && e == cudaSuccess)
+        for (int64_t k = 0; k < g->nnz; k++) col[k] &= kColMask;     // drop the hot-row tags
     if (val && e == cudaSuccess) e = cudaMemcpyAsync(val, g->val, (size_t)g->nnz * 4, cudaMemcpyDeviceToHost, g->stream);
     if (deg && e == cudaSuccess) e = cudaMemcpyAsync(deg, g->deg, (size_t)g->n * 8, cudaMemcpyDeviceToHost, g->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
@@ -678,6 +893,8 @@ int cleora_info(const cleora_graph* g, cleora_info_t* o) {
     o->shard_end = g->r1;
     o->rank = g->rank;
     o->world = g->world;
+    o->hot_rows = g->n_hot;
+    o->exchange = g->xmode;
     o->device_bytes = g->bytes + (g->T[0] ? 2 * (int64_t)g->n * g->dp * 4 : 0) +
                       (g->partials ? g->sched.n_items * (int64_t)g->dp * 4 : 0);
     DeviceGuard guard(g->device);
@@ -723,9 +940,17 @@ void cleora_destroy(cleora_graph* g) {
         dfree(g->col, g->stream);
         dfree(g->val, g->stream);
         dfree(g->deg, g->stream);
-        dfree(g->sched.items, g->stream);
-        dfree(g->sched.counters, g->stream);
-        dfree(g->sched.work, g->stream);
+        if (g->sched_p.empty()) {
+            dfree(g->sched.items, g->stream);
+            dfree(g->sched.counters, g->stream);
+            dfree(g->sched.work, g->stream);
+        }
+        for (auto& sc : g->sched_p) {      // loopback: g->sched aliases sched_p[rank]
+            dfree(sc.items, g->stream);
+            dfree(sc.counters, g->stream);
+            dfree(sc.work, g->stream);
+        }
+        dfree(g->d_flag, g->stream);
         cudaStreamSynchronize(g->stream);
     }
     for (auto& p : g->ev_spmm) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }

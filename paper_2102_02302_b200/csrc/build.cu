@@ -426,60 +426,81 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
 namespace {
 __global__ void k_indegree(const int32_t* __restrict__ col, int64_t nnz, int32_t* __restrict__ indeg) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) atomicAdd(indeg + col[k], 1);
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride)
+        atomicAdd(indeg + (col[k] & kColMask), 1);
 }
-__global__ void k_indeg_hist(const int32_t* __restrict__ indeg, int32_t N, unsigned long long* __restrict__ hist) {
-    __shared__ unsigned long long h[33];
-    if (threadIdx.x < 33) h[threadIdx.x] = 0;
-    __syncthreads();
+// c[0] += #rows with indeg >= t, c[1] += #rows with indeg >= t + 1
+__global__ void k_count_ge(const int32_t* __restrict__ indeg, int32_t N, int32_t t, unsigned long long* __restrict__ c) {
+    unsigned long long a = 0, b = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < N; v += stride) {
-        const int x = indeg[v];
-        atomicAdd(&h[x > 0 ? 32 - __clz(x) : 0], 1ull);        // bin b >= 1: 2^(b-1) <= x < 2^b
+        const int32_t x = indeg[v];
+        a += x >= t;
+        b += x > t;
     }
-    __syncthreads();
-    if (threadIdx.x < 33) atomicAdd(hist + threadIdx.x, h[threadIdx.x]);
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (a | b)) {
+        atomicAdd(c, a);
+        atomicAdd(c + 1, b);
+    }
 }
-__global__ void k_tag(const int32_t* __restrict__ col, int64_t nnz, const int32_t* __restrict__ indeg, int32_t t,
-                      int32_t* __restrict__ out) {
+__global__ void k_tag(int32_t* __restrict__ col, int64_t nnz, const int32_t* __restrict__ indeg, int32_t t) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
-        const int32_t c = col[k];
-        out[k] = indeg[c] >= t ? (int32_t)((uint32_t)c | 0x80000000u) : c;
+        const int32_t c = col[k] & kColMask;
+        col[k] = indeg[c] >= t ? (int32_t)((uint32_t)c | 0x80000000u) : c;
     }
 }
 }  // namespace
 
-Status hot_tag(const int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes, cudaStream_t s,
-               int32_t* d_col_tag, int64_t* n_hot) {
-    DevBuf<int32_t> indeg;
-    DevBuf<unsigned long long> hist;
+Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes, cudaStream_t s,
+               int64_t* n_hot) {
+    // hot rows = the K = budget / row_bytes rows of largest in-degree (exact threshold: the K-th
+    // largest in-degree, from a radix sort of the in-degrees; ties at the threshold are kept
+    // unless they overshoot the budget by more than a quarter)
+    DevBuf<int32_t> indeg, sorted;
+    DevBuf<unsigned long long> cnt;
     CL_TRY(indeg.alloc(N, s, "in-degree"));
-    CL_TRY(hist.alloc(33, s, "in-degree histogram"));
+    CL_TRY(sorted.alloc(N, s, "sorted in-degree"));
+    CL_TRY(cnt.alloc(2, s, "hot count"));
     CL_CUDA_TRY(cudaMemsetAsync(indeg.p, 0, (size_t)N * 4, s));
-    CL_CUDA_TRY(cudaMemsetAsync(hist.p, 0, 33 * 8, s));
     k_indegree<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
-    k_indeg_hist<<<grid_for(N, 8), kThreads, 0, s>>>(indeg.p, N, hist.p);
+    {
+        size_t tmp_bytes = 0;
+        CL_CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, indeg.p, sorted.p, (int64_t)N, 0, 32, s));
+        DevBuf<uint8_t> tmp;
+        CL_TRY(tmp.alloc(tmp_bytes, s, "in-degree sort temp"));
+        CL_CUDA_TRY(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, indeg.p, sorted.p, (int64_t)N, 0, 32, s));
+        count_launches(2 + 4);
+    }
+    int64_t K = budget_bytes / (row_bytes > 0 ? row_bytes : 1);
+    if (K > N) K = N;
+    int32_t t = INT32_MAX;
+    if (K > 0) {
+        CL_CUDA_TRY(cudaMemcpyAsync(&t, sorted.p + (N - K), sizeof t, cudaMemcpyDeviceToHost, s));
+        CL_CUDA_TRY(cudaStreamSynchronize(s));
+        if (t < 2) t = 2;                 // a row read once or never gains nothing from pinning
+    }
+    CL_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), s));
+    k_count_ge<<<grid_for(N, 8), kThreads, 0, s>>>(indeg.p, N, t, cnt.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
-    unsigned long long h[33];
-    CL_CUDA_TRY(cudaMemcpyAsync(h, hist.p, sizeof h, cudaMemcpyDeviceToHost, s));
+    unsigned long long c[2];
+    CL_CUDA_TRY(cudaMemcpyAsync(c, cnt.p, sizeof c, cudaMemcpyDeviceToHost, s));
     CL_CUDA_TRY(cudaStreamSynchronize(s));
-    // rows with in-degree >= 2^(b-1) are those in bins >= b; take the lowest b that fits the budget
-    int64_t cum = 0;
-    int best = 33;
-    for (int b = 32; b >= 2; b--) {
-        cum += (int64_t)h[b];
-        if (cum * row_bytes > budget_bytes) break;
-        best = b;
+    int64_t nh = (int64_t)c[0];           // rows with in-degree >= t
+    if (t != INT32_MAX && nh > K + K / 4) {
+        t += 1;
+        nh = (int64_t)c[1];               // rows with in-degree >= t + 1
     }
-    int64_t nh = 0;
-    for (int b = best; b <= 32; b++) nh += (int64_t)h[b];
+    if (t == INT32_MAX) nh = 0;
     *n_hot = nh;
-    const int32_t t = best >= 32 ? INT32_MAX : (int32_t)(1u << (best - 1));
-    k_tag<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p, t, d_col_tag);
+    k_tag<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p, t);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     return Status::ok();

@@ -56,12 +56,12 @@ struct HeavyItem {
 static_assert(sizeof(HeavyItem) == 32, "HeavyItem layout");
 
 constexpr int kWarpsPerCta = 8;     // 256 threads
+constexpr int kMaxPeers = 7;        // other replicas a launch writes into (8 GPUs per box)
 constexpr int kMaxV = 8;            // float4 per lane per column slice (slice = 1024 floats)
 
 struct SpmmArgs {
     const int64_t* row_ptr;
-    const int32_t* col;
-    const int32_t* col_tag; // optional: col with bit 31 set for hot columns (TMA path), or NULL
+    const int32_t* col;     // column ids; bit 31 = "hot" tag (hot_tag below), masked on use
     const float* val;
     const float* T_in;
     float* T_out;
@@ -74,7 +74,21 @@ struct SpmmArgs {
     unsigned* counters;     // one per heavy row, 0 between launches
     unsigned* work;         // 3 work tickets of the persistent kernel, 0 between launches
     int32_t cold_first;     // TMA path: gathers of non-hot rows with evict_first (else evict_normal)
+    // Fused exchange (multi-GPU): every finished row is also stored into the T_out replicas of
+    // the other ranks -- NVLink peer pointers opened through CUDA IPC, or, in loopback
+    // emulation, the other local replicas -- so the all-gather overlaps the SpMM row by row.
+    int32_t n_peers;
+    float* peer_out[kMaxPeers];
+    // Rows without entries are already 0 in T_out (written by an earlier iteration): skip them.
+    int32_t skip_zero_rows;
 };
+
+// Store float4 f of row `row` of the iteration's output into T_out and every peer replica.
+__device__ __forceinline__ void put_out4(const SpmmArgs& a, int64_t row, int f, const float4& v) {
+    const int64_t off = row * (int64_t)a.dp;
+    __stcs(reinterpret_cast<float4*>(a.T_out + off) + f, v);
+    for (int p = 0; p < a.n_peers; p++) __stcs(reinterpret_cast<float4*>(a.peer_out[p] + off) + f, v);
+}
 
 // build.cu
 struct BuildOut {
@@ -98,11 +112,13 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
                       cudaStream_t s, Schedule* out);
 Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts);
 
-// Hot-row tagging for L2 residency hints: col_tag[k] = col[k] | (indeg(col[k]) >= 2^b) << 31,
-// b the smallest power of two such that the hot rows' bytes fit `budget_bytes`.  Returns the
-// number of hot rows in *n_hot (0 => no tagging was useful).
-Status hot_tag(const int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes,
-               cudaStream_t s, int32_t* d_col_tag, int64_t* n_hot);
+// Hot-row tagging for L2 residency hints, in place: col[k] = (col[k] & 0x7fffffff) |
+// (indeg(col[k]) >= 2^b) << 31, b the smallest power of two such that the hot rows' bytes fit
+// `budget_bytes` (node ids are < 2^31, so bit 31 is free).  Returns the number of hot rows in
+// *n_hot (0 => no row is tagged).  Every reader of col masks bit 31.
+constexpr int32_t kColMask = 0x7fffffff;
+Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes,
+               cudaStream_t s, int64_t* n_hot);
 
 // init.cu
 Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s);

@@ -15,14 +15,9 @@ __host__ __device__ __forceinline__ uint64_t sm64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ float h2f(uint64_t h) {
-    // (h >> 40) has 24 bits; subtracting 2^23 and scaling by 2^-23 is exact in fp32
-    return (float)((int32_t)(h >> 40) - 8388608) * (1.0f / 8388608.0f);
-}
-
 constexpr uint64_t kC1 = 0xBF58476D1CE4E5B9ull, kC2 = 0x94D049BB133111EBull;
 
-// The same value as h2f(sm64(base ^ j)) for 0 <= j < 2^30, with the per-row work hoisted
+// The same value as ((int32)(sm64(base ^ j) >> 40) - 2^23) * 2^-23 for 0 <= j < 2^30, with the per-row work hoisted
 // (the kernel is integer-ALU bound, not HBM bound, when written naively):
 //   z1 = base ^ j ^ (base >> 30)            (j < 2^30 contributes nothing to z1 >> 30)
 //   z2 = z1 * C1  = lo*C1lo + ((lo*C1hi + hi*C1lo) << 32), hi*C1lo a per-row constant

@@ -43,7 +43,7 @@ __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, int64_t k0, i
         int32_t mc = 0;
         float mw = 0.0f;
         if (lane < n) {
-            mc = __ldg(a.col + kb + lane);
+            mc = __ldg(a.col + kb + lane) & kColMask;
             mw = __ldg(a.val + kb + lane);
         }
         int j = 0;
@@ -79,6 +79,7 @@ __device__ void light_row(const SpmmArgs& a, int64_t row, int64_t k0, int64_t k1
     constexpr int SW = 128 * V;                   // floats per column slice
     const int dp = a.dp;
     const int ns = (dp + SW - 1) / SW;
+    if (k1 == k0 && a.skip_zero_rows) return;     // already 0 in T_out (reading RZ)
     float4* out = reinterpret_cast<float4*>(a.T_out + row * (int64_t)dp);
     double ss = 0.0;
     float4 acc[V];
@@ -102,10 +103,10 @@ __device__ void light_row(const SpmmArgs& a, int64_t row, int64_t k0, int64_t k1
 #pragma unroll
         for (int v = 0; v < V; v++) {
             const int f = lane + 32 * v;
-            if (4 * f < dp) __stcs(out + f, scale4(acc[v], inv));
+            if (4 * f < dp) put_out4(a, row, f, scale4(acc[v], inv));
         }
     } else {
-        for (int f = lane; 4 * f < dp; f += 32) __stcs(out + f, scale4(out[f], inv));
+        for (int f = lane; 4 * f < dp; f += 32) put_out4(a, row, f, scale4(out[f], inv));
     }
 }
 
@@ -153,9 +154,10 @@ __device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* 
         const double tot = block_sum(ss, scratch);
         const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
         if (ns == 1) {
-            if (t < Q && t < nq) __stcs(dst + t, scale4(y, inv));
+            if (t < Q && t < nq) put_out4(a, it.row, t, scale4(y, inv));
         } else {
-            for (int f = t; f < nq; f += blockDim.x) __stcs(dst + f, scale4(dst[f], inv));
+            __syncthreads();   // dst (= this row of T_out) holds the unnormalised slices
+            for (int f = t; f < nq; f += blockDim.x) put_out4(a, it.row, f, scale4(dst[f], inv));
         }
         return;
     }
@@ -172,7 +174,6 @@ __device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* 
     const int64_t first = idx - it.part;
     const float4* parts = reinterpret_cast<const float4*>(a.partials + first * (int64_t)dp);
     const int64_t pstride = dp / 4;
-    float4* out = reinterpret_cast<float4*>(a.T_out + (int64_t)it.row * dp);
     double zx = 0, zy = 0, zz = 0, zw = 0;
     double ss2 = 0.0;
     for (int f = t; f < nq; f += blockDim.x) {
@@ -187,7 +188,8 @@ __device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* 
     const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
     if (nq <= (int)blockDim.x) {
         if (t < nq)
-            __stcs(out + t, make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
+            put_out4(a, it.row, t,
+                     make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
     } else {
         for (int f = t; f < nq; f += blockDim.x) {
             zx = zy = zz = zw = 0.0;
@@ -195,7 +197,8 @@ __device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* 
                 const float4 p = __ldcg(parts + q * pstride + f);
                 zx += p.x; zy += p.y; zz += p.z; zw += p.w;
             }
-            __stcs(out + f, make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
+            put_out4(a, it.row, f,
+                     make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
         }
     }
     if (t == 0) a.counters[it.hrow] = 0u;         // ready for the next launch
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_norm(const SpmmAr
     __shared__ double scratch[kWarpsPerCta];
     __shared__ int flag;
     __shared__ unsigned s_item;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31;
     if (a.n_items > 0) {
         for (;;) {
             if (threadIdx.x == 0) s_item = atomicAdd(a.work + 0, 1u);

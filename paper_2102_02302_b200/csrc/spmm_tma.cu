@@ -43,12 +43,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(saddr(dst)),
-        "l"(src), "r"(bytes), "r"(saddr(bar))
-        : "memory");
-}
 
 __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
     asm volatile(
@@ -125,20 +119,23 @@ __device__ __forceinline__ void ring_issue(const SpmmArgs& a, Ring& r, int slot,
     }
 }
 
+// `empty`: the row has no entries (its output is the zero vector, reading RZ); with
+// a.skip_zero_rows the zeros are already in T_out and nothing is written.
 template <int V, bool FULL>
-__device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, float4 (&acc)[V], int lane) {
+__device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, float4 (&acc)[V], int lane,
+                                               bool empty) {
     const int dp = FULL ? 128 * V : a.dp;
+    if (empty && a.skip_zero_rows) return;           // acc is still all zeros
     double ss = 0.0;
 #pragma unroll
     for (int v = 0; v < V; v++)
         if (FULL || 4 * (lane + 32 * v) < dp) ss += sq4(acc[v]);
     ss = warp_sum(ss);
     const double inv = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
-    float4* out = reinterpret_cast<float4*>(a.T_out + row * (int64_t)dp);
 #pragma unroll
     for (int v = 0; v < V; v++) {
         const int f = lane + 32 * v;
-        if (FULL || 4 * f < dp) __stcs(out + f, scale4(acc[v], inv));
+        if (FULL || 4 * f < dp) put_out4(a, row, f, scale4(acc[v], inv));
         acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
@@ -152,7 +149,7 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
     const int dp = FULL ? 128 * V : a.dp;
     int64_t row = ra;
     int64_t kend = ROWS ? __shfl_sync(kFull, rpl, (int)(ra - rb + 1)) : E1;
-    const int32_t* colp = a.col_tag ? a.col_tag : a.col;
+    const int32_t* colp = a.col;   // bit 31 = hot tag (ring_issue picks the L2 policy from it)
     int32_t mc0 = 0, mc1 = 0;
     float mw0 = 0.f, mw1 = 0.f;
     if (E0 + lane < E1) {
@@ -179,7 +176,8 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
             const int64_t e = kb + j;
             if (ROWS) {
                 while (e >= kend) {                       // row boundary (warp-uniform)
-                    finalize_row_t<V, FULL>(a, row, acc, lane);
+                    const int64_t kbeg = __shfl_sync(kFull, rpl, (int)(row - rb));
+                    finalize_row_t<V, FULL>(a, row, acc, lane, kbeg == kend);
                     row++;
                     kend = __shfl_sync(kFull, rpl, (int)(row - rb + 1));
                 }
@@ -210,7 +208,9 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
     }
     if (ROWS) {
         while (row < rz) {                                // last row and trailing zero rows
-            finalize_row_t<V, FULL>(a, row, acc, lane);
+            const int64_t kbeg = __shfl_sync(kFull, rpl, (int)(row - rb));
+            const int64_t kfin = __shfl_sync(kFull, rpl, (int)(row - rb + 1));
+            finalize_row_t<V, FULL>(a, row, acc, lane, kbeg == kfin);
             row++;
         }
     }
@@ -250,7 +250,7 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
     if (it.nparts == 1) {
         const double tot = block_sum(ss, scratch);
         const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
-        if (t < nq) __stcs(reinterpret_cast<float4*>(a.T_out + (int64_t)it.row * dp) + t, scale4(y, inv));
+        if (t < nq) put_out4(a, it.row, t, scale4(y, inv));
     } else {
         float4* part = reinterpret_cast<float4*>(a.partials + idx * (int64_t)dp);
         if (t < nq) part[t] = y;
@@ -274,8 +274,8 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
             const double tot = block_sum(zx * zx + zy * zy + zz * zz + zw * zw, scratch);
             const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
             if (t < nq)
-                __stcs(reinterpret_cast<float4*>(a.T_out + (int64_t)it.row * dp) + t,
-                       make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
+                put_out4(a, it.row, t,
+                         make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
             if (t == 0) a.counters[it.hrow] = 0u;
         }
     }

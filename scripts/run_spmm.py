@@ -20,5 +20,6 @@ cl.cleora_iterate(G, iters)
 st = cl.cleora_stats(G)
 info = cl.cleora_info(G)
 print(cfg, "d", d, "nnz", info["nnz"], "heavy rows", info["heavy_rows"], "items", info["heavy_items"],
+      "hot rows", info["hot_rows"],
       "spmm ms/launch", st["spmm_ms_total"] / max(1, st["spmm_launches"]), "min", st["spmm_ms_min"])
 G.close()
