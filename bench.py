@@ -254,7 +254,8 @@ def load_traffic(name, d):
     if not os.path.exists(p):
         return None
     try:
-        return json.load(open(p)).get(f"{name}_d{d}")
+        e = json.load(open(p)).get(f"{name}_d{d}")
+        return None if e is None else e["bytes_per_launch_mean"]
     except Exception:
         return None
 
@@ -366,12 +367,21 @@ def main():
         G.close()
     spmm_ms = max_over_ranks(spmm["ms"] / max(spmm["n"], 1))
     peak, peak_src = load_peaks()
-    b_comp = 8 * (g.n + 1) + 8 * nnz + 2 * g.n * d * 4       # SURVEY.md §8(d) B_comp per iteration
+    # SURVEY.md §8(d) / BASELINE north star: compulsory bytes per iteration = CSR (int64 row
+    # pointer, int32 col, fp32 val) + one read and one write of the N x d fp32 T; per rank 1/P
+    b_comp = (8 * (g.n + 1) + 8 * nnz + 2 * g.n * d * 4) / world
     achieved = b_comp / (spmm_ms / 1e3) / 1e9
+    # stricter variant: only rows that are ever gathered are read, only rows with out-edges are
+    # written (steady state: empty rows are not rewritten after the first two steps)
+    ref_rows = info.get("referenced_rows", -1)
+    ref_rows = g.n if ref_rows is None or ref_rows < 0 else ref_rows
+    b_strict = (8 * (g.n + 1) + 8 * nnz + (ref_rows + g.n - info["zero_rows"]) * d * 4) / world
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic(g.name, d), "kernel": "k_spmm_norm (fused SpMM + row L2 normalise)",
+                "traffic": load_traffic(g.name, d), "kernel": "k_spmm_tma (fused SpMM + row L2 normalise)",
                 "kernel_ms": spmm_ms, "algorithmic_bytes_per_launch": b_comp, "peak_source": peak_src,
-                "gather_bytes_per_launch": nnz * d * 4}
+                "strict_bytes_per_launch": b_strict, "strict_frac": b_strict / (spmm_ms / 1e3) / 1e9 / peak,
+                "gather_bytes_per_launch": nnz * d * 4 / world,
+                "bytes_def": "8(N+1) + 8 nnz + 2 N d 4 (CSR + one read and one write of T), per rank"}
 
     # e2e through the public C-ABI with host buffers (pinned), copies inside the timed region
     e2e = None

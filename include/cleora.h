@@ -158,6 +158,7 @@ typedef struct cleora_info_t {
     int32_t rank, world;
     int64_t device_bytes;   /* device memory currently owned by the handle              */
     int64_t hot_rows;       /* rows whose gathers carry the L2 evict_last hint (0 = none) */
+    int64_t referenced_rows;/* rows with in-degree > 0, i.e. ever gathered (-1: unknown)  */
     int32_t exchange;       /* 0 one GPU, 1 NCCL all-gather, 2 fused peer stores, 3 loopback */
 } cleora_info_t;
 CLEORA_API int cleora_info(const cleora_graph* g, cleora_info_t* out);

@@ -17,6 +17,11 @@ What each function computes, with the paper passage it follows
 * :func:`step` -- one ``T_i = M T_{i-1}`` followed by row L2 normalisation
   (Alg. 1 lines 6-7).
 * :func:`embed` -- Algorithm 1 with Q = 1 chunk.
+* :func:`chunk_assign`, :func:`chunk_occurrences`, :func:`merge`, :func:`embed_chunked` --
+  Algorithm 1 with Q > 1 chunks (lines 1-2 and 10-12), readings R13/R14.
+* :func:`reconstruct` -- a new node's embedding as the normalised weighted average of its
+  neighbours' rows (§3.2): one row of normalize(M T) over the
+  new nodes' own transition rows.
 """
 from __future__ import annotations
 
@@ -75,6 +80,10 @@ def _L():
         lib.oracle_step_rows.argtypes = [vp, ctypes.c_int32, f32p, f32p, ctypes.c_int64, ctypes.c_int64]
         lib.oracle_embed.argtypes = [vp, ctypes.c_int32, ctypes.c_uint64, ctypes.c_int32, f32p, f32p]
         lib.oracle_num_threads.restype = ctypes.c_int
+        lib.oracle_chunk_of_edge.restype = ctypes.c_int32
+        lib.oracle_chunk_of_edge.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32]
+        lib.oracle_chunk_assign.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, i32p]
+        lib.oracle_merge.argtypes = [ctypes.POINTER(f32p), i64p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, f32p]
         _lib = lib
     return _lib
 
@@ -163,3 +172,72 @@ def embed(M: Csr, d: int, seed: int, iters: int, keep_all: bool = False):
 
 def num_threads() -> int:
     return int(_L().oracle_num_threads())
+
+
+# ---------------------------------------------------------------- f1: chunks (Algorithm 1, Q > 1)
+
+def chunk_of_edge(chunk_seed: int, i: int, Q: int) -> int:
+    return int(_L().oracle_chunk_of_edge(chunk_seed & 0xFFFFFFFFFFFFFFFF, int(i), int(Q)))
+
+
+def chunk_assign(n_edges: int, Q: int, chunk_seed: int) -> np.ndarray:
+    """Chunk index of every input edge (reading R13)."""
+    out = np.empty(n_edges, np.int32)
+    _L().oracle_chunk_assign(chunk_seed & 0xFFFFFFFFFFFFFFFF, int(n_edges), int(Q), _p(out, ctypes.c_int32))
+    return out
+
+
+def chunk_occurrences(src, dst, chunk, Q: int, n: int) -> np.ndarray:
+    """occ[q, v] = occurrences of v as an endpoint of the edges of chunk q (reading R14)."""
+    occ = np.zeros((Q, n), np.int64)
+    np.add.at(occ, (chunk, src), 1)
+    np.add.at(occ, (chunk, dst), 1)
+    return occ
+
+
+def merge(Tq: list, occ: np.ndarray) -> np.ndarray:
+    """T_v = sum_q w_qv T^q_v (Algorithm 1 lines 10-12)."""
+    Q, n = occ.shape
+    d = Tq[0].shape[1]
+    Tq = [np.ascontiguousarray(t, np.float32) for t in Tq]
+    ptrs = (ctypes.POINTER(ctypes.c_float) * Q)(*[_p(t, ctypes.c_float) for t in Tq])
+    occ = np.ascontiguousarray(occ, np.int64)
+    out = np.empty((n, d), np.float32)
+    _L().oracle_merge(ptrs, _p(occ, ctypes.c_int64), Q, n, d, _p(out, ctypes.c_float))
+    return out
+
+
+def embed_chunked(src, dst, w, n: int, directed: bool, Q: int, chunk_seed: int, d: int, seed: int, iters: int,
+                  return_parts: bool = False):
+    """Algorithm 1 with Q chunks: split the edges (R13), embed every chunk
+    independently (its own M_q, T_0^q from the same id-keyed init, I steps), merge (R14)."""
+    src = np.ascontiguousarray(src, np.int32)
+    dst = np.ascontiguousarray(dst, np.int32)
+    chunk = chunk_assign(src.shape[0], Q, chunk_seed)
+    parts = []
+    for q in range(Q):
+        m = chunk == q
+        if not m.any():
+            parts.append(np.zeros((n, d), np.float32))     # an empty chunk: every row zero
+            continue
+        Mq = build_csr(src[m], dst[m], None if w is None else np.asarray(w)[m], n, directed)
+        parts.append(embed(Mq, d, seed, iters))
+    occ = chunk_occurrences(src, dst, chunk, Q, n)
+    T = merge(parts, occ)
+    return (T, parts, occ, chunk) if return_parts else T
+
+
+# ---------------------------------------------------------------- f2: inductive embedding
+
+def reconstruct(new_idx, known_idx, w, n_new: int, T_src: np.ndarray) -> np.ndarray:
+    """Embeddings of n_new unseen nodes from edges (new node i, known node b, weight): row i =
+    normalize(sum_b e_ib / sum e_i. * T_src[b]) -- "creation of new node embedding by weighted
+    averaging of all neighbors' representations", the transition-row multiply the
+    training loop performs; T_src should be T_{I-1}.  Built as
+    one step of normalize(M T) over the directed graph new -> known (readings B1-B4, R6, RZ)."""
+    T_src = np.ascontiguousarray(T_src, np.float32)
+    n_src, d = T_src.shape
+    n = max(n_new, n_src)
+    M = build_csr(new_idx, known_idx, w, n, True)
+    T_in = T_src if n == n_src else np.vstack([T_src, np.zeros((n - n_src, d), np.float32)])
+    return step(M, T_in, 0, n_new)

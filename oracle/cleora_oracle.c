@@ -251,6 +251,56 @@ void oracle_embed(const oracle_csr* M, int32_t d, uint64_t seed, int32_t iters, 
     if (a != T) memcpy(T, a, (size_t)M->n * (size_t)d * sizeof(float));
 }
 
+/* ------------------------------------------------------------------ f1: chunks (Q > 1) */
+
+/*
+ * Algorithm 1 line 1: "Divide graph G into Q chunks.  Let G_q be the q-th chunk
+ * with edge set E_q".  The paper does not say how; reading R13: edge i of the
+ * input list goes to chunk
+ *     q(i) = floor(Q * (h_i >> 32) / 2^32),   h_i = mix(mix(chunk_seed + 0x9E3779B97F4A7C15) XOR i)
+ * (mix = the SplitMix64 output function above), so every edge is in exactly one chunk and the
+ * assignment is deterministic and order-free ("deterministic hash-based edge
+ * assignment").
+ */
+int32_t oracle_chunk_of_edge(uint64_t chunk_seed, int64_t i, int32_t Q) {
+    uint64_t s = or_splitmix64_mix(chunk_seed + 0x9E3779B97F4A7C15ULL);
+    uint64_t h = or_splitmix64_mix(s ^ (uint64_t)i);
+    return (int32_t)(((h >> 32) * (uint64_t)Q) >> 32);
+}
+
+void oracle_chunk_assign(uint64_t chunk_seed, int64_t n_edges, int32_t Q, int32_t* out) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n_edges; i++) out[i] = oracle_chunk_of_edge(chunk_seed, i, Q);
+}
+
+/*
+ * Algorithm 1 lines 10-12:
+ *     T_v = sum_q w_qv T^q_v,   w_qv = |n in V_q : n = n_v| / sum_k |n in V_k : n = n_v|
+ * Reading R14: |n in V_q : n = n_v| = occurrences of v as an endpoint of the edges of E_q
+ * (occ[q*n + v]; an edge contributes one occurrence to each of its two endpoints, a self-loop
+ * two).  A node that occurs in no chunk gets the zero row.  No normalisation after the merge
+ * (Algorithm 1 performs none).  Arithmetic: w = (double)occ / (double)total, one fp64 division;
+ * acc = acc + w * (double)T^q[v][j] in fp64 over ascending q; one rounding to fp32 at the end.
+ * Tq[q] points to chunk q's N x d fp32 embedding.
+ */
+void oracle_merge(const float* const* Tq, const int64_t* occ, int32_t Q, int32_t n, int32_t d, float* out) {
+    #pragma omp parallel for schedule(static)
+    for (int32_t v = 0; v < n; v++) {
+        int64_t tot = 0;
+        for (int32_t q = 0; q < Q; q++) tot += occ[(int64_t)q * n + v];
+        float* o = out + (int64_t)v * d;
+        for (int32_t j = 0; j < d; j++) {
+            double acc = 0.0;
+            if (tot > 0)
+                for (int32_t q = 0; q < Q; q++) {
+                    double w = (double)occ[(int64_t)q * n + v] / (double)tot;
+                    acc = acc + w * (double)Tq[q][(int64_t)v * d + j];
+                }
+            o[j] = (float)acc;
+        }
+    }
+}
+
 /* Threads the oracle will use (for reporting cpu_baseline.cores). */
 int oracle_num_threads(void) {
 #ifdef _OPENMP

@@ -47,7 +47,7 @@ class _Info(ctypes.Structure):
                 ("zero_rows", ctypes.c_int64), ("max_degree", ctypes.c_int64), ("heavy_rows", ctypes.c_int64),
                 ("heavy_items", ctypes.c_int64), ("shard_begin", ctypes.c_int64), ("shard_end", ctypes.c_int64),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
-                ("hot_rows", ctypes.c_int64), ("exchange", ctypes.c_int32)]
+                ("hot_rows", ctypes.c_int64), ("referenced_rows", ctypes.c_int64), ("exchange", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):

@@ -291,6 +291,7 @@ struct cleora_graph {
     float* partials = nullptr;
     int32_t tag_dp = 0;             // row stride the hot-row tags in col (bit 31) were chosen for
     int64_t n_hot = 0;
+    int64_t n_ref = -1;             // rows with in-degree > 0 (known once hot_tag ran)
     int cur = 0;
     int64_t iters = 0;
     int rank = 0, world = 1;
@@ -701,7 +702,7 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
         // budget of the 126 MB L2
         const char* e = getenv("CLEORA_HOT_MB");
         const int64_t budget = (int64_t)(e ? atof(e) : 72.0) * 1024 * 1024;
-        Status s = hot_tag(g->col, g->nnz, g->n, (int64_t)dp * 4, budget, g->stream, &g->n_hot);
+        Status s = hot_tag(g->col, g->nnz, g->n, (int64_t)dp * 4, budget, g->stream, &g->n_hot, &g->n_ref);
         if (!s.good()) {
             free_T(g);
             return fail(s);
@@ -894,6 +895,7 @@ int cleora_info(const cleora_graph* g, cleora_info_t* o) {
     o->rank = g->rank;
     o->world = g->world;
     o->hot_rows = g->n_hot;
+    o->referenced_rows = g->n_ref;
     o->exchange = g->xmode;
     o->device_bytes = g->bytes + (g->T[0] ? 2 * (int64_t)g->n * g->dp * 4 : 0) +
                       (g->partials ? g->sched.n_items * (int64_t)g->dp * 4 : 0);

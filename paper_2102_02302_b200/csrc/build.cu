@@ -27,15 +27,18 @@ inline int grid_for(int64_t n, int per_thread = 1) {
     return (int)b;
 }
 
+// n_drop counts entries that sort to the end as `sentinel` and are not part of M: mirrors of
+// self-loops (reading R5) and, when chunking, every entry of an edge outside the chunk.
 __global__ void k_validate_expand(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
-                                  const float* __restrict__ w, int64_t E, int32_t N, int directed,
+                                  const float* __restrict__ w, int64_t E, int32_t N, int32_t dst_limit, int directed,
                                   uint64_t sentinel, uint64_t* __restrict__ keys, uint32_t* __restrict__ pos,
                                   unsigned long long* __restrict__ err_first, int* __restrict__ err_kind,
-                                  unsigned long long* __restrict__ n_self) {
+                                  unsigned long long* __restrict__ n_drop, int32_t n_chunks, int32_t chunk,
+                                  uint64_t chunk_key, int32_t* __restrict__ occ) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += stride) {
         int32_t u = src[i], v = dst[i];
-        bool bad_id = u < 0 || u >= N || v < 0 || v >= N;
+        bool bad_id = u < 0 || u >= N || v < 0 || v >= dst_limit;
         bool bad_w = false;
         if (w) {
             float x = w[i];
@@ -46,17 +49,26 @@ __global__ void k_validate_expand(const int32_t* __restrict__ src, const int32_t
             atomicOr(err_kind, bad_id ? 1 : 2);
             u = 0; v = 0;
         }
-        keys[i] = (uint64_t)(uint32_t)u * (uint64_t)N + (uint64_t)(uint32_t)v;
+        // chunk q(i) = floor(Q * (h_i >> 32) / 2^32), h_i = mix(key ^ i)  (reading R13)
+        const bool keep = n_chunks <= 1 ||
+                          (int32_t)(((sm64(chunk_key ^ (uint64_t)i) >> 32) * (uint64_t)n_chunks) >> 32) == chunk;
+        if (keep && occ) {
+            atomicAdd(occ + u, 1);               // endpoint occurrences (reading R14)
+            atomicAdd(occ + v, 1);
+        }
+        keys[i] = keep ? (uint64_t)(uint32_t)u * (uint64_t)N + (uint64_t)(uint32_t)v : sentinel;
         pos[i] = (uint32_t)i;
+        unsigned long long drop = keep ? 0 : 1;
         if (!directed) {
-            if (u == v) {
+            if (!keep || u == v) {
                 keys[E + i] = sentinel;          // the mirror of a self-loop is dropped (reading R5)
-                atomicAdd(n_self, 1ull);
+                drop++;
             } else {
                 keys[E + i] = (uint64_t)(uint32_t)v * (uint64_t)N + (uint64_t)(uint32_t)u;
             }
             pos[E + i] = (uint32_t)(E + i);
         }
+        if (drop) atomicAdd(n_drop, drop);
     }
 }
 
@@ -102,54 +114,97 @@ __global__ void k_row_ptr(const int32_t* __restrict__ rows, int64_t nnz, int32_t
     }
 }
 
-// B3: deg(a) = sum over ascending b of e_ab, the sequential left-to-right fp64 sum.  One warp
-// per row.  Fast path: when every e_ab of the row is an integer and the total is below 2^52, every
-// partial sum is exact, so a warp tree reduction returns exactly the sequential result (unit-weight
-// graphs always take it).  Otherwise the lanes load 32 consecutive e_ab (coalesced) and every
-// lane folds them in ascending order via shuffles -- literally the sequential sum.
+// B3: deg(a) = sum over ascending b of e_ab, the sequential left-to-right fp64 sum.
+// A warp takes 32 consecutive rows.  Rows with <= 32 entries: one lane each, literally the
+// sequential sum.  Longer rows: the whole warp, one row after another (ballot).  Fast path
+// there: when every e_ab of the row is an integer and the total is below 2^52, every partial sum
+// is exact, so any summation order returns exactly the sequential result (unit-weight graphs
+// always take it); otherwise the lanes load 32 consecutive e_ab (coalesced) and every lane folds
+// them in ascending order via shuffles -- the sequential sum again.
+__device__ double degree_long_row(const double* __restrict__ e_ab, int64_t k0, int64_t k1, int lane) {
+    // 8 independent partial sums per lane keep 8 loads in flight on hub rows
+    double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool integral = true;
+    int64_t k = k0 + lane;
+    for (; k + 7 * 32 < k1; k += 8 * 32) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) x[u] = e_ab[k + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            integral &= (x[u] == trunc(x[u]));
+            p[u] += x[u];
+        }
+    }
+    for (; k < k1; k += 32) {
+        const double x = e_ab[k];
+        integral &= (x == trunc(x));
+        p[0] += x;
+    }
+    double s = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (!__all_sync(0xffffffffu, integral) || !(s < 4503599627370496.0)) {
+        s = 0.0;                                   // general case: sequential fold
+        for (int64_t kb = k0; kb < k1; kb += 32) {
+            const int n = (int)min((int64_t)32, k1 - kb);
+            const double mine = lane < n ? e_ab[kb + lane] : 0.0;
+            for (int j = 0; j < n; j++) s = s + __shfl_sync(0xffffffffu, mine, j);
+        }
+    }
+    return s;
+}
+
 __global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __restrict__ e_ab, int32_t N,
                          double* __restrict__ deg, unsigned long long* __restrict__ zero_rows,
                          unsigned long long* __restrict__ max_deg) {
     const int lane = threadIdx.x & 31;
-    const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < N; a += wstride) {
-        const int64_t k0 = row_ptr[a], k1 = row_ptr[a + 1];
-        // 8 independent partial sums per lane keep 8 loads in flight on hub rows (any order
-        // is exact on the integer fast path; the general path below redoes the sum in order)
-        double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        bool integral = true;
-        int64_t k = k0 + lane;
-        for (; k + 7 * 32 < k1; k += 8 * 32) {
-            double x[8];
-#pragma unroll
-            for (int u = 0; u < 8; u++) x[u] = e_ab[k + 32 * u];
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                integral &= (x[u] == trunc(x[u]));
-                p[u] += x[u];
-            }
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // zero-row count and max degree: per-lane registers, one atomic per block at the end (per-row
+    // atomics on two addresses serialise in L2)
+    unsigned long long my_zero = 0, my_max = 0;
+    for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < N; base += nwarps * 32) {
+        const int64_t a = base + lane;
+        int64_t k0 = 0, k1 = 0;
+        if (a < N) {
+            k0 = row_ptr[a];
+            k1 = row_ptr[a + 1];
+            if (k1 == k0) my_zero++;
+            else my_max = max(my_max, (unsigned long long)(k1 - k0));
         }
-        for (; k < k1; k += 32) {
-            const double x = e_ab[k];
-            integral &= (x == trunc(x));
-            p[0] += x;
-        }
-        double s = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (!__all_sync(0xffffffffu, integral) || !(s < 4503599627370496.0)) {
-            s = 0.0;                                   // general case: sequential fold
-            for (int64_t kb = k0; kb < k1; kb += 32) {
-                const int n = (int)min((int64_t)32, k1 - kb);
-                const double mine = lane < n ? e_ab[kb + lane] : 0.0;
-                for (int j = 0; j < n; j++) s = s + __shfl_sync(0xffffffffu, mine, j);
-            }
-        }
-        if (lane == 0) {
+        const bool lng = a < N && k1 - k0 > 32;
+        if (a < N && !lng) {
+            double s = 0.0;
+            for (int64_t k = k0; k < k1; k++) s = s + e_ab[k];
             deg[a] = s;
-            if (k1 == k0) atomicAdd(zero_rows, 1ull);
-            else atomicMax(max_deg, (unsigned long long)(k1 - k0));
         }
+        unsigned m = __ballot_sync(0xffffffffu, lng);
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            const double s = degree_long_row(e_ab, __shfl_sync(0xffffffffu, k0, l), __shfl_sync(0xffffffffu, k1, l), lane);
+            if (lane == 0) deg[base + l] = s;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        my_zero += __shfl_xor_sync(0xffffffffu, my_zero, o);
+        my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, o));
+    }
+    __shared__ unsigned long long s_zero[32], s_max[32];
+    const int warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        s_zero[warp] = my_zero;
+        s_max[warp] = my_max;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long z = 0, mx = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            z += s_zero[w];
+            mx = max(mx, s_max[w]);
+        }
+        if (z) atomicAdd(zero_rows, z);
+        if (mx) atomicMax(max_deg, mx);
     }
 }
 
@@ -230,7 +285,9 @@ struct DevBuf {
 }  // namespace
 
 Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N,
-                 int directed, cudaStream_t s, BuildOut* out) {
+                 int directed, cudaStream_t s, BuildOut* out, const BuildExtra* extra) {
+    const BuildExtra none;
+    const BuildExtra& x = extra ? *extra : none;
     const int64_t n_ent = directed ? E : 2 * E;
     if (n_ent >= (int64_t)UINT32_MAX) return Status::make(2, "cleora_build: too many edges (entry positions are 32-bit)");
     const uint64_t NN = (uint64_t)N * (uint64_t)N;
@@ -251,8 +308,10 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     CL_CUDA_TRY(cudaMemsetAsync(scal.p, 0xFF, sizeof(unsigned long long), s));   // err_first = max
     CL_CUDA_TRY(cudaMemsetAsync(err_kind.p, 0, sizeof(int), s));
 
-    k_validate_expand<<<grid_for(E, 4), kThreads, 0, s>>>(d_src, d_dst, d_w, E, N, directed, sentinel, keys.p, pos.p,
-                                                          scal.p + 0, err_kind.p, scal.p + 1);
+    if (x.occ) CL_CUDA_TRY(cudaMemsetAsync(x.occ, 0, (size_t)N * sizeof(int32_t), s));
+    k_validate_expand<<<grid_for(E, 4), kThreads, 0, s>>>(d_src, d_dst, d_w, E, N, x.dst_limit < 0 ? N : x.dst_limit,
+                                                          directed, sentinel, keys.p, pos.p, scal.p + 0, err_kind.p,
+                                                          scal.p + 1, x.n_chunks, x.chunk, x.chunk_key, x.occ);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     unsigned long long h_scal[2];
@@ -263,7 +322,8 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     if (h_kind) {
         char buf[256];
         snprintf(buf, sizeof buf, "cleora_build: edge %llu: %s", (unsigned long long)h_scal[0],
-                 (h_kind & 1) ? "node id outside [0, n_nodes)" : "weight not finite or <= 0");
+                 (h_kind & 1) ? (x.dst_limit >= 0 ? "node id outside its range" : "node id outside [0, n_nodes)")
+                              : "weight not finite or <= 0");
         return Status::make(3, buf);
     }
     const int64_t n_valid = n_ent - (int64_t)h_scal[1];
@@ -327,14 +387,21 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     dfree(pos2.release(), s);
 
     CL_TRY(row_ptr.alloc((size_t)N + 1, s, "CSR row_ptr"));
-    CL_CUDA_TRY(cudaMemsetAsync(row_ptr.p, 0, sizeof(int64_t), s));
+    // k_row_ptr fills row_ptr[1..N] from the entries; with no entries at all (an empty chunk) it is all 0
+    CL_CUDA_TRY(cudaMemsetAsync(row_ptr.p, 0, nnz == 0 ? ((size_t)N + 1) * sizeof(int64_t) : sizeof(int64_t), s));
     k_row_ptr<<<grid_for(nnz, 4), kThreads, 0, s>>>(rows.p, nnz, N, row_ptr.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
 
     trace("csr: row_ptr", s, true);
     CL_TRY(deg.alloc(N, s, "degree"));
-    k_degree<<<grid_for((int64_t)N * 32, 4), kThreads, 0, s>>>(row_ptr.p, e_ab.p, N, deg.p, scal.p + 2, scal.p + 3);
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int blocks = std::min(grid_for(N, 1), sms * 16);   // 32 rows per warp step, grid-stride
+        k_degree<<<blocks, kThreads, 0, s>>>(row_ptr.p, e_ab.p, N, deg.p, scal.p + 2, scal.p + 3);
+    }
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     trace("csr: degree", s, true);
@@ -429,22 +496,25 @@ __global__ void k_indegree(const int32_t* __restrict__ col, int64_t nnz, int32_t
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride)
         atomicAdd(indeg + (col[k] & kColMask), 1);
 }
-// c[0] += #rows with indeg >= t, c[1] += #rows with indeg >= t + 1
+// c[0] += #rows with indeg >= t, c[1] += #rows with indeg >= t + 1, c[2] += #rows with indeg > 0
 __global__ void k_count_ge(const int32_t* __restrict__ indeg, int32_t N, int32_t t, unsigned long long* __restrict__ c) {
-    unsigned long long a = 0, b = 0;
+    unsigned long long a = 0, b = 0, z = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < N; v += stride) {
         const int32_t x = indeg[v];
         a += x >= t;
         b += x > t;
+        z += x > 0;
     }
     for (int o = 16; o > 0; o >>= 1) {
         a += __shfl_xor_sync(0xffffffffu, a, o);
         b += __shfl_xor_sync(0xffffffffu, b, o);
+        z += __shfl_xor_sync(0xffffffffu, z, o);
     }
-    if ((threadIdx.x & 31) == 0 && (a | b)) {
+    if ((threadIdx.x & 31) == 0 && (a | b | z)) {
         atomicAdd(c, a);
         atomicAdd(c + 1, b);
+        atomicAdd(c + 2, z);
     }
 }
 __global__ void k_tag(int32_t* __restrict__ col, int64_t nnz, const int32_t* __restrict__ indeg, int32_t t) {
@@ -457,7 +527,7 @@ __global__ void k_tag(int32_t* __restrict__ col, int64_t nnz, const int32_t* __r
 }  // namespace
 
 Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes, cudaStream_t s,
-               int64_t* n_hot) {
+               int64_t* n_hot, int64_t* n_ref) {
     // hot rows = the K = budget / row_bytes rows of largest in-degree (exact threshold: the K-th
     // largest in-degree, from a radix sort of the in-degrees; ties at the threshold are kept
     // unless they overshoot the budget by more than a quarter)
@@ -465,7 +535,7 @@ Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_
     DevBuf<unsigned long long> cnt;
     CL_TRY(indeg.alloc(N, s, "in-degree"));
     CL_TRY(sorted.alloc(N, s, "sorted in-degree"));
-    CL_TRY(cnt.alloc(2, s, "hot count"));
+    CL_TRY(cnt.alloc(3, s, "hot count"));
     CL_CUDA_TRY(cudaMemsetAsync(indeg.p, 0, (size_t)N * 4, s));
     k_indegree<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p);
     CL_CUDA_TRY(cudaGetLastError());
@@ -486,11 +556,11 @@ Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_
         CL_CUDA_TRY(cudaStreamSynchronize(s));
         if (t < 2) t = 2;                 // a row read once or never gains nothing from pinning
     }
-    CL_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), s));
+    CL_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, 3 * sizeof(unsigned long long), s));
     k_count_ge<<<grid_for(N, 8), kThreads, 0, s>>>(indeg.p, N, t, cnt.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
-    unsigned long long c[2];
+    unsigned long long c[3];
     CL_CUDA_TRY(cudaMemcpyAsync(c, cnt.p, sizeof c, cudaMemcpyDeviceToHost, s));
     CL_CUDA_TRY(cudaStreamSynchronize(s));
     int64_t nh = (int64_t)c[0];           // rows with in-degree >= t
@@ -498,8 +568,16 @@ Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_
         t += 1;
         nh = (int64_t)c[1];               // rows with in-degree >= t + 1
     }
+    // pin only when the hot rows are re-read far more often than the average gathered row
+    // (power-law graphs); on near-regular graphs (lattices: in-degree <= 6) pinning evicts the
+    // rows whose re-reads are local in time, and everything keeps the normal policy (measured:
+    // c3: threshold 1.4x the mean, 2.09 ms unpinned vs 2.43 ms pinned; c2: 4.7x, 2.70 ms pinned vs
+    // 2.95 ms unpinned)
+    const double avg_in = c[2] ? (double)nnz / (double)c[2] : 0.0;
+    if (t != INT32_MAX && (double)t < 3.0 * avg_in) t = INT32_MAX;
     if (t == INT32_MAX) nh = 0;
     *n_hot = nh;
+    if (n_ref) *n_ref = (int64_t)c[2];
     k_tag<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p, t);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);

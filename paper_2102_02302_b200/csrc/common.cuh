@@ -45,6 +45,14 @@ void count_launches(int64_t n);
 Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what);
 void dfree(void* p, cudaStream_t s);
 
+// SplitMix64 output function (the mixer of the T_0 hash, reading R1, and of the chunk
+// assignment, reading R13).
+__host__ __device__ __forceinline__ uint64_t sm64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
 // ---------------------------------------------------------------- schedule
 // A CTA work item of the heavy path: entries [k0, k1) of row `row`, which is part `part`
 // of `nparts` of that row; `hrow` indexes the row's completion counter; the partial vector
@@ -99,8 +107,18 @@ struct BuildOut {
     double* deg = nullptr;
     int64_t zero_rows = 0, max_degree = 0;
 };
+// Optional parts of a build: keep only the edges of chunk `chunk` of `n_chunks` (Algorithm 1
+// line 1, reading R13), count every node's endpoint occurrences among the kept edges (reading
+// R14; `occ` int32[N], zeroed here), and require dst < dst_limit (inductive CSRs, whose columns
+// index another graph's rows).
+struct BuildExtra {
+    int32_t n_chunks = 0, chunk = 0;
+    uint64_t chunk_key = 0;     // sm64(chunk_seed + 0x9E3779B97F4A7C15)
+    int32_t* occ = nullptr;
+    int32_t dst_limit = -1;     // -1: N
+};
 Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N,
-                 int directed, cudaStream_t s, BuildOut* out);
+                 int directed, cudaStream_t s, BuildOut* out, const BuildExtra* extra = nullptr);
 
 struct Schedule {
     int64_t n_heavy_rows = 0, n_items = 0;
@@ -118,7 +136,7 @@ Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s
 // *n_hot (0 => no row is tagged).  Every reader of col masks bit 31.
 constexpr int32_t kColMask = 0x7fffffff;
 Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes,
-               cudaStream_t s, int64_t* n_hot);
+               cudaStream_t s, int64_t* n_hot, int64_t* n_ref /* rows with in-degree > 0, or NULL */);
 
 // init.cu
 Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s);

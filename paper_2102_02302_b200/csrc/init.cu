@@ -9,12 +9,6 @@ namespace cleora {
 
 namespace {
 
-__host__ __device__ __forceinline__ uint64_t sm64(uint64_t z) {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
-
 constexpr uint64_t kC1 = 0xBF58476D1CE4E5B9ull, kC2 = 0x94D049BB133111EBull;
 
 // The same value as ((int32)(sm64(base ^ j) >> 40) - 2^23) * 2^-23 for 0 <= j < 2^30, with the per-row work hoisted
@@ -58,13 +52,16 @@ __global__ void k_hash_init(float4* __restrict__ T, int64_t N, int32_t d, int32_
     for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < N; v += wstride) {
         const RowHash rh = row_hash(s ^ ((uint64_t)v << 32));
         float4* row = T + v * q;
+#pragma unroll 2
         for (int f = lane; f < q; f += 32) {
-            const uint32_t j0 = 4u * f;
-            float4 o;
-            o.x = (j0 + 0 < (uint32_t)d) ? hash_elem(rh, j0 + 0) : 0.0f;
-            o.y = (j0 + 1 < (uint32_t)d) ? hash_elem(rh, j0 + 1) : 0.0f;
-            o.z = (j0 + 2 < (uint32_t)d) ? hash_elem(rh, j0 + 2) : 0.0f;
-            o.w = (j0 + 3 < (uint32_t)d) ? hash_elem(rh, j0 + 3) : 0.0f;
+            const uint32_t j0 = 4u * f;                  // < d: dp is d rounded up to 4
+            float4 o = make_float4(hash_elem(rh, j0), hash_elem(rh, j0 + 1), hash_elem(rh, j0 + 2),
+                                   hash_elem(rh, j0 + 3));
+            if (j0 + 4 > (uint32_t)d) {                  // the padded tail of a row (d % 4 != 0)
+                o.y = j0 + 1 < (uint32_t)d ? o.y : 0.0f;
+                o.z = j0 + 2 < (uint32_t)d ? o.z : 0.0f;
+                o.w = 0.0f;
+            }
             __stcs(row + f, o);
         }
     }

@@ -1,9 +1,10 @@
 """Multi-rank (N > 1) host logic on CPU with the gloo backend, world_size 2 and 3.
 
-The multi-GPU path row-shards M by nnz balance (cleora_plan_shards), every
-rank computes normalize(M T) for its rows, and each iteration ends with an all-gather-v: one
-broadcast per rank of its row block into every replica (exactly the NCCL calls of api.cu's
-exchange()).  Here each rank computes its rows with the oracle and exchanges them with the same
+The multi-GPU path row-shards M by nnz balance (cleora_plan_shards), every rank
+computes normalize(M T) for its rows, and the rows reach every replica either through the fused
+peer stores of the SpMM epilogue (protocol "peer": stores into all replicas, empty rows skipped once
+clean, a barrier per step) or through the NCCL fallback, an all-gather-v of one broadcast per rank
+(protocol "nccl", exactly the calls of api.cu's exchange()).  Here each rank computes its rows with the oracle and exchanges them with the same
 protocol over gloo; the result must be bitwise equal to the single-process oracle, which pins
 the cut planning, the exchange offsets and the row independence the sharding relies on.
 """
@@ -42,6 +43,12 @@ def _worker(rank, world, port, cfg, q):
         cuts = cl.cleora_plan_shards(M.row_ptr, world)
         r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
         T = torch.from_numpy(oracle.hash_init(g.n, cfg["d"], 0))
+        if cfg.get("protocol") == "peer":
+            T = _peer_protocol(M, T, cuts, rank, world, cfg["iters"])
+            if rank == 0:
+                ref = oracle.embed(M, cfg["d"], 0, cfg["iters"])
+                q.put((T.numpy().tobytes() == ref.tobytes(), [int(c) for c in cuts]))
+            return
         for _ in range(cfg["iters"]):
             out = torch.empty_like(T)
             out[r0:r1] = torch.from_numpy(oracle.step(M, T.numpy(), r0, r1))
@@ -60,11 +67,39 @@ def _worker(rank, world, port, cfg, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,kind", [(2, "cl"), (3, "rmat")])
-def test_sharded_iteration_equals_single_process(world, kind):
+def _peer_protocol(M, T0, cuts, rank, world, iters):
+    """The fused exchange of api.cu (X_PEER) on CPU: each rank holds two replica buffers; in a
+    step it computes its rows [cuts[rank], cuts[rank+1]) from its replica of T_in and stores them
+    into EVERY rank's replica of T_out (here: all_gather_object of the stored rows), skipping rows
+    without entries once that buffer already holds their zeros (zclean bookkeeping), then a
+    barrier orders the steps.  Buffer 1 starts as garbage, so a missed store shows."""
+    import oracle
+    bufs = [T0.clone(), torch.full_like(T0, 7.0)]
+    zclean = [False, False]
+    cur = 0
+    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    empty = (M.row_ptr[1:] == M.row_ptr[:-1])[r0:r1]
+    for _ in range(iters):
+        out = 1 - cur
+        mine = oracle.step(M, bufs[cur].numpy(), r0, r1)
+        write = ~empty if zclean[out] else np.ones(r1 - r0, bool)
+        stores = [None] * world
+        dist.all_gather_object(stores, (r0, r1, write, mine[write]))
+        for b, e, w, vals in stores:
+            blk = bufs[out][b:e]
+            blk[torch.from_numpy(w)] = torch.from_numpy(vals)
+        dist.barrier()
+        zclean[out] = True
+        cur = out
+    return bufs[cur]
+
+
+@pytest.mark.parametrize("world,kind,protocol", [(2, "cl", "nccl"), (3, "rmat", "nccl"), (2, "rmat", "peer"),
+                                                 (3, "cl", "peer")])
+def test_sharded_iteration_equals_single_process(world, kind, protocol):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    cfg = dict(kind=kind, seed=world, d=16, iters=3)
+    cfg = dict(kind=kind, seed=world, d=16, iters=4, protocol=protocol)
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
     for p in procs:
