@@ -75,6 +75,14 @@ typedef struct cleora_opts {
     const uint8_t* nccl_id;  /* world > 1: the 128-byte ncclUniqueId, identical on all ranks;
                                 the library initialises its own communicator from it         */
     int32_t flags;           /* CLEORA_F_* bit set                                              */
+    /* Algorithm 1 with Q > 1 chunks.  n_chunks >= 1: this handle holds chunk
+       `chunk` of n_chunks -- the edges i with q(i) = floor(n_chunks * (h_i >> 32) / 2^32) = chunk,
+       h_i = mix(mix(chunk_seed + 0x9E3779B97F4A7C15) XOR i) (reading R13) -- and counts every
+       node's endpoint occurrences among them (reading R14) for cleora_merge_chunks.
+       n_chunks = 0: the whole graph, no occurrence counts.                                 */
+    int32_t n_chunks;
+    int32_t chunk;
+    uint64_t chunk_seed;
 } cleora_opts;
 
 typedef struct cleora_graph cleora_graph;   /* opaque */
@@ -140,6 +148,38 @@ CLEORA_API int cleora_iterate(cleora_graph* g, int32_t k);
  */
 CLEORA_API int cleora_fetch(const cleora_graph* g, int64_t row_begin, int64_t row_end, float* out,
                  int32_t out_on_device);
+
+/*
+ * cleora_merge_chunks -- Algorithm 1 lines 10-12: out[v] = sum_q w_qv T^q[v]
+ * over the current T of the n_chunks handles (built with opts.n_chunks = n_chunks, chunk = q,
+ * the same chunk_seed and edge list, and initialised with the same d), with
+ *   w_qv = occ_q(v) / sum_k occ_k(v)    (occ = endpoint occurrences, reading R14);
+ * a node in no chunk gets the zero row; no normalisation after the merge (Algorithm 1 has none).
+ * Arithmetic: w in fp64 (one division), fp64 accumulation in ascending q, one rounding to fp32
+ * (bit-exact with the oracle's merge on the same chunk embeddings).
+ *   chunks [n_chunks] handles on one device, same N and d; out: N x d fp32 row-major, host
+ *   (out_on_device = 0) or device memory.  Waits for the chunks' streams and for the copy.
+ *   Errors: EUSAGE (NULL, n_chunks < 1, mixed devices / N / d, a handle without occurrence
+ *   counts or not initialised), EINTERNAL.
+ */
+CLEORA_API int cleora_merge_chunks(cleora_graph* const* chunks, int32_t n_chunks, float* out, int32_t out_on_device);
+
+/*
+ * cleora_reconstruct -- embeddings of n_new unseen nodes ("creation of new node
+ * embedding by weighted averaging of all neighbors' representations"):
+ *   out[i] = normalize( sum_b (e_ib / sum_c e_ic) * T[b] ),  T = g's current T
+ * i.e. one step of the same fused SpMM + row-normalise kernel over the transition rows of the
+ * new nodes (built on the device with readings B1-B4, directed new -> known).  The paper advises
+ * T from iteration I-1: call cleora_iterate(I-1), reconstruct, then cleora_iterate(1).
+ *   new_idx[n_edges] in [0, n_new), known_idx[n_edges] in [0, N), weight[n_edges] > 0 or NULL;
+ *   host arrays, or device arrays with inputs_on_device = 1.  out: n_new x d fp32 row-major,
+ *   host or device.  A new node without edges gets the zero row (reading RZ).  Synchronous.
+ *   Errors: EUSAGE (NULL, n_new < 1, n_edges < 1, before cleora_init), EDATA (an index out of
+ *   range, a weight not finite or <= 0), EINTERNAL.
+ */
+CLEORA_API int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int32_t* known_idx,
+                                  const float* weight, int64_t n_edges, int32_t n_new, int32_t inputs_on_device,
+                                  float* out, int32_t out_on_device);
 
 /* Facts about a handle (all sizes in elements). */
 typedef struct cleora_info_t {

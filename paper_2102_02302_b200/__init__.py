@@ -22,7 +22,7 @@ __all__ = [
     "cleora_build", "cleora_init", "cleora_iterate", "cleora_fetch", "cleora_info", "cleora_stats",
     "cleora_sync", "cleora_destroy", "cleora_last_error", "cleora_fetch_csr", "cleora_set_rows", "cleora_fetch_replica",
     "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
-    "cleora_release_cached_memory",
+    "cleora_release_cached_memory", "cleora_merge_chunks", "cleora_reconstruct",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcleora.so")
@@ -38,7 +38,8 @@ F_TIMING, F_LOOPBACK, F_EXCHANGE_NCCL = 1, 2, 4
 class _Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("input_on_device", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
-                ("flags", ctypes.c_int32)]
+                ("flags", ctypes.c_int32), ("n_chunks", ctypes.c_int32), ("chunk", ctypes.c_int32),
+                ("chunk_seed", ctypes.c_uint64)]
 
 
 class _Info(ctypes.Structure):
@@ -70,6 +71,8 @@ _SIGS = {
     "cleora_fetch_csr": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "cleora_set_rows": (ctypes.c_int, [_vp, _i64, _i64, _vp]),
     "cleora_fetch_replica": (ctypes.c_int, [_vp, _i32, _i64, _i64, _vp]),
+    "cleora_merge_chunks": (ctypes.c_int, [_vp, _i32, _vp, _i32]),
+    "cleora_reconstruct": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _i32]),
     "cleora_nccl_id_size": (ctypes.c_int, []),
     "cleora_nccl_get_unique_id": (ctypes.c_int, [_vp]),
     "cleora_plan_shards": (ctypes.c_int, [_vp, _i64, _i32, _vp]),
@@ -160,7 +163,8 @@ class Graph:
 
 def cleora_build(src, dst, weight, n_nodes: int, directed: bool = False, *, device: int = -1, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None, timing: bool = False,
-                 loopback: bool = False, exchange_nccl: bool = False) -> Graph:
+                 loopback: bool = False, exchange_nccl: bool = False, n_chunks: int = 0, chunk: int = 0,
+                 chunk_seed: int = 0) -> Graph:
     """COO edge list -> device CSR of M = D^-1 A.  See include/cleora.h."""
     ps, ds, ks = _ptr(src, np.int32)
     pd, dd, kd = _ptr(dst, np.int32)
@@ -187,6 +191,7 @@ def cleora_build(src, dst, weight, n_nodes: int, directed: bool = False, *, devi
         o.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
     o.flags = (F_TIMING if timing else 0) | (F_LOOPBACK if loopback else 0) | \
         (F_EXCHANGE_NCCL if exchange_nccl else 0)
+    o.n_chunks, o.chunk, o.chunk_seed = int(n_chunks), int(chunk), int(chunk_seed) & 0xFFFFFFFFFFFFFFFF
     h = ctypes.c_void_p()
     _check(_lib.cleora_build(ps, pd, pw, n, int(n_nodes), 1 if directed else 0, ctypes.byref(o), ctypes.byref(h)))
     return Graph(h.value)
@@ -252,6 +257,45 @@ def cleora_fetch_replica(g: Graph, rank: int, row_begin: int = 0, row_end: int |
         row_end = info["n_nodes"]
     out = np.empty((max(0, row_end - row_begin), info["d"]), np.float32)
     _check(_lib.cleora_fetch_replica(g.handle, int(rank), int(row_begin), int(row_end), out.ctypes.data))
+    return out
+
+
+def cleora_merge_chunks(chunks, out=None):
+    """Algorithm 1 lines 10-12: the occurrence-weighted average of the chunks' current T
+    (handles built with n_chunks / chunk / chunk_seed).  Returns an N x d fp32 array (or `out`)."""
+    chunks = list(chunks)
+    info = cleora_info(chunks[0])
+    if out is None:
+        out = np.empty((info["n_nodes"], info["d"]), np.float32)
+    p, on_dev, keep = _ptr(out, np.float32)
+    if keep is not out:
+        raise CleoraError(EUSAGE, "out must be a contiguous fp32 array")
+    arr = (ctypes.c_void_p * len(chunks))(*[c.handle for c in chunks])
+    _check(_lib.cleora_merge_chunks(ctypes.cast(arr, ctypes.c_void_p), len(chunks), p, 1 if on_dev else 0))
+    return out
+
+
+def cleora_reconstruct(g: Graph, new_idx, known_idx, weight, n_new: int, out=None):
+    """Embeddings of n_new unseen nodes from edges (new_idx[i] -> known_idx[i], weight) against
+    g's current T (use T_{I-1}).  Returns an n_new x d fp32 array (or `out`)."""
+    pn, dn, kn = _ptr(new_idx, np.int32)
+    pk, dk, kk = _ptr(known_idx, np.int32)
+    pw, dw, kw = _ptr(weight, np.float32)
+    if pn is None or pk is None:
+        raise CleoraError(EUSAGE, "new_idx/known_idx required")
+    n_e = int(kn.shape[0])
+    if int(kk.shape[0]) != n_e or (kw is not None and int(kw.shape[0]) != n_e):
+        raise CleoraError(EUSAGE, "new_idx, known_idx, weight must have the same length")
+    on_dev = dn or dk or dw
+    if on_dev and not (dn and dk and (kw is None or dw)):
+        raise CleoraError(EUSAGE, "inputs must be all on the host or all on the device")
+    info = cleora_info(g)
+    if out is None:
+        out = np.empty((int(n_new), info["d"]), np.float32)
+    po, od, ko = _ptr(out, np.float32)
+    if ko is not out:
+        raise CleoraError(EUSAGE, "out must be a contiguous fp32 array")
+    _check(_lib.cleora_reconstruct(g.handle, pn, pk, pw, n_e, int(n_new), 1 if on_dev else 0, po, 1 if od else 0))
     return out
 
 

@@ -290,6 +290,9 @@ struct cleora_graph {
     float* T[2] = {nullptr, nullptr};
     float* partials = nullptr;
     int32_t tag_dp = 0;             // row stride the hot-row tags in col (bit 31) were chosen for
+    int32_t* occ = nullptr;         // chunked builds: endpoint occurrences per node (reading R14)
+    int32_t n_chunks = 0, chunk = 0;
+    uint64_t chunk_seed = 0;
     int64_t n_hot = 0;
     int64_t n_ref = -1;             // rows with in-degree > 0 (known once hot_tag ran)
     int cur = 0;
@@ -551,7 +554,18 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
     }
     trace("build: inputs staged", g->stream, true);
     BuildOut b;
-    Status st = build_csr(dsrc, ddst, dw, E, N, directed, g->stream, &b);
+    BuildExtra bx;
+    if (o && o->n_chunks >= 1) {
+        g->n_chunks = o->n_chunks;
+        g->chunk = o->chunk;
+        g->chunk_seed = o->chunk_seed;
+        CL_TRY(dalloc((void**)&g->occ, (size_t)N * sizeof(int32_t), g->stream, "chunk occurrences"));
+        bx.n_chunks = o->n_chunks;
+        bx.chunk = o->chunk;
+        bx.chunk_key = sm64(o->chunk_seed + 0x9E3779B97F4A7C15ull);
+        bx.occ = g->occ;
+    }
+    Status st = build_csr(dsrc, ddst, dw, E, N, directed, g->stream, &b, &bx);
     trace("build: csr", g->stream, true);
     dfree(bs, g->stream);
     dfree(bd, g->stream);
@@ -635,6 +649,10 @@ int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, in
         if (!opts->nccl_id && !(opts->flags & CLEORA_F_LOOPBACK))
             return usage("cleora_build: world > 1 needs nccl_id");
         if (opts->rank < 0 || opts->rank >= opts->world) return usage("cleora_build: rank outside [0, world)");
+    }
+    if (opts && opts->n_chunks != 0) {
+        if (opts->n_chunks < 0 || opts->chunk < 0 || opts->chunk >= opts->n_chunks)
+            return usage("cleora_build: chunk must be in [0, n_chunks)");
     }
     DeviceGuard guard(opts ? opts->device : -1);
     cleora_graph* g = new cleora_graph();
@@ -819,6 +837,154 @@ int cleora_fetch(const cleora_graph* g, int64_t row_begin, int64_t row_end, floa
     return CLEORA_OK;
 }
 
+int cleora_merge_chunks(cleora_graph* const* chunks, int32_t n_chunks, float* out, int32_t out_on_device) {
+    if (!chunks || !out) return usage("cleora_merge_chunks: NULL argument");
+    if (n_chunks < 1) return usage("cleora_merge_chunks: n_chunks must be >= 1");
+    const cleora_graph* g0 = chunks[0];
+    if (!g0) return usage("cleora_merge_chunks: NULL handle");
+    for (int q = 0; q < n_chunks; q++) {
+        const cleora_graph* g = chunks[q];
+        if (!g) return usage("cleora_merge_chunks: NULL handle");
+        if (g->device != g0->device || g->n != g0->n || g->d != g0->d || g->dp != g0->dp)
+            return usage("cleora_merge_chunks: chunks differ in device, n_nodes or d");
+        if (!g->occ) return usage("cleora_merge_chunks: a handle was built without n_chunks (no occurrence counts)");
+        if (!g->T[0]) return usage("cleora_merge_chunks: a chunk is not initialised");
+    }
+    DeviceGuard guard(g0->device);
+    cudaStream_t s = g0->stream;
+    for (int q = 1; q < n_chunks; q++)
+        if (chunks[q]->stream != s) {
+            cudaError_t e = cudaStreamSynchronize(chunks[q]->stream);
+            if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_merge_chunks: ") + cudaGetErrorString(e)));
+        }
+    std::vector<const void*> h_ptr(2 * (size_t)n_chunks);
+    for (int q = 0; q < n_chunks; q++) {
+        h_ptr[q] = chunks[q]->T[chunks[q]->cur];
+        h_ptr[n_chunks + q] = chunks[q]->occ;
+    }
+    void* d_ptr = nullptr;
+    float* stage = nullptr;
+    const bool direct = out_on_device && g0->d == g0->dp;
+    Status st = dalloc(&d_ptr, h_ptr.size() * sizeof(void*), s, "merge pointer table");
+    if (st.good() && !direct) st = dalloc((void**)&stage, (size_t)g0->n * g0->dp * sizeof(float), s, "merge staging");
+    cudaError_t e = cudaSuccess;
+    if (st.good()) {
+        e = cudaMemcpyAsync(d_ptr, h_ptr.data(), h_ptr.size() * sizeof(void*), cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) st = Status::make(4, std::string("cleora_merge_chunks: ") + cudaGetErrorString(e));
+    }
+    if (st.good())
+        st = launch_merge(reinterpret_cast<const float* const*>(d_ptr),
+                          reinterpret_cast<const int32_t* const*>(reinterpret_cast<const void* const*>(d_ptr) + n_chunks),
+                          n_chunks, g0->n, g0->dp, direct ? out : stage, s);
+    if (st.good() && !direct) {
+        e = cudaMemcpy2DAsync(out, (size_t)g0->d * sizeof(float), stage, (size_t)g0->dp * sizeof(float),
+                              (size_t)g0->d * sizeof(float), (size_t)g0->n,
+                              out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) st = Status::make(4, std::string("cleora_merge_chunks: ") + cudaGetErrorString(e));
+    }
+    e = cudaStreamSynchronize(s);
+    if (st.good() && e != cudaSuccess) st = Status::make(4, std::string("cleora_merge_chunks: ") + cudaGetErrorString(e));
+    dfree(stage, s);
+    dfree(d_ptr, s);
+    if (!st.good()) return fail(st);
+    return CLEORA_OK;
+}
+
+int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int32_t* known_idx, const float* weight,
+                       int64_t n_edges, int32_t n_new, int32_t inputs_on_device, float* out, int32_t out_on_device) {
+    if (!g || !new_idx || !known_idx || !out) return usage("cleora_reconstruct: NULL argument");
+    if (!g->T[0]) return usage("cleora_reconstruct: call cleora_init first");
+    if (n_new < 1) return usage("cleora_reconstruct: n_new must be >= 1");
+    if (n_edges < 1) return usage("cleora_reconstruct: n_edges must be >= 1");
+    DeviceGuard guard(g->device);
+    cudaStream_t s = g->stream;
+    const int32_t N2 = std::max(n_new, g->n);   // row space of the new nodes' transition rows
+    void *bs = nullptr, *bd = nullptr, *bw = nullptr;
+    const int32_t* dsrc = new_idx;
+    const int32_t* ddst = known_idx;
+    const float* dw = weight;
+    Status st = Status::ok();
+    if (!inputs_on_device) {
+        st = dalloc(&bs, n_edges * sizeof(int32_t), s, "reconstruct new_idx");
+        if (st.good()) st = dalloc(&bd, n_edges * sizeof(int32_t), s, "reconstruct known_idx");
+        if (st.good() && weight) st = dalloc(&bw, n_edges * sizeof(float), s, "reconstruct weight");
+        if (st.good()) {
+            cudaMemcpyAsync(bs, new_idx, n_edges * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+            cudaMemcpyAsync(bd, known_idx, n_edges * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+            if (weight) cudaMemcpyAsync(bw, weight, n_edges * sizeof(float), cudaMemcpyHostToDevice, s);
+            dsrc = (const int32_t*)bs;
+            ddst = (const int32_t*)bd;
+            dw = (const float*)bw;
+        }
+    }
+    BuildOut b;
+    Schedule sc;
+    float* Tnew = nullptr;
+    float* parts = nullptr;
+    if (st.good()) {
+        BuildExtra bx;
+        bx.dst_limit = g->n;                     // columns index this graph's rows
+        // new_idx must lie in [0, n_new): validated as a row id below N2, then checked here
+        st = build_csr(dsrc, ddst, dw, n_edges, N2, 1, s, &b, &bx);
+    }
+    if (st.good() && n_new < N2) {
+        // rows in [n_new, N2) must be empty: a new_idx >= n_new is out of range
+        int64_t tail[2] = {0, 0};
+        cudaMemcpyAsync(&tail[0], b.row_ptr + n_new, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(&tail[1], b.row_ptr + N2, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (tail[1] != tail[0]) st = Status::make(3, "cleora_reconstruct: new_idx outside [0, n_new)");
+    }
+    if (st.good()) st = build_schedule(b.row_ptr, N2, 0, n_new, g->heavy_thresh, s, &sc);
+    if (st.good()) st = dalloc((void**)&Tnew, (size_t)n_new * g->dp * sizeof(float), s, "reconstructed rows");
+    if (st.good() && sc.n_items > 0)
+        st = dalloc((void**)&parts, (size_t)sc.n_items * g->dp * sizeof(float), s, "reconstruct partials");
+    if (st.good()) {
+        SpmmArgs a;
+        a.row_ptr = b.row_ptr;
+        a.col = b.col;
+        a.val = b.val;
+        a.T_in = g->T[g->cur];
+        a.T_out = Tnew;
+        a.dp = g->dp;
+        a.r0 = 0;
+        a.r1 = n_new;
+        a.heavy_thresh = g->heavy_thresh;
+        a.items = sc.items;
+        a.n_items = sc.n_items;
+        a.partials = parts;
+        a.counters = sc.counters;
+        a.work = sc.work;
+        a.cold_first = 0;
+        a.n_peers = 0;
+        for (int q = 0; q < kMaxPeers; q++) a.peer_out[q] = nullptr;
+        a.skip_zero_rows = 0;
+        st = launch_spmm_norm(a, s);
+    }
+    if (st.good()) {
+        cudaError_t e = cudaMemcpy2DAsync(out, (size_t)g->d * sizeof(float), Tnew, (size_t)g->dp * sizeof(float),
+                                          (size_t)g->d * sizeof(float), (size_t)n_new,
+                                          out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = Status::make(4, std::string("cleora_reconstruct: ") + cudaGetErrorString(e));
+    }
+    cudaStreamSynchronize(s);
+    dfree(parts, s);
+    dfree(Tnew, s);
+    dfree(sc.items, s);
+    dfree(sc.counters, s);
+    dfree(sc.work, s);
+    dfree(b.row_ptr, s);
+    dfree(b.col, s);
+    dfree(b.val, s);
+    dfree(b.deg, s);
+    dfree(bs, s);
+    dfree(bd, s);
+    dfree(bw, s);
+    if (!st.good()) return fail(st);
+    return CLEORA_OK;
+}
+
 int cleora_fetch_replica(const cleora_graph* g, int32_t rank, int64_t row_begin, int64_t row_end, float* host_out) {
     if (!g || !host_out) return usage("cleora_fetch_replica: NULL argument");
     if (!g->T[0]) return usage("cleora_fetch_replica: call cleora_init first");
@@ -953,6 +1119,7 @@ void cleora_destroy(cleora_graph* g) {
             dfree(sc.work, g->stream);
         }
         dfree(g->d_flag, g->stream);
+        dfree(g->occ, g->stream);
         cudaStreamSynchronize(g->stream);
     }
     for (auto& p : g->ev_spmm) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }

@@ -138,6 +138,11 @@ constexpr int32_t kColMask = 0x7fffffff;
 Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes,
                cudaStream_t s, int64_t* n_hot, int64_t* n_ref /* rows with in-degree > 0, or NULL */);
 
+// chunks.cu: out = sum_q w_qv Tq[q] (Algorithm 1 lines 10-12); d_Tq / d_occ are device arrays
+// of Q device pointers; out and every Tq[q] are N x dp
+Status launch_merge(const float* const* d_Tq, const int32_t* const* d_occ, int Q, int64_t N, int dp, float* d_out,
+                    cudaStream_t s);
+
 // init.cu
 Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s);
 
