@@ -1,0 +1,109 @@
+"""Measurement of the SURVEY §8(f) rows on one B200 (one JSON line):
+
+f1 -- chunked embedding of c2 with Q chunks: per-chunk build + init + I iterations, then
+      cleora_merge_chunks into device memory.  The merge kernel is HBM-bound: its algorithmic
+      bytes are Q*N*dp*4 (chunk rows read) + Q*N*4 (occurrences) + N*dp*4 (merged rows written);
+      achieved = bytes / (CUDA-event time of the merge call, device output, no D2H).
+f2 -- cleora_reconstruct of n_new unseen nodes against c2's T_{I-1}, device inputs and output:
+      new nodes/s and nnz*d/s of the one fused SpMM step it runs.
+Usage: python scripts/bench_next.py [--chunks 4] [--new 200000] [--reps 5]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+import paper_2102_02302_b200 as cl  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--chunks", type=int, default=4)
+ap.add_argument("--new", type=int, default=200_000)
+ap.add_argument("--reps", type=int, default=5)
+args = ap.parse_args()
+
+peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] \
+    if os.path.exists("MEASURED_PEAKS.json") else 6650.0
+g = gen.config(args.config)
+d, iters, Q = g.d, g.iters, args.chunks
+dev = torch.device("cuda", 0)
+s = torch.cuda.Stream()
+src, dst = torch.from_numpy(g.src).to(dev), torch.from_numpy(g.dst).to(dev)
+w = torch.from_numpy(g.w).to(dev) if g.w is not None else None
+torch.cuda.synchronize()
+
+
+def ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+# ---------------------------------------------------------------- f1
+hs = []
+e0, e1 = ev(), ev()
+e0.record(s)
+for q in range(Q):
+    G = cl.cleora_build(src, dst, w, g.n, g.directed, device=0, stream=s.cuda_stream, n_chunks=Q, chunk=q, chunk_seed=1)
+    cl.cleora_init(G, d, 0)
+    cl.cleora_iterate(G, iters)
+    hs.append(G)
+e1.record(s)
+e1.synchronize()
+chunks_ms = e0.elapsed_time(e1)
+nnz_chunks = sum(cl.cleora_info(G)["nnz"] for G in hs)
+out = torch.empty((g.n, d), dtype=torch.float32, device=dev)
+cl.cleora_merge_chunks(hs, out)            # warm-up
+ts = []
+for _ in range(args.reps):
+    torch.cuda.synchronize()
+    a, b = ev(), ev()
+    a.record(s)
+    cl.cleora_merge_chunks(hs, out)        # enqueued on chunk 0's stream (s), synchronous
+    b.record(s)
+    b.synchronize()
+    ts.append(a.elapsed_time(b))
+merge_ms = min(ts)
+dp = (d + 3) // 4 * 4
+merge_bytes = Q * g.n * dp * 4 + Q * g.n * 4 + g.n * dp * 4
+for G in hs:
+    G.close()
+del out
+
+# ---------------------------------------------------------------- f2
+rng = np.random.default_rng(0)
+deg = np.bincount(np.concatenate([g.src, g.dst]), minlength=g.n)
+k = rng.geometric(1 / max(1.0, deg[deg > 0].mean()), args.new).astype(np.int64)      # new-node degrees
+new_idx = torch.from_numpy(np.repeat(np.arange(args.new, dtype=np.int32), k)).to(dev)
+p = deg / deg.sum()                                                                   # preferential attachment
+known = torch.from_numpy(rng.choice(g.n, int(k.sum()), p=p).astype(np.int32)).to(dev)
+G = cl.cleora_build(src, dst, w, g.n, g.directed, device=0, stream=s.cuda_stream)
+cl.cleora_init(G, d, 0)
+cl.cleora_iterate(G, iters - 1)
+rout = torch.empty((args.new, d), dtype=torch.float32, device=dev)
+cl.cleora_reconstruct(G, new_idx, known, None, args.new, rout)
+ts = []
+for _ in range(args.reps):
+    torch.cuda.synchronize()
+    a, b = ev(), ev()
+    a.record(s)
+    cl.cleora_reconstruct(G, new_idx, known, None, args.new, rout)
+    b.record(s)
+    b.synchronize()
+    ts.append(a.elapsed_time(b))
+rec_ms = min(ts)
+G.close()
+
+line = {"what": "SURVEY 8(f) f1 chunked embedding + merge, f2 inductive reconstruction", "config": g.name, "d": d,
+        "f1": {"chunks": Q, "nnz_all_chunks": nnz_chunks, "chunks_build_init_iterate_ms": chunks_ms,
+               "merge_ms": merge_ms, "merge_bytes": merge_bytes,
+               "merge_roofline": {"bound": "hbm", "achieved": merge_bytes / (merge_ms / 1e3) / 1e9, "peak": peak,
+                                  "unit": "GB/s", "frac": merge_bytes / (merge_ms / 1e3) / 1e9 / peak}},
+        "f2": {"new_nodes": args.new, "edges": int(k.sum()), "ms": rec_ms, "new_nodes_per_s": args.new / (rec_ms / 1e3),
+               "nnz_d_per_s": int(k.sum()) * d / (rec_ms / 1e3),
+               "includes": "device-side CSR build of the new nodes' rows + one fused SpMM step + D2D copy"}}
+print(json.dumps(line), flush=True)
