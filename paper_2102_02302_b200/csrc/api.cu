@@ -780,6 +780,8 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
             // (e.g. lattices, whose re-reads are local) they keep the normal policy (measured: c2, c4, c3)
             a.cold_first = getenv("CLEORA_COLD_FIRST") ? atoi(getenv("CLEORA_COLD_FIRST")) : (g->n_hot > 0 ? 1 : 0);
             a.work = sc.work;
+            a.light_start = sc.light_start;
+            a.n_light = sc.n_light;
             a.n_peers = 0;
             for (int q = 0; q < kMaxPeers; q++) a.peer_out[q] = nullptr;
             if (g->xmode == X_LOOPBACK) {
@@ -955,6 +957,8 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
         a.partials = parts;
         a.counters = sc.counters;
         a.work = sc.work;
+        a.light_start = sc.light_start;
+        a.n_light = sc.n_light;
         a.cold_first = 0;
         a.n_peers = 0;
         for (int q = 0; q < kMaxPeers; q++) a.peer_out[q] = nullptr;
@@ -974,6 +978,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
     dfree(sc.items, s);
     dfree(sc.counters, s);
     dfree(sc.work, s);
+    dfree(sc.light_start, s);
     dfree(b.row_ptr, s);
     dfree(b.col, s);
     dfree(b.val, s);
@@ -1112,11 +1117,13 @@ void cleora_destroy(cleora_graph* g) {
             dfree(g->sched.items, g->stream);
             dfree(g->sched.counters, g->stream);
             dfree(g->sched.work, g->stream);
+            dfree(g->sched.light_start, g->stream);
         }
         for (auto& sc : g->sched_p) {      // loopback: g->sched aliases sched_p[rank]
             dfree(sc.items, g->stream);
             dfree(sc.counters, g->stream);
             dfree(sc.work, g->stream);
+            dfree(sc.light_start, g->stream);
         }
         dfree(g->d_flag, g->stream);
         dfree(g->occ, g->stream);

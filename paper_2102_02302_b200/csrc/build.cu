@@ -222,6 +222,17 @@ struct IsHeavy {
     __host__ __device__ bool operator()(int64_t r) const { return rp[r + 1] - rp[r] > thresh; }
 };
 
+// r starts a light chunk: the first row, every kChunkRows-th row, or the first row whose entries
+// begin in a new window of `win` entries (counted from the shard's first entry)
+struct IsChunkStart {
+    const int64_t* rp;
+    int64_t r0, win;
+    __host__ __device__ bool operator()(int64_t r) const {
+        if (r == r0 || (r - r0) % kChunkRows == 0) return true;
+        return (rp[r] - rp[r0]) / win != (rp[r - 1] - rp[r0]) / win;
+    }
+};
+
 __global__ void k_items_per_row(const int64_t* __restrict__ rp, const int64_t* __restrict__ hrows, int64_t nh,
                                 int64_t per_item, int64_t* __restrict__ nit) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -438,6 +449,31 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         out->work = work.release();
     }
     if (nr <= 0) return Status::ok();
+    {
+        // light chunks (see Schedule); window from CLEORA_CHUNK_ENTRIES, default 1024 entries
+        const char* e = getenv("CLEORA_CHUNK_ENTRIES");
+        int64_t win = e ? atoll(e) : 1024;
+        if (win < 1) win = 1;
+        DevBuf<int64_t> starts, cnt1;
+        CL_TRY(starts.alloc(nr + 1, s, "light chunk starts"));
+        CL_TRY(cnt1.alloc(1, s, "scalars"));
+        thrust::counting_iterator<int64_t> it(r0);
+        IsChunkStart pred{d_row_ptr, r0, win};
+        size_t tmp_bytes = 0;
+        CL_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, it, starts.p, cnt1.p, nr, pred, s));
+        DevBuf<uint8_t> tmp;
+        CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
+        CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, starts.p, cnt1.p, nr, pred, s));
+        count_launches(2);
+        int64_t nl = 0;
+        CL_CUDA_TRY(cudaMemcpyAsync(&nl, cnt1.p, sizeof nl, cudaMemcpyDeviceToHost, s));
+        CL_CUDA_TRY(cudaStreamSynchronize(s));
+        const int64_t end = r1;
+        CL_CUDA_TRY(cudaMemcpyAsync(starts.p + nl, &end, sizeof end, cudaMemcpyHostToDevice, s));
+        CL_CUDA_TRY(cudaStreamSynchronize(s));   // `end` lives on this stack frame
+        out->n_light = nl;
+        out->light_start = starts.release();
+    }
     DevBuf<int64_t> hrows, cnt;
     CL_TRY(hrows.alloc(nr, s, "heavy rows"));
     CL_TRY(cnt.alloc(2, s, "scalars"));

@@ -81,6 +81,8 @@ struct SpmmArgs {
     float* partials;        // n_items * dp floats
     unsigned* counters;     // one per heavy row, 0 between launches
     unsigned* work;         // 3 work tickets of the persistent kernel, 0 between launches
+    const int64_t* light_start;   // light chunks (Schedule::light_start)
+    int64_t n_light;
     int32_t cold_first;     // TMA path: gathers of non-hot rows with evict_first (else evict_normal)
     // Fused exchange (multi-GPU): every finished row is also stored into the T_out replicas of
     // the other ranks -- NVLink peer pointers opened through CUDA IPC, or, in loopback
@@ -120,11 +122,18 @@ struct BuildExtra {
 Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N,
                  int directed, cudaStream_t s, BuildOut* out, const BuildExtra* extra = nullptr);
 
+// Light-row work units: chunks [light_start[c], light_start[c+1]) of at most kChunkRows
+// consecutive rows whose entries start within one window of `chunk_entries` entries, so a
+// ticket's work is bounded in rows (row pointers fit one register per lane) and in entries
+// (no long tail behind a chunk of medium-degree rows).
+constexpr int kChunkRows = 31;
 struct Schedule {
     int64_t n_heavy_rows = 0, n_items = 0;
     HeavyItem* items = nullptr;
     unsigned* counters = nullptr;
     unsigned* work = nullptr;   // [4] persistent-kernel tickets
+    int64_t* light_start = nullptr;   // [n_light + 1]
+    int64_t n_light = 0;
 };
 Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int heavy_thresh,
                       cudaStream_t s, Schedule* out);

@@ -206,11 +206,10 @@ __device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* 
 
 // Persistent kernel: one wave of CTAs (SM count x resident CTAs per SM).  Work is handed out
 // dynamically through global tickets so that no warp waits for another: CTAs first take heavy
-// items one at a time (a.work[0]); then every warp takes chunks of kChunk consecutive light rows
+// items one at a time (a.work[0]); then every warp takes light chunks (<= 31 consecutive rows)
 // (a.work[1]).  The last warp to finish resets the tickets (a.work[2] counts finished warps), so
 // the counters are 0 again at the next launch.  Which warp computes a row never changes its
 // arithmetic, so results stay bitwise deterministic.
-constexpr int kChunk = 16;
 
 template <int V>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_norm(const SpmmArgs a) {
@@ -229,14 +228,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_norm(const SpmmAr
             heavy_item<V>(a, it, red, scratch, &flag);
         }
     }
-    const int64_t nchunks = (a.r1 - a.r0 + kChunk - 1) / kChunk;
+    const int64_t nchunks = a.n_light;
     for (;;) {
         unsigned c = 0;
         if (lane == 0) c = atomicAdd(a.work + 1, 1u);
         c = __shfl_sync(kFull, c, 0);
         if ((int64_t)c >= nchunks) break;
-        const int64_t rb = a.r0 + (int64_t)c * kChunk;
-        const int64_t re = min(rb + kChunk, a.r1);
+        const int64_t rb = a.light_start[c];
+        const int64_t re = a.light_start[c + 1];
         const int64_t rpl = (lane <= re - rb) ? a.row_ptr[rb + lane] : 0;
         for (int64_t r = rb; r < re; r++) {
             const int64_t k0 = __shfl_sync(kFull, rpl, (int)(r - rb));

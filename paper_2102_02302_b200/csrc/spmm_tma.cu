@@ -8,7 +8,8 @@
 // SM) instead of the register file, which is what a latency-bound gather needs; registers only
 // hold the fp32 accumulator (dp/32 floats per lane).
 //
-// Light rows (<= heavy_thresh entries): a warp takes a ticket for kChunk consecutive rows and
+// Light rows (<= heavy_thresh entries): a warp takes a ticket for a light chunk (<= 31 consecutive
+// rows, entry-bounded, see Schedule) and
 // streams their entries flat through its ring -- the pipeline keeps running across row
 // boundaries, where the finished row is reduced (fp64 sum of squares, warp shuffles), scaled
 // and written with 16-byte streaming stores.  Heavy rows: CTA work items; each warp streams a
@@ -94,7 +95,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-constexpr int kChunk = 31;    // rows per light ticket: their 32 row pointers fit one register per lane
 
 struct Ring {
     float4* buf;       // S slots of slot_f4 float4
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
             heavy_item_t<V, FULL>(a, it, r, smem, ring_f4, scratch, &flag);
         }
     }
-    const int64_t nchunks = (a.r1 - a.r0 + kChunk - 1) / kChunk;
+    const int64_t nchunks = a.n_light;
     float4 acc[V];
 #pragma unroll
     for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -329,8 +329,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
         if (lane == 0) c = atomicAdd(a.work + 1, 1u);
         c = __shfl_sync(kFull, c, 0);
         if ((int64_t)c >= nchunks) break;
-        const int64_t rb = a.r0 + (int64_t)c * kChunk;
-        const int64_t re = min(rb + kChunk, a.r1);
+        const int64_t rb = a.light_start[c];
+        const int64_t re = a.light_start[c + 1];
         const int64_t rpl = (lane <= re - rb) ? a.row_ptr[rb + lane] : 0;
         int64_t row = rb;
         while (row < re) {   // segments of consecutive light rows; heavy rows are skipped
