@@ -113,6 +113,26 @@ CLEORA_API int cleora_build(const int32_t* src, const int32_t* dst, const float*
                  int32_t n_nodes, int32_t directed, const cleora_opts* opts, cleora_graph** out);
 
 /*
+ * cleora_build_batch -- many independent graphs in ONE handle (several M, e.g.
+ * one per relation pair of a table -- "a separate embedding matrix for each relation pair",
+ * in one launch per step).  The handle holds the block-diagonal M of
+ * the graphs; every step is one fused SpMM launch over all of them.
+ *   edge_ptr [n_graphs + 1] int64 (host): graph g's edges are entries [edge_ptr[g], edge_ptr[g+1])
+ *            of src / dst / weight, with node ids LOCAL to g in [0, node_count[g]).
+ *   node_count [n_graphs] int32 (host), each >= 1.
+ *   src, dst, weight, directed, opts: as cleora_build (host or device per opts; one GPU only).
+ * Graph g's rows are rows [base_g, base_g + node_count[g]) of the handle, base_g = sum of the
+ * node counts before g (fetch them with cleora_fetch).  T_0 is keyed on the LOCAL id, so every
+ * graph's embedding is bitwise the one cleora_build of that graph alone would give.
+ *   Errors: EUSAGE (NULL, n_graphs < 1, a node_count < 1, edge_ptr not non-decreasing from 0,
+ *   no edges, world > 1 or n_chunks set), EDATA (a local id out of its graph's range, bad weight),
+ *   EINTERNAL.
+ */
+CLEORA_API int cleora_build_batch(const int32_t* src, const int32_t* dst, const float* weight,
+                                  const int64_t* edge_ptr, const int32_t* node_count, int32_t n_graphs,
+                                  int32_t directed, const cleora_opts* opts, cleora_graph** out);
+
+/*
  * cleora_init -- allocate the two N x d fp32 embedding buffers and set T <- T_0 with
  *   T_0[v][j] = ((int32)(h >> 40) - 2^23) * 2^-23,
  *   h = mix(mix(seed + 0x9E3779B97F4A7C15) XOR (v << 32 | j)), mix = SplitMix64 finaliser
@@ -200,6 +220,7 @@ typedef struct cleora_info_t {
     int64_t hot_rows;       /* rows whose gathers carry the L2 evict_last hint (0 = none) */
     int64_t referenced_rows;/* rows with in-degree > 0, i.e. ever gathered (-1: unknown)  */
     int32_t exchange;       /* 0 one GPU, 1 NCCL all-gather, 2 fused peer stores, 3 loopback */
+    int32_t n_graphs;       /* graphs in a batched handle (cleora_build_batch), else 0   */
 } cleora_info_t;
 CLEORA_API int cleora_info(const cleora_graph* g, cleora_info_t* out);
 

@@ -22,7 +22,7 @@ __all__ = [
     "cleora_build", "cleora_init", "cleora_iterate", "cleora_fetch", "cleora_info", "cleora_stats",
     "cleora_sync", "cleora_destroy", "cleora_last_error", "cleora_fetch_csr", "cleora_set_rows", "cleora_fetch_replica",
     "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
-    "cleora_release_cached_memory", "cleora_merge_chunks", "cleora_reconstruct",
+    "cleora_release_cached_memory", "cleora_merge_chunks", "cleora_reconstruct", "cleora_build_batch",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcleora.so")
@@ -48,7 +48,8 @@ class _Info(ctypes.Structure):
                 ("zero_rows", ctypes.c_int64), ("max_degree", ctypes.c_int64), ("heavy_rows", ctypes.c_int64),
                 ("heavy_items", ctypes.c_int64), ("shard_begin", ctypes.c_int64), ("shard_end", ctypes.c_int64),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
-                ("hot_rows", ctypes.c_int64), ("referenced_rows", ctypes.c_int64), ("exchange", ctypes.c_int32)]
+                ("hot_rows", ctypes.c_int64), ("referenced_rows", ctypes.c_int64), ("exchange", ctypes.c_int32),
+                ("n_graphs", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -61,6 +62,7 @@ _vp, _i32, _i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
 _SIGS = {
     "cleora_build": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i32, _i32, ctypes.POINTER(_Opts), ctypes.POINTER(_vp)]),
     "cleora_init": (ctypes.c_int, [_vp, _i32, ctypes.c_uint64]),
+    "cleora_build_batch": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, ctypes.POINTER(_Opts), ctypes.POINTER(_vp)]),
     "cleora_iterate": (ctypes.c_int, [_vp, _i32]),
     "cleora_fetch": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i32]),
     "cleora_info": (ctypes.c_int, [_vp, ctypes.POINTER(_Info)]),
@@ -194,6 +196,39 @@ def cleora_build(src, dst, weight, n_nodes: int, directed: bool = False, *, devi
     o.n_chunks, o.chunk, o.chunk_seed = int(n_chunks), int(chunk), int(chunk_seed) & 0xFFFFFFFFFFFFFFFF
     h = ctypes.c_void_p()
     _check(_lib.cleora_build(ps, pd, pw, n, int(n_nodes), 1 if directed else 0, ctypes.byref(o), ctypes.byref(h)))
+    return Graph(h.value)
+
+
+def cleora_build_batch(src, dst, weight, edge_ptr, node_count, directed: bool = False, *, device: int = -1,
+                       stream=None, timing: bool = False) -> Graph:
+    """Several independent graphs in one handle (block-diagonal M, one launch per step; SURVEY
+    §8(f) f4).  Graph g: edges [edge_ptr[g], edge_ptr[g+1]) with LOCAL ids; its rows are
+    [sum(node_count[:g]), +node_count[g]).  See include/cleora.h."""
+    ps, ds, ks = _ptr(src, np.int32)
+    pd, dd, kd = _ptr(dst, np.int32)
+    pw, dw, kw = _ptr(weight, np.float32)
+    ep = np.ascontiguousarray(edge_ptr, np.int64)
+    nc = np.ascontiguousarray(node_count, np.int32)
+    if ps is None or pd is None:
+        raise CleoraError(EUSAGE, "src/dst required")
+    n = int(ks.shape[0])
+    if int(kd.shape[0]) != n or (kw is not None and int(kw.shape[0]) != n) or int(ep[-1]) != n:
+        raise CleoraError(EUSAGE, "src, dst, weight and edge_ptr[-1] must agree")
+    on_dev = ds or dd or dw
+    if on_dev and not (ds and dd and (kw is None or dw)):
+        raise CleoraError(EUSAGE, "src/dst/weight must be all on the host or all on the device")
+    if on_dev and device < 0:
+        device = int(ks.device.index or 0)
+    o = _Opts()
+    o.device = device
+    o.input_on_device = 1 if on_dev else 0
+    if stream is not None:
+        o.stream = stream if isinstance(stream, int) else int(getattr(stream, "cuda_stream", stream))
+    o.world = 1
+    o.flags = F_TIMING if timing else 0
+    h = ctypes.c_void_p()
+    _check(_lib.cleora_build_batch(ps, pd, pw, ep.ctypes.data, nc.ctypes.data, int(nc.shape[0]), 1 if directed else 0,
+                                   ctypes.byref(o), ctypes.byref(h)))
     return Graph(h.value)
 
 

@@ -263,7 +263,10 @@ static Nccl& nccl() {
 
 static int heavy_thresh_default() {
     const char* e = getenv("CLEORA_HEAVY_THRESH");
-    int v = e ? atoi(e) : 64;
+    // 256: rows up to 256 entries stream on the warp path (measured: c5 427 -> 375 ms per step,
+    // c2 / c4 unchanged vs 64); every sequential fp32 run stays <= 256 terms (SURVEY §0.4:
+    // 256-entry blocks keep the error ~3e-7)
+    int v = e ? atoi(e) : 256;
     if (v < 8) v = 8;
     if (v > 4096) v = 4096;
     return v;
@@ -291,6 +294,8 @@ struct cleora_graph {
     float* partials = nullptr;
     int32_t tag_dp = 0;             // row stride the hot-row tags in col (bit 31) were chosen for
     int32_t* occ = nullptr;         // chunked builds: endpoint occurrences per node (reading R14)
+    int32_t n_graphs = 0;           // batched handles (cleora_build_batch): graphs in the batch
+    int64_t* d_base = nullptr;      //   [n_graphs + 1] first row of every graph (device)
     int32_t n_chunks = 0, chunk = 0;
     uint64_t chunk_seed = 0;
     int64_t n_hot = 0;
@@ -504,8 +509,14 @@ Status exchange(cleora_graph* g, float* buf) {
     return Status::ok();
 }
 
+struct BatchSpec {
+    const int64_t* edge_ptr;    // host [n_graphs + 1]
+    const int32_t* node_count;  // host [n_graphs]
+    int32_t n_graphs;
+};
+
 Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t E, int32_t N, int directed,
-                const cleora_opts* o, cleora_graph* g) {
+                const cleora_opts* o, cleora_graph* g, const BatchSpec* batch = nullptr) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
@@ -554,6 +565,35 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
     }
     trace("build: inputs staged", g->stream, true);
     BuildOut b;
+    // batched handle: local ids -> rows of the block-diagonal M
+    void *gs = nullptr, *gd = nullptr;
+    if (batch) {
+        std::vector<int64_t> base(batch->n_graphs + 1, 0);
+        for (int i = 0; i < batch->n_graphs; i++) base[i + 1] = base[i] + batch->node_count[i];
+        g->n_graphs = batch->n_graphs;
+        void* d_ep = nullptr;
+        Status st0 = dalloc((void**)&g->d_base, base.size() * sizeof(int64_t), g->stream, "batch bases");
+        if (st0.good()) st0 = dalloc(&d_ep, base.size() * sizeof(int64_t), g->stream, "batch edge offsets");
+        if (st0.good()) st0 = dalloc(&gs, E * sizeof(int32_t), g->stream, "batch src");
+        if (st0.good()) st0 = dalloc(&gd, E * sizeof(int32_t), g->stream, "batch dst");
+        if (st0.good()) {
+            cudaMemcpyAsync(g->d_base, base.data(), base.size() * sizeof(int64_t), cudaMemcpyHostToDevice, g->stream);
+            cudaMemcpyAsync(d_ep, batch->edge_ptr, base.size() * sizeof(int64_t), cudaMemcpyHostToDevice, g->stream);
+            st0 = batch_global_ids(dsrc, ddst, E, (const int64_t*)d_ep, g->d_base, batch->n_graphs, g->stream,
+                                   (int32_t*)gs, (int32_t*)gd);
+        }
+        dfree(d_ep, g->stream);
+        if (!st0.good()) {
+            dfree(gs, g->stream);
+            dfree(gd, g->stream);
+            dfree(bs, g->stream);
+            dfree(bd, g->stream);
+            dfree(bw, g->stream);
+            return st0;
+        }
+        dsrc = (const int32_t*)gs;
+        ddst = (const int32_t*)gd;
+    }
     BuildExtra bx;
     if (o && o->n_chunks >= 1) {
         g->n_chunks = o->n_chunks;
@@ -570,6 +610,8 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
     dfree(bs, g->stream);
     dfree(bd, g->stream);
     dfree(bw, g->stream);
+    dfree(gs, g->stream);
+    dfree(gd, g->stream);
     if (!st.good()) return st;
     g->nnz = b.nnz;
     g->row_ptr = b.row_ptr;
@@ -665,6 +707,37 @@ int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, in
     return CLEORA_OK;
 }
 
+int cleora_build_batch(const int32_t* src, const int32_t* dst, const float* weight, const int64_t* edge_ptr,
+                       const int32_t* node_count, int32_t n_graphs, int32_t directed, const cleora_opts* opts,
+                       cleora_graph** out) {
+    if (!out) return usage("cleora_build_batch: out is NULL");
+    *out = nullptr;
+    if (!src || !dst || !edge_ptr || !node_count) return usage("cleora_build_batch: NULL argument");
+    if (n_graphs < 1) return usage("cleora_build_batch: n_graphs must be >= 1");
+    if (edge_ptr[0] != 0) return usage("cleora_build_batch: edge_ptr[0] must be 0");
+    int64_t ntot = 0;
+    for (int i = 0; i < n_graphs; i++) {
+        if (node_count[i] < 1) return usage("cleora_build_batch: every node_count must be >= 1");
+        if (edge_ptr[i + 1] < edge_ptr[i]) return usage("cleora_build_batch: edge_ptr must be non-decreasing");
+        ntot += node_count[i];
+    }
+    if (ntot > INT32_MAX) return usage("cleora_build_batch: the batch has more than 2^31-1 nodes");
+    const int64_t E = edge_ptr[n_graphs];
+    if (E <= 0) return usage("cleora_build_batch: the batch has no edges");
+    if (opts && (opts->world > 1 || opts->n_chunks != 0))
+        return usage("cleora_build_batch: batches are single-GPU and unchunked");
+    DeviceGuard guard(opts ? opts->device : -1);
+    cleora_graph* g = new cleora_graph();
+    BatchSpec b{edge_ptr, node_count, n_graphs};
+    Status s = do_build(src, dst, weight, E, (int32_t)ntot, directed ? 1 : 0, opts, g, &b);
+    if (!s.good()) {
+        cleora_destroy(g);
+        return fail(s);
+    }
+    *out = g;
+    return CLEORA_OK;
+}
+
 int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     if (!g) return usage("cleora_init: graph is NULL");
     if (d < 1 || d > CLEORA_MAX_D) return usage("cleora_init: d must be in [1, CLEORA_MAX_D]");
@@ -727,12 +800,12 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
         }
         g->tag_dp = dp;
     }
-    Status s = launch_hash_init(g->T[0], g->n, d, dp, seed, g->stream);
+    Status s = launch_hash_init(g->T[0], g->n, d, dp, seed, g->stream, g->d_base, g->n_graphs);
     if (!s.good()) return fail(s);
     if (g->xmode == X_LOOPBACK)   // every emulated rank initialises its own replica
         for (int p = 0; p < g->world; p++)
             if (p != g->rank) {
-                s = launch_hash_init(g->rep[p][0], g->n, d, dp, seed, g->stream);
+                s = launch_hash_init(g->rep[p][0], g->n, d, dp, seed, g->stream, g->d_base, g->n_graphs);
                 if (!s.good()) return fail(s);
             }
     if (g->xmode == X_PEER) {
@@ -1066,6 +1139,7 @@ int cleora_info(const cleora_graph* g, cleora_info_t* o) {
     o->rank = g->rank;
     o->world = g->world;
     o->hot_rows = g->n_hot;
+    o->n_graphs = g->n_graphs;
     o->referenced_rows = g->n_ref;
     o->exchange = g->xmode;
     o->device_bytes = g->bytes + (g->T[0] ? 2 * (int64_t)g->n * g->dp * 4 : 0) +
@@ -1127,6 +1201,7 @@ void cleora_destroy(cleora_graph* g) {
         }
         dfree(g->d_flag, g->stream);
         dfree(g->occ, g->stream);
+        dfree(g->d_base, g->stream);
         cudaStreamSynchronize(g->stream);
     }
     for (auto& p : g->ev_spmm) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }

@@ -620,6 +620,51 @@ Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_
     return Status::ok();
 }
 
+namespace {
+__global__ void k_batch_ids(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t E,
+                            const int64_t* __restrict__ edge_ptr, const int64_t* __restrict__ base, int32_t n_graphs,
+                            int32_t* __restrict__ gsrc, int32_t* __restrict__ gdst,
+                            unsigned long long* __restrict__ err_first) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += stride) {
+        int lo = 0, hi = n_graphs - 1;                // graph of edge i: last g with edge_ptr[g] <= i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (edge_ptr[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        const int64_t b = base[lo], cnt = base[lo + 1] - b;
+        const int32_t u = src[i], v = dst[i];
+        if (u < 0 || u >= cnt || v < 0 || v >= cnt) {
+            atomicMin(err_first, (unsigned long long)i);
+            gsrc[i] = (int32_t)b;
+            gdst[i] = (int32_t)b;
+        } else {
+            gsrc[i] = (int32_t)(b + u);
+            gdst[i] = (int32_t)(b + v);
+        }
+    }
+}
+}  // namespace
+
+Status batch_global_ids(const int32_t* d_src, const int32_t* d_dst, int64_t E, const int64_t* d_edge_ptr,
+                        const int64_t* d_base, int32_t n_graphs, cudaStream_t s, int32_t* d_gsrc, int32_t* d_gdst) {
+    DevBuf<unsigned long long> err;
+    CL_TRY(err.alloc(1, s, "batch error"));
+    CL_CUDA_TRY(cudaMemsetAsync(err.p, 0xFF, sizeof(unsigned long long), s));
+    k_batch_ids<<<grid_for(E, 4), kThreads, 0, s>>>(d_src, d_dst, E, d_edge_ptr, d_base, n_graphs, d_gsrc, d_gdst, err.p);
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    unsigned long long h = 0;
+    CL_CUDA_TRY(cudaMemcpyAsync(&h, err.p, sizeof h, cudaMemcpyDeviceToHost, s));
+    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h != ~0ull) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "cleora_build_batch: edge %llu: node id outside [0, node_count) of its graph", h);
+        return Status::make(3, buf);
+    }
+    return Status::ok();
+}
+
 Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts) {
     DevBuf<int64_t> cuts;
     CL_TRY(cuts.alloc(world + 1, s, "shard cuts"));

@@ -153,7 +153,14 @@ Status launch_merge(const float* const* d_Tq, const int32_t* const* d_occ, int Q
                     cudaStream_t s);
 
 // init.cu
-Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s);
+Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s,
+                        const int64_t* d_base = nullptr, int32_t n_graphs = 0);
+
+// build.cu, batched handles: global ids = local ids + base[graph of the edge]; edge_ptr and
+// base are [n_graphs + 1] device arrays.  Returns EDATA (with the first bad edge) for a local id
+// outside its graph.
+Status batch_global_ids(const int32_t* d_src, const int32_t* d_dst, int64_t E, const int64_t* d_edge_ptr,
+                        const int64_t* d_base, int32_t n_graphs, cudaStream_t s, int32_t* d_gsrc, int32_t* d_gdst);
 
 // spmm_norm.cu (register gathers; any d) and spmm_tma.cu (TMA bulk gathers; dp <= 1024)
 Status launch_spmm_norm(const SpmmArgs& a, cudaStream_t s);

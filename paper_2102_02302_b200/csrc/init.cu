@@ -45,12 +45,24 @@ __device__ __forceinline__ float hash_elem(const RowHash& r, uint32_t j) {
 
 // One warp per row (grid-stride over rows): lane l writes float4 columns l, l+32, ... -- no
 // 64-bit division per element, 512 contiguous bytes per warp store instruction.
-__global__ void k_hash_init(float4* __restrict__ T, int64_t N, int32_t d, int32_t dp, uint64_t s) {
+// base (batched handles, NULL otherwise): [n_graphs + 1] first row of every graph; the hash then
+// keys on the row's id local to its graph, so each graph of a batch gets its own T_0.
+__global__ void k_hash_init(float4* __restrict__ T, int64_t N, int32_t d, int32_t dp, uint64_t s,
+                            const int64_t* __restrict__ base, int32_t n_graphs) {
     const int lane = threadIdx.x & 31;
     const int q = dp / 4;
     const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < N; v += wstride) {
-        const RowHash rh = row_hash(s ^ ((uint64_t)v << 32));
+        int64_t id = v;
+        if (base) {                                  // graph of row v: last g with base[g] <= v
+            int lo = 0, hi = n_graphs - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (base[mid] <= v) lo = mid; else hi = mid - 1;
+            }
+            id = v - base[lo];
+        }
+        const RowHash rh = row_hash(s ^ ((uint64_t)id << 32));
         float4* row = T + v * q;
 #pragma unroll 2
         for (int f = lane; f < q; f += 32) {
@@ -69,7 +81,8 @@ __global__ void k_hash_init(float4* __restrict__ T, int64_t N, int32_t d, int32_
 
 }  // namespace
 
-Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s) {
+Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s,
+                        const int64_t* d_base, int32_t n_graphs) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -78,7 +91,7 @@ Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t see
     const int64_t cap = (int64_t)sms * 8 * 4;            // ... grid-stride, a multiple of the SM count
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    k_hash_init<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4*>(T), N, d, dp, key);
+    k_hash_init<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4*>(T), N, d, dp, key, d_base, n_graphs);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     return Status::ok();

@@ -6,6 +6,9 @@ f1 -- chunked embedding of c2 with Q chunks: per-chunk build + init + I iteratio
       achieved = bytes / (CUDA-event time of the merge call, device output, no D2H).
 f2 -- cleora_reconstruct of n_new unseen nodes against c2's T_{I-1}, device inputs and output:
       new nodes/s and nnz*d/s of the one fused SpMM step it runs.
+f4 -- many small graphs (2,000 Erdos-Renyi graphs, N log-uniform in [50, 5000], 4N edges each,
+      d = 128, I = 4): one batched handle (block-diagonal M, one launch per step) against the same
+      graphs one handle at a time (a prefix of 200 graphs, scaled), device-resident inputs.
 Usage: python scripts/bench_next.py [--chunks 4] [--new 200000] [--reps 5]
 """
 import argparse
@@ -98,12 +101,71 @@ for _ in range(args.reps):
 rec_ms = min(ts)
 G.close()
 
-line = {"what": "SURVEY 8(f) f1 chunked embedding + merge, f2 inductive reconstruction", "config": g.name, "d": d,
+# ---------------------------------------------------------------- f4
+rng = np.random.default_rng(1)
+ns = np.exp(rng.uniform(np.log(50), np.log(5000), 2000)).astype(np.int64)
+graphs = [gen.er(int(n), int(4 * n), seed=100 + i) for i, n in enumerate(ns)]
+ep = np.zeros(len(graphs) + 1, np.int64)
+ep[1:] = np.cumsum([x.n_edges for x in graphs])
+bsrc = torch.from_numpy(np.concatenate([x.src for x in graphs])).to(dev)
+bdst = torch.from_numpy(np.concatenate([x.dst for x in graphs])).to(dev)
+nc = np.array([x.n for x in graphs], np.int32)
+d4, it4 = 128, 4
+
+
+def batch_step(timing=False):
+    B = cl.cleora_build_batch(bsrc, bdst, None, ep, nc, False, device=0, stream=s.cuda_stream, timing=timing)
+    cl.cleora_init(B, d4, 0)
+    cl.cleora_iterate(B, it4)
+    return B
+
+
+batch_step().close()
+ts = []
+for _ in range(args.reps):
+    torch.cuda.synchronize()
+    a, b = ev(), ev()
+    a.record(s)
+    B = batch_step()
+    B.close()
+    b.record(s)
+    b.synchronize()
+    ts.append(a.elapsed_time(b))
+batch_ms = min(ts)
+B = batch_step(timing=True)
+st = cl.cleora_stats(B)
+info = cl.cleora_info(B)
+B.close()
+nnz4 = info["nnz"]
+spmm4 = st["spmm_ms_total"] / max(1, st["spmm_launches"])
+b4 = 8 * (info["n_nodes"] + 1) + 8 * nnz4 + 2 * info["n_nodes"] * d4 * 4
+gs = [(torch.from_numpy(x.src).to(dev), torch.from_numpy(x.dst).to(dev), x.n) for x in graphs[:200]]
+torch.cuda.synchronize()
+a, b = ev(), ev()
+a.record(s)
+for xs, xd, xn in gs:
+    G = cl.cleora_build(xs, xd, None, xn, False, device=0, stream=s.cuda_stream)
+    cl.cleora_init(G, d4, 0)
+    cl.cleora_iterate(G, it4)
+    G.close()
+b.record(s)
+b.synchronize()
+seq_ms = a.elapsed_time(b) * len(graphs) / len(gs)
+
+line = {"what": "SURVEY 8(f) f1 chunked embedding + merge, f2 inductive reconstruction, f4 batched graphs",
+        "config": g.name, "d": d,
         "f1": {"chunks": Q, "nnz_all_chunks": nnz_chunks, "chunks_build_init_iterate_ms": chunks_ms,
                "merge_ms": merge_ms, "merge_bytes": merge_bytes,
                "merge_roofline": {"bound": "hbm", "achieved": merge_bytes / (merge_ms / 1e3) / 1e9, "peak": peak,
                                   "unit": "GB/s", "frac": merge_bytes / (merge_ms / 1e3) / 1e9 / peak}},
         "f2": {"new_nodes": args.new, "edges": int(k.sum()), "ms": rec_ms, "new_nodes_per_s": args.new / (rec_ms / 1e3),
                "nnz_d_per_s": int(k.sum()) * d / (rec_ms / 1e3),
-               "includes": "device-side CSR build of the new nodes' rows + one fused SpMM step + D2D copy"}}
+               "includes": "device-side CSR build of the new nodes' rows + one fused SpMM step + D2D copy"},
+        "f4": {"graphs": len(graphs), "nodes": info["n_nodes"], "nnz": nnz4, "d": d4, "iterations": it4,
+               "batched_step_ms": batch_ms, "batched_graphs_per_s": len(graphs) / (batch_ms / 1e3),
+               "batched_nnz_d_per_s": nnz4 * d4 * it4 / (batch_ms / 1e3),
+               "one_at_a_time_ms": seq_ms, "speedup": seq_ms / batch_ms,
+               "spmm_ms_per_launch": spmm4,
+               "spmm_roofline": {"bound": "hbm", "achieved": b4 / (spmm4 / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                                 "frac": b4 / (spmm4 / 1e3) / 1e9 / peak}}}
 print(json.dumps(line), flush=True)

@@ -58,6 +58,14 @@ def test_usage_errors_are_host_side():
     with pytest.raises(cl.CleoraError) as e:
         cl.cleora_build(np.array([0], np.int32), np.array([1], np.int32), None, 2, world=2, rank=0)
     assert e.value.code == cl.EUSAGE and "nccl_id" in str(e.value)
+    one = np.array([0], np.int32)
+    for ep, nc, why in (([0, 1], [0], "node_count"), ([1, 1], [2], "edge_ptr[0]"), ([0, 2, 1], [2, 2], "non-decreasing")):
+        with pytest.raises(cl.CleoraError) as e:
+            cl.cleora_build_batch(one, one, None, np.array(ep, np.int64), np.array(nc, np.int32))
+        assert e.value.code == cl.EUSAGE and why in str(e.value), why
+    with pytest.raises(cl.CleoraError) as e:
+        cl.cleora_build(one, one, None, 2, n_chunks=2, chunk=3)
+    assert e.value.code == cl.EUSAGE and "chunk" in str(e.value)
 
 
 def test_plan_shards_balances_nnz():
