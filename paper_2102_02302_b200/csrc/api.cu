@@ -787,7 +787,7 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     g->cur = 0;
     g->iters = 0;
     g->zclean[0] = g->zclean[1] = false;
-    if (g->tag_dp != dp && tma_path_supported(dp) && !getenv("CLEORA_NO_HOT") && g->nnz > 0) {
+    if (g->tag_dp != dp && !getenv("CLEORA_NO_HOT") && g->nnz > 0) {
         // L2 residency hints: tag (bit 31 of col, in place) the columns whose rows are re-read
         // most (highest in-degree) so that their gathers use an evict_last policy, within a
         // budget of the 126 MB L2

@@ -28,10 +28,48 @@ namespace cleora {
 
 namespace {
 
+// L2 cache policies (createpolicy): hot rows (col bit 31, see hot_tag) stay resident
+// (evict_last), other gathers go first (evict_first) when hot rows exist, CSR words are streamed.
+struct Pol {
+    uint64_t hot, cold, csr;
+};
+
+__device__ __forceinline__ Pol make_pol(const SpmmArgs& a) {
+    Pol p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p.hot));
+    if (a.cold_first)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p.cold));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p.cold));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p.csr));
+    return p;
+}
+
+__device__ __forceinline__ float4 ldg4_pol(const float4* p, uint64_t pol) {
+    float4 x;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                 : "l"(p), "l"(pol));
+    return x;
+}
+
+__device__ __forceinline__ int32_t ldcsr_i32(const int32_t* p, uint64_t pol) {
+    int32_t x;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(x) : "l"(p), "l"(pol));
+    return x;
+}
+
+__device__ __forceinline__ float ldcsr_f32(const float* p, uint64_t pol) {
+    float x;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(x) : "l"(p), "l"(pol));
+    return x;
+}
+
 // acc[v] += sum_{k in [k0,k1)} val[k] * T_in[col[k]][cbase + 4*(lane + 32 v) .. +3], ascending k.
 template <int V>
 __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, int64_t k0, int64_t k1, int cbase, int lane,
                                                 float4 (&acc)[V]) {
+    const Pol pol = make_pol(a);
     constexpr int U = (16 / V > 8) ? 8 : 16 / V;  // neighbours per batch: U*V 16-byte loads in flight
     const int dp = a.dp;
     bool ok[V];
@@ -43,8 +81,8 @@ __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, int64_t k0, i
         int32_t mc = 0;
         float mw = 0.0f;
         if (lane < n) {
-            mc = __ldg(a.col + kb + lane) & kColMask;
-            mw = __ldg(a.val + kb + lane);
+            mc = ldcsr_i32(a.col + kb + lane, pol.csr);     // bit 31: hot row
+            mw = ldcsr_f32(a.val + kb + lane, pol.csr);
         }
         int j = 0;
         for (; j + U <= n; j += U) {
@@ -52,11 +90,12 @@ __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, int64_t k0, i
             float w[U];
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const int c = __shfl_sync(kFull, mc, j + u);
+                const int ct = __shfl_sync(kFull, mc, j + u);
                 w[u] = __shfl_sync(kFull, mw, j + u);
-                const float4* p = reinterpret_cast<const float4*>(tb + (int64_t)c * dp);
+                const uint64_t pl = ct < 0 ? pol.hot : pol.cold;
+                const float4* p = reinterpret_cast<const float4*>(tb + (int64_t)(ct & kColMask) * dp);
 #pragma unroll
-                for (int v = 0; v < V; v++) x[u][v] = ok[v] ? ldg4(p + 32 * v) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int v = 0; v < V; v++) x[u][v] = ok[v] ? ldg4_pol(p + 32 * v, pl) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
             for (int u = 0; u < U; u++)
@@ -64,12 +103,13 @@ __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, int64_t k0, i
                 for (int v = 0; v < V; v++) fma4(acc[v], w[u], x[u][v]);
         }
         for (; j < n; j++) {
-            const int c = __shfl_sync(kFull, mc, j);
+            const int ct = __shfl_sync(kFull, mc, j);
             const float w = __shfl_sync(kFull, mw, j);
-            const float4* p = reinterpret_cast<const float4*>(tb + (int64_t)c * dp);
+            const uint64_t pl = ct < 0 ? pol.hot : pol.cold;
+            const float4* p = reinterpret_cast<const float4*>(tb + (int64_t)(ct & kColMask) * dp);
 #pragma unroll
             for (int v = 0; v < V; v++)
-                if (ok[v]) fma4(acc[v], w, ldg4(p + 32 * v));
+                if (ok[v]) fma4(acc[v], w, ldg4_pol(p + 32 * v, pl));
         }
     }
 }

@@ -400,7 +400,14 @@ Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-bool tma_path_supported(int dp) { return dp <= 1024 && getenv("CLEORA_NO_TMA") == nullptr; }
+// TMA bulk gathers win for rows of >= 2 KB; below that the per-copy issue rate of the bulk-copy
+// engine binds (~6.7e9 copies/s on B200: c5 at d = 256 made 2.84e9 copies in 0.43 s with DRAM
+// 58% busy) and the register kernel's 16-byte LDGs are faster (measured, c4 at d = 64 / 128 /
+// 256: 5.7 / 6.4 / 8.3 ms vs 7.8 / 8.9 / 9.4 ms; equal at d = 512; TMA 2.78 vs 3.48 ms at 1024).
+bool tma_path_supported(int dp) {
+    if (dp > 1024 || getenv("CLEORA_NO_TMA")) return false;
+    return dp >= 512 || getenv("CLEORA_FORCE_TMA") != nullptr;
+}
 
 Status launch_spmm_tma(const SpmmArgs& a, cudaStream_t s) {
     if (a.dp == 1024) return launch_tma_v<8, true>(a, s);

@@ -240,7 +240,7 @@ def test_info_and_stats(cl):
     G.close()
 
 
-@pytest.mark.parametrize("d", [100, 256, 1024])
+@pytest.mark.parametrize("d", [100, 256, 600, 1024])
 def test_tma_and_register_kernels_bitwise_equal(cl, d, monkeypatch):
     """The TMA-gather kernel (spmm_tma.cu) and the register-gather kernel (spmm_norm.cu) run the
     same per-row arithmetic in the same order, so their outputs are bitwise identical."""
@@ -248,7 +248,10 @@ def test_tma_and_register_kernels_bitwise_equal(cl, d, monkeypatch):
     outs = []
     for no_tma in (False, True):
         if no_tma:
+            monkeypatch.delenv("CLEORA_FORCE_TMA", raising=False)
             monkeypatch.setenv("CLEORA_NO_TMA", "1")
+        else:
+            monkeypatch.setenv("CLEORA_FORCE_TMA", "1")    # TMA also below its default dp >= 512
         G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0)
         cl.cleora_init(G, d, 0)
         cl.cleora_iterate(G, 3)
