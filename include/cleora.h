@@ -113,6 +113,29 @@ CLEORA_API int cleora_build(const int32_t* src, const int32_t* dst, const float*
                  int32_t n_nodes, int32_t directed, const cleora_opts* opts, cleora_graph** out);
 
 /*
+ * cleora_expand -- hypergraph expansion on the device (§3.2 "Hypergraph
+ * Expansion"; the paper's timed workloads were expanded adjacency rows):
+ *   CLEORA_EXPAND_CLIQUE: hyperedge e with members m_0..m_{k-1} gives the edges (m_i, m_j) for
+ *     all i < j with m_i != m_j (reading R16), in the order (e, i, j);
+ *   CLEORA_EXPAND_STAR: hyperedge e gets the virtual node n_nodes + e and the edges
+ *     (n_nodes + e, m_i) for every listed member (reading R17), in the order (e, i); the expanded
+ *     graph has n_nodes + n_hyperedges nodes.
+ * Every edge carries its hyperedge's weight (or 1.0f).  The output is an undirected edge list for
+ * cleora_build (directed = 0).
+ *   he_ptr [n_hyperedges + 1] int64 (he_ptr[0] = 0, non-decreasing), he_nodes [he_ptr[n]] int32 in
+ *   [0, n_nodes), he_weight [n_hyperedges] or NULL; on_device = 1: all input AND output pointers
+ *   are device memory of `device` (-1: current), else host.  stream: cudaStream_t or NULL (per-thread
+ *   default stream).  out_src == NULL: count only.  *n_out receives the edge count.
+ *   Synchronous.  Errors: EUSAGE (NULL, bad mode / sizes, capacity < count, id range overflow),
+ *   EDATA (member id out of range, weight not finite or <= 0), EINTERNAL.
+ */
+enum { CLEORA_EXPAND_CLIQUE = 0, CLEORA_EXPAND_STAR = 1 };
+CLEORA_API int cleora_expand(const int64_t* he_ptr, const int32_t* he_nodes, const float* he_weight,
+                             int64_t n_hyperedges, int32_t n_nodes, int32_t mode, int32_t device, int32_t on_device,
+                             void* stream, int32_t* out_src, int32_t* out_dst, float* out_weight, int64_t capacity,
+                             int64_t* n_out);
+
+/*
  * cleora_build_batch -- many independent graphs in ONE handle (several M, e.g.
  * one per relation pair of a table -- "a separate embedding matrix for each relation pair",
  * in one launch per step).  The handle holds the block-diagonal M of

@@ -241,3 +241,34 @@ def reconstruct(new_idx, known_idx, w, n_new: int, T_src: np.ndarray) -> np.ndar
     M = build_csr(new_idx, known_idx, w, n, True)
     T_in = T_src if n == n_src else np.vstack([T_src, np.zeros((n - n_src, d), np.float32)])
     return step(M, T_in, 0, n_new)
+
+
+# ---------------------------------------------------------------- f3: hypergraph expansion
+
+def expand_clique(he_ptr, he_nodes, he_weight=None):
+    """Clique expansion ("each hyperedge is transformed into a clique"), reading R16:
+    hyperedge e with members m_0..m_{k-1} gives (m_i, m_j) for i < j, m_i != m_j, in the order
+    (e, i, j), each with the hyperedge's weight.  Plain loops: small inputs only."""
+    src, dst, w = [], [], []
+    for e in range(len(he_ptr) - 1):
+        m = [int(x) for x in he_nodes[he_ptr[e]:he_ptr[e + 1]]]
+        we = 1.0 if he_weight is None else float(he_weight[e])
+        for i in range(len(m)):
+            for j in range(i + 1, len(m)):
+                if m[i] != m[j]:
+                    src.append(m[i])
+                    dst.append(m[j])
+                    w.append(we)
+    return np.array(src, np.int32), np.array(dst, np.int32), np.array(w, np.float32)
+
+
+def expand_star(he_ptr, he_nodes, n_nodes: int, he_weight=None):
+    """Star expansion ("an extra node is introduced which links to the original
+    nodes contained by a hyperedge"), reading R17: hyperedge e gets node n_nodes + e and the edges
+    (n_nodes + e, m_i) for every listed member, in the order (e, i)."""
+    he_ptr = np.asarray(he_ptr, np.int64)
+    k = np.diff(he_ptr)
+    src = (n_nodes + np.repeat(np.arange(len(k), dtype=np.int64), k)).astype(np.int32)
+    dst = np.asarray(he_nodes, np.int32)[:he_ptr[-1]].copy()
+    w = np.ones(len(dst), np.float32) if he_weight is None else np.repeat(np.asarray(he_weight, np.float32), k)
+    return src, dst, w

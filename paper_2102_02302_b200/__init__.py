@@ -23,6 +23,7 @@ __all__ = [
     "cleora_sync", "cleora_destroy", "cleora_last_error", "cleora_fetch_csr", "cleora_set_rows", "cleora_fetch_replica",
     "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
     "cleora_release_cached_memory", "cleora_merge_chunks", "cleora_reconstruct", "cleora_build_batch",
+    "cleora_expand", "EXPAND_CLIQUE", "EXPAND_STAR",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcleora.so")
@@ -62,6 +63,8 @@ _vp, _i32, _i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
 _SIGS = {
     "cleora_build": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i32, _i32, ctypes.POINTER(_Opts), ctypes.POINTER(_vp)]),
     "cleora_init": (ctypes.c_int, [_vp, _i32, ctypes.c_uint64]),
+    "cleora_expand": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i64,
+                                     ctypes.POINTER(_i64)]),
     "cleora_build_batch": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, ctypes.POINTER(_Opts), ctypes.POINTER(_vp)]),
     "cleora_iterate": (ctypes.c_int, [_vp, _i32]),
     "cleora_fetch": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i32]),
@@ -197,6 +200,44 @@ def cleora_build(src, dst, weight, n_nodes: int, directed: bool = False, *, devi
     h = ctypes.c_void_p()
     _check(_lib.cleora_build(ps, pd, pw, n, int(n_nodes), 1 if directed else 0, ctypes.byref(o), ctypes.byref(h)))
     return Graph(h.value)
+
+
+EXPAND_CLIQUE, EXPAND_STAR = 0, 1
+
+
+def cleora_expand(he_ptr, he_nodes, n_nodes: int, mode: int, he_weight=None, *, device: int = -1, stream=None,
+                  with_weight: bool = False):
+    """Hypergraph -> undirected edge list on the device (clique or star expansion).
+    Host arrays in -> numpy (src, dst[, w]) out; CUDA tensors in -> CUDA tensors out."""
+    pp, dp_, kp = _ptr(he_ptr, np.int64)
+    pn, dn, kn = _ptr(he_nodes, np.int32)
+    pw, dw, kw = _ptr(he_weight, np.float32)
+    on_dev = dp_ or dn or dw
+    if on_dev and not (dp_ and dn and (kw is None or dw)):
+        raise CleoraError(EUSAGE, "inputs must be all on the host or all on the device")
+    n_he = int(kp.shape[0]) - 1
+    st = 0 if stream is None else (stream if isinstance(stream, int) else int(getattr(stream, "cuda_stream", stream)))
+    if on_dev and device < 0:
+        device = int(kp.device.index or 0)
+    n = ctypes.c_int64()
+    _check(_lib.cleora_expand(pp, pn, pw, n_he, int(n_nodes), int(mode), int(device), 1 if on_dev else 0, st,
+                              None, None, None, 0, ctypes.byref(n)))
+    m = int(n.value)
+    want_w = with_weight or he_weight is not None
+    if on_dev:
+        import torch
+        os_ = torch.empty(m, dtype=torch.int32, device=kp.device)
+        od_ = torch.empty(m, dtype=torch.int32, device=kp.device)
+        ow_ = torch.empty(m, dtype=torch.float32, device=kp.device) if want_w else None
+        ptrs = (os_.data_ptr(), od_.data_ptr(), ow_.data_ptr() if want_w else None)
+    else:
+        os_, od_ = np.empty(m, np.int32), np.empty(m, np.int32)
+        ow_ = np.empty(m, np.float32) if want_w else None
+        ptrs = (os_.ctypes.data, od_.ctypes.data, ow_.ctypes.data if want_w else None)
+    if m > 0:
+        _check(_lib.cleora_expand(pp, pn, pw, n_he, int(n_nodes), int(mode), int(device), 1 if on_dev else 0, st,
+                                  ptrs[0], ptrs[1], ptrs[2], m, ctypes.byref(n)))
+    return (os_, od_, ow_) if want_w else (os_, od_)
 
 
 def cleora_build_batch(src, dst, weight, edge_ptr, node_count, directed: bool = False, *, device: int = -1,

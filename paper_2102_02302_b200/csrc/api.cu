@@ -707,6 +707,90 @@ int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, in
     return CLEORA_OK;
 }
 
+int cleora_expand(const int64_t* he_ptr, const int32_t* he_nodes, const float* he_weight, int64_t n_hyperedges,
+                  int32_t n_nodes, int32_t mode, int32_t device, int32_t on_device, void* stream, int32_t* out_src,
+                  int32_t* out_dst, float* out_weight, int64_t capacity, int64_t* n_out) {
+    if (!he_ptr || !he_nodes || !n_out) return usage("cleora_expand: NULL argument");
+    if (n_hyperedges < 1 || n_nodes < 1) return usage("cleora_expand: n_hyperedges and n_nodes must be >= 1");
+    if (mode != CLEORA_EXPAND_CLIQUE && mode != CLEORA_EXPAND_STAR) return usage("cleora_expand: unknown mode");
+    if (mode == CLEORA_EXPAND_STAR && (int64_t)n_nodes + n_hyperedges > INT32_MAX)
+        return usage("cleora_expand: n_nodes + n_hyperedges exceeds the int32 id range");
+    if ((out_dst == nullptr) != (out_src == nullptr)) return usage("cleora_expand: out_src and out_dst go together");
+    *n_out = 0;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(Status::make(4, "cleora_expand: no CUDA device visible (libcleora has no CPU fallback)"));
+    }
+    DeviceGuard guard(device);
+    cudaStream_t s = stream ? (cudaStream_t)stream : cudaStreamPerThread;
+    int64_t n_members = 0;
+    const int64_t* dptr = he_ptr;
+    const int32_t* dnodes = he_nodes;
+    const float* dw = he_weight;
+    void *bp = nullptr, *bn = nullptr, *bw = nullptr;
+    void *os = nullptr, *od = nullptr, *ow = nullptr;
+    Status st = Status::ok();
+    if (on_device) {
+        cudaError_t e = cudaMemcpyAsync(&n_members, he_ptr + n_hyperedges, sizeof n_members, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_expand: ") + cudaGetErrorString(e)));
+    } else {
+        n_members = he_ptr[n_hyperedges];
+        if (he_ptr[0] != 0) return usage("cleora_expand: he_ptr[0] must be 0");
+        for (int64_t i = 0; i < n_hyperedges; i++)
+            if (he_ptr[i + 1] < he_ptr[i]) return usage("cleora_expand: he_ptr must be non-decreasing");
+        st = dalloc(&bp, (n_hyperedges + 1) * sizeof(int64_t), s, "expand he_ptr");
+        if (st.good()) st = dalloc(&bn, (n_members > 0 ? n_members : 1) * sizeof(int32_t), s, "expand members");
+        if (st.good() && he_weight) st = dalloc(&bw, n_hyperedges * sizeof(float), s, "expand weights");
+        if (st.good()) {
+            cudaMemcpyAsync(bp, he_ptr, (n_hyperedges + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+            if (n_members > 0) cudaMemcpyAsync(bn, he_nodes, n_members * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+            if (he_weight) cudaMemcpyAsync(bw, he_weight, n_hyperedges * sizeof(float), cudaMemcpyHostToDevice, s);
+            dptr = (const int64_t*)bp;
+            dnodes = (const int32_t*)bn;
+            dw = (const float*)bw;
+        }
+    }
+    if (st.good() && !on_device && out_src) {
+        // count first, then stage the outputs on the device
+        st = expand_hypergraph(dptr, dnodes, dw, n_hyperedges, n_members, n_nodes, mode, s, nullptr, nullptr, nullptr, 0,
+                               n_out);
+        if (st.good() && *n_out > capacity) st = Status::make(2, "cleora_expand: capacity smaller than the edge count");
+        if (st.good() && *n_out > 0) {
+            st = dalloc(&os, *n_out * sizeof(int32_t), s, "expand out src");
+            if (st.good()) st = dalloc(&od, *n_out * sizeof(int32_t), s, "expand out dst");
+            if (st.good() && out_weight) st = dalloc(&ow, *n_out * sizeof(float), s, "expand out weight");
+        }
+    }
+    if (st.good()) {
+        int32_t* ts = on_device ? out_src : (int32_t*)os;
+        int32_t* td = on_device ? out_dst : (int32_t*)od;
+        float* tw = on_device ? out_weight : (float*)ow;
+        if (out_src && (on_device || *n_out > 0))
+            st = expand_hypergraph(dptr, dnodes, dw, n_hyperedges, n_members, n_nodes, mode, s, ts, td, tw, capacity, n_out);
+        else if (!out_src)
+            st = expand_hypergraph(dptr, dnodes, dw, n_hyperedges, n_members, n_nodes, mode, s, nullptr, nullptr, nullptr,
+                                   0, n_out);
+    }
+    if (st.good() && !on_device && out_src && *n_out > 0) {
+        cudaMemcpyAsync(out_src, os, *n_out * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(out_dst, od, *n_out * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        if (out_weight) cudaMemcpyAsync(out_weight, ow, *n_out * sizeof(float), cudaMemcpyDeviceToHost, s);
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = Status::make(4, std::string("cleora_expand: ") + cudaGetErrorString(e));
+    }
+    cudaStreamSynchronize(s);
+    dfree(os, s);
+    dfree(od, s);
+    dfree(ow, s);
+    dfree(bp, s);
+    dfree(bn, s);
+    dfree(bw, s);
+    if (!st.good()) return fail(st);
+    return CLEORA_OK;
+}
+
 int cleora_build_batch(const int32_t* src, const int32_t* dst, const float* weight, const int64_t* edge_ptr,
                        const int32_t* node_count, int32_t n_graphs, int32_t directed, const cleora_opts* opts,
                        cleora_graph** out) {

@@ -152,6 +152,12 @@ Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_
 Status launch_merge(const float* const* d_Tq, const int32_t* const* d_occ, int Q, int64_t N, int dp, float* d_out,
                     cudaStream_t s);
 
+// expand.cu: hypergraph -> edge list (mode 0 clique, 1 star); all pointers device; d_os == NULL
+// counts only (*n_out); EUSAGE when capacity < *n_out
+Status expand_hypergraph(const int64_t* d_ptr, const int32_t* d_nodes, const float* d_w, int64_t n_he, int64_t n_members,
+                         int32_t n_nodes, int mode, cudaStream_t s, int32_t* d_os, int32_t* d_od, float* d_ow,
+                         int64_t capacity, int64_t* n_out);
+
 // init.cu
 Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s,
                         const int64_t* d_base = nullptr, int32_t n_graphs = 0);

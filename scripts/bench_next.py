@@ -6,6 +6,9 @@ f1 -- chunked embedding of c2 with Q chunks: per-chunk build + init + I iteratio
       achieved = bytes / (CUDA-event time of the merge call, device output, no D2H).
 f2 -- cleora_reconstruct of n_new unseen nodes against c2's T_{I-1}, device inputs and output:
       new nodes/s and nnz*d/s of the one fused SpMM step it runs.
+f3 -- the paper's pipeline for YouTube: every adjacency row of c2 (node v and its
+      neighbours, non-isolated nodes) as a hyperedge, star-expanded on the device, then build + init
+      + I iterations of the expanded graph (d = 1024); and c1's rows clique-expanded.
 f4 -- many small graphs (2,000 Erdos-Renyi graphs, N log-uniform in [50, 5000], 4N edges each,
       d = 128, I = 4): one batched handle (block-diagonal M, one launch per step) against the same
       graphs one handle at a time (a prefix of 200 graphs, scaled), device-resident inputs.
@@ -101,6 +104,53 @@ for _ in range(args.reps):
 rec_ms = min(ts)
 G.close()
 
+# ---------------------------------------------------------------- f3
+def rows_as_hyperedges(x):
+    Gx = cl.cleora_build(x.src, x.dst, None, x.n, x.directed, device=0)
+    csr = cl.cleora_fetch_csr(Gx)
+    Gx.close()
+    rp, col = csr["row_ptr"], csr["col"]
+    k = np.diff(rp)
+    live = np.flatnonzero(k > 0)
+    ptr = np.concatenate([[0], np.cumsum(k[live] + 1)]).astype(np.int64)
+    nodes = np.empty(ptr[-1], np.int32)
+    nodes[ptr[:-1]] = live                                   # the row's own node first
+    mask = np.ones(ptr[-1], bool)
+    mask[ptr[:-1]] = False
+    nodes[mask] = np.concatenate([col[rp[v]:rp[v + 1]] for v in live]) if live.size < 20000 else \
+        col[np.concatenate([np.arange(rp[v], rp[v + 1]) for v in live])]
+    return torch.from_numpy(ptr).to(dev), torch.from_numpy(nodes).to(dev), x.n
+
+
+f3 = {}
+for name, x, mode, d3 in (("c2_star", g, cl.EXPAND_STAR, 1024), ("c1_clique", gen.config("c1"), cl.EXPAND_CLIQUE, 128)):
+    hp, hn, n0 = rows_as_hyperedges(x)
+    es, ed = cl.cleora_expand(hp, hn, n0, mode, stream=s.cuda_stream)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(args.reps):
+        a, b = ev(), ev()
+        a.record(s)
+        es, ed = cl.cleora_expand(hp, hn, n0, mode, stream=s.cuda_stream)
+        b.record(s)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    nn = n0 + (hp.numel() - 1 if mode == cl.EXPAND_STAR else 0)
+    a, b = ev(), ev()
+    a.record(s)
+    es, ed = cl.cleora_expand(hp, hn, n0, mode, stream=s.cuda_stream)
+    G3 = cl.cleora_build(es, ed, None, nn, False, device=0, stream=s.cuda_stream)
+    cl.cleora_init(G3, d3, 0)
+    cl.cleora_iterate(G3, 4)
+    b.record(s)
+    b.synchronize()
+    nnz3 = cl.cleora_info(G3)["nnz"]
+    G3.close()
+    f3[name] = {"hyperedges": hp.numel() - 1, "members": int(hn.numel()), "expanded_edges": int(es.numel()),
+                "expanded_nodes": nn, "nnz": nnz3, "d": d3, "expand_ms": min(ts),
+                "expanded_edges_per_s": es.numel() / (min(ts) / 1e3),
+                "pipeline_ms": a.elapsed_time(b), "pipeline": "expand + build + init + 4 iterations"}
+
 # ---------------------------------------------------------------- f4
 rng = np.random.default_rng(1)
 ns = np.exp(rng.uniform(np.log(50), np.log(5000), 2000)).astype(np.int64)
@@ -152,7 +202,7 @@ b.record(s)
 b.synchronize()
 seq_ms = a.elapsed_time(b) * len(graphs) / len(gs)
 
-line = {"what": "SURVEY 8(f) f1 chunked embedding + merge, f2 inductive reconstruction, f4 batched graphs",
+line = {"what": "SURVEY 8(f) f1 chunked embedding + merge, f2 inductive reconstruction, f3 expansion, f4 batched graphs",
         "config": g.name, "d": d,
         "f1": {"chunks": Q, "nnz_all_chunks": nnz_chunks, "chunks_build_init_iterate_ms": chunks_ms,
                "merge_ms": merge_ms, "merge_bytes": merge_bytes,
@@ -161,6 +211,7 @@ line = {"what": "SURVEY 8(f) f1 chunked embedding + merge, f2 inductive reconstr
         "f2": {"new_nodes": args.new, "edges": int(k.sum()), "ms": rec_ms, "new_nodes_per_s": args.new / (rec_ms / 1e3),
                "nnz_d_per_s": int(k.sum()) * d / (rec_ms / 1e3),
                "includes": "device-side CSR build of the new nodes' rows + one fused SpMM step + D2D copy"},
+        "f3": f3,
         "f4": {"graphs": len(graphs), "nodes": info["n_nodes"], "nnz": nnz4, "d": d4, "iterations": it4,
                "batched_step_ms": batch_ms, "batched_graphs_per_s": len(graphs) / (batch_ms / 1e3),
                "batched_nnz_d_per_s": nnz4 * d4 * it4 / (batch_ms / 1e3),

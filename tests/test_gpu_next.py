@@ -1,4 +1,4 @@
-"""SURVEY §8(f) rows on the GPU, through the C ABI, against the oracle:
+"""SURVEY §8(f) rows on the GPU, through the C ABI, against the oracle (f4 batches: test_gpu_batch.py):
 
 f1 -- Algorithm 1 with Q chunks: every chunk handle's CSR bit-exact against the
       oracle's build of the same edge subset (reading R13), chunk embeddings within the bars, the
@@ -8,6 +8,8 @@ f1 -- Algorithm 1 with Q chunks: every chunk handle's CSR bit-
 f2 -- inductive embedding of new nodes: cleora_reconstruct against
       oracle.reconstruct on the GPU's own T_{I-1}; the training-consistency identity
       reconstruct(every node from its own edges, T_{I-1}) == T_I, bitwise on the GPU.
+f3 -- hypergraph clique / star expansion on the device: edge lists byte-identical to the oracle's
+      (readings R16/R17), host and device paths, and expand -> build -> embed within the bars.
 """
 import numpy as np
 import pytest
@@ -163,3 +165,49 @@ def test_reconstruct_new_nodes(cl, d):
         assert e.value.code == cl.EDATA
     finally:
         G.close()
+
+
+# ---------------------------------------------------------------- f3
+
+def _hyper(seed, n=3000, n_he=2000, kmax=40):
+    rng = np.random.default_rng(seed)
+    k = rng.integers(1, kmax + 1, n_he)
+    k[::97] = 300                                                      # some wide hyperedges
+    ptr = np.concatenate([[0], np.cumsum(k)]).astype(np.int64)
+    nodes = rng.integers(0, n, ptr[-1]).astype(np.int32)
+    return ptr, nodes, rng.lognormal(0, 1, n_he).astype(np.float32), n
+
+
+def test_expansion_bit_exact_and_embedding(cl):
+    import torch
+    for seed in range(3):
+        ptr, nodes, w, n = _hyper(seed)
+        for mode, ref in ((cl.EXPAND_CLIQUE, oracle.expand_clique(ptr, nodes, w)),
+                          (cl.EXPAND_STAR, oracle.expand_star(ptr, nodes, n, w))):
+            got = cl.cleora_expand(ptr, nodes, n, mode, w)
+            for a, b in zip(got, ref):
+                assert a.tobytes() == b.tobytes(), f"seed {seed} mode {mode}"
+            # device in -> device out, same bytes
+            dgot = cl.cleora_expand(torch.from_numpy(ptr).cuda(), torch.from_numpy(nodes).cuda(), n, mode,
+                                    torch.from_numpy(w).cuda())
+            for a, b in zip(dgot, ref):
+                assert a.cpu().numpy().tobytes() == b.tobytes()
+            # end to end: expand -> build -> embed, against the oracle on the oracle's expansion
+            nn = n if mode == cl.EXPAND_CLIQUE else n + len(ptr) - 1
+            G = cl.cleora_build(dgot[0], dgot[1], dgot[2], nn, False)
+            cl.cleora_init(G, 64, 1)
+            cl.cleora_iterate(G, 3)
+            T = cl.cleora_fetch(G)
+            G.close()
+            R = oracle.embed(oracle.build_csr(ref[0], ref[1], ref[2], nn, False), 64, 1, 3)
+            close(T, R, f"expanded seed {seed} mode {mode}")
+
+
+def test_expansion_errors(cl):
+    ptr = np.array([0, 2], np.int64)
+    with pytest.raises(cl.CleoraError) as e:
+        cl.cleora_expand(ptr, np.array([0, 5], np.int32), 5, cl.EXPAND_CLIQUE)
+    assert e.value.code == cl.EDATA and "member 1" in str(e.value)
+    with pytest.raises(cl.CleoraError) as e:
+        cl.cleora_expand(ptr, np.array([0, 1], np.int32), 5, cl.EXPAND_STAR, np.array([-1.0], np.float32))
+    assert e.value.code == cl.EDATA

@@ -166,3 +166,54 @@ def test_reconstruct_closed_forms():
     assert abs(np.linalg.norm(R[1]) - 1) < 1e-6
     R2 = oracle.reconstruct(np.array([1, 1, 1], np.int32), np.array([4, 0, 2], np.int32), None, 3, T)
     assert R.tobytes() == R2.tobytes()
+
+
+# ---------------------------------------------------------------- f3: hypergraph expansion
+
+def _random_hypergraph(seed, n=40, n_he=30, kmax=7):
+    rng = np.random.default_rng(seed)
+    k = rng.integers(1, kmax + 1, n_he)
+    ptr = np.concatenate([[0], np.cumsum(k)]).astype(np.int64)
+    nodes = rng.integers(0, n, ptr[-1]).astype(np.int32)          # duplicates inside a hyperedge happen
+    return ptr, nodes, rng.lognormal(0, 1, n_he).astype(np.float32)
+
+
+def test_expansion_spec_examples():
+    # SPEC.md:136 star {c,p,s} -> virtual h, edges (h,c),(h,p),(h,s); width 1 -> one edge
+    s, d, w = oracle.expand_star([0, 3, 4], [5, 6, 7, 2], 10)
+    assert list(zip(s.tolist(), d.tolist())) == [(10, 5), (10, 6), (10, 7), (11, 2)]
+    # 1000 hyperedges of width 4 -> 1000 virtual nodes, 4000 edges
+    ptr = np.arange(0, 4001, 4)
+    s, d, _ = oracle.expand_star(ptr, np.arange(4000) % 97, 97)
+    assert s.size == 4000 and np.unique(s).size == 1000 and s.min() == 97
+    # clique of {u,v,w} -> (u,v),(u,w),(v,w); width 2 is the identity; no self-loops
+    s, d, _ = oracle.expand_clique([0, 3], [1, 2, 3])
+    assert list(zip(s.tolist(), d.tolist())) == [(1, 2), (1, 3), (2, 3)]
+    s, d, _ = oracle.expand_clique([0, 2], [4, 9])
+    assert list(zip(s.tolist(), d.tolist())) == [(4, 9)]
+    s, d, _ = oracle.expand_clique([0, 3], [4, 4, 9])
+    assert list(zip(s.tolist(), d.tolist())) == [(4, 9), (4, 9)]
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_expansion_counts_against_incidence_algebra(seed):
+    """Clique: the unordered pair {u,v} (u != v) appears sum_e mult_e(u) mult_e(v) times, i.e. the
+    off-diagonal of H^T H for the hyperedge-node multiplicity matrix H.  Star: the
+    graph is bipartite original/virtual and node v is joined to hyperedge e mult_e(v) times."""
+    ptr, nodes, w = _random_hypergraph(seed)
+    n, n_he = 40, len(ptr) - 1
+    H = np.zeros((n_he, n), np.int64)
+    for e in range(n_he):
+        np.add.at(H[e], nodes[ptr[e]:ptr[e + 1]], 1)
+    s, d, ww = oracle.expand_clique(ptr, nodes, w)
+    C = np.zeros((n, n), np.int64)
+    np.add.at(C, (np.minimum(s, d), np.maximum(s, d)), 1)
+    G = H.T @ H
+    assert np.array_equal(C, np.triu(G, 1))
+    assert not (s == d).any()
+    s, d, ww = oracle.expand_star(ptr, nodes, n, w)
+    assert (s >= n).all() and (d < n).all()                         # bipartite
+    S = np.zeros((n_he, n), np.int64)
+    np.add.at(S, (s - n, d), 1)
+    assert np.array_equal(S, H)
+    assert np.array_equal(ww, np.repeat(w, np.diff(ptr)))
