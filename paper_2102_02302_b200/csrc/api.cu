@@ -261,12 +261,9 @@ static Nccl& nccl() {
             return Status::make(4, std::string(#expr) + ": " + nccl().GetErrorString(_r));       \
     } while (0)
 
-static int heavy_thresh_default() {
+static int heavy_thresh_default(int dflt) {
     const char* e = getenv("CLEORA_HEAVY_THRESH");
-    // 256: rows up to 256 entries stream on the warp path (measured: c5 427 -> 375 ms per step,
-    // c2 / c4 unchanged vs 64); every sequential fp32 run stays <= 256 terms (SURVEY §0.4:
-    // 256-entry blocks keep the error ~3e-7)
-    int v = e ? atoi(e) : 256;
+    int v = e ? atoi(e) : dflt;
     if (v < 8) v = 8;
     if (v > 4096) v = 4096;
     return v;
@@ -317,6 +314,8 @@ struct cleora_graph {
     std::vector<std::array<float*, 2>> rep;
     std::vector<Schedule> sched_p;
     int64_t max_items = 0;
+    int sched_thresh = -1;          // heavy_thresh the current schedule(s) were built with
+    size_t partials_floats = 0;     // capacity of `partials`
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_spmm, ev_x;
     std::vector<cudaEvent_t> ev_pool;
@@ -403,6 +402,43 @@ void close_peers(cleora_graph* g) {
             }
 }
 
+void free_schedules(cleora_graph* g) {
+    auto drop = [g](Schedule& sc) {
+        dfree(sc.items, g->stream);
+        dfree(sc.counters, g->stream);
+        dfree(sc.work, g->stream);
+        dfree(sc.light_start, g->stream);
+        sc = Schedule();
+    };
+    if (g->sched_p.empty()) {
+        drop(g->sched);
+    } else {
+        for (auto& sc : g->sched_p) drop(sc);   // g->sched aliases sched_p[rank]
+        g->sched = Schedule();
+    }
+    g->max_items = 0;
+    g->sched_thresh = -1;
+}
+
+// The schedule (heavy-row CTA items, light chunks) for this handle's rows -- for every emulated
+// rank in loopback -- with the current heavy_thresh.
+Status make_schedules(cleora_graph* g) {
+    free_schedules(g);
+    if (!g->sched_p.empty()) {
+        for (int p = 0; p < g->world; p++) {
+            CL_TRY(build_schedule(g->row_ptr, g->n, g->cuts[p], g->cuts[p + 1], g->heavy_thresh, g->stream,
+                                  &g->sched_p[p]));
+            g->max_items = std::max(g->max_items, g->sched_p[p].n_items);
+        }
+        g->sched = g->sched_p[g->rank];
+    } else {
+        CL_TRY(build_schedule(g->row_ptr, g->n, g->r0, g->r1, g->heavy_thresh, g->stream, &g->sched));
+        g->max_items = g->sched.n_items;
+    }
+    g->sched_thresh = g->heavy_thresh;
+    return Status::ok();
+}
+
 void free_T(cleora_graph* g) {
     close_peers(g);
     for (size_t p = 0; p < g->rep.size(); p++)
@@ -415,6 +451,7 @@ void free_T(cleora_graph* g) {
     }
     dfree(g->partials, g->stream);
     g->partials = nullptr;
+    g->partials_floats = 0;
     g->zclean[0] = g->zclean[1] = false;
 }
 
@@ -540,7 +577,7 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
     g->n = N;
     g->n_edges_in = E;
     g->directed = directed;
-    g->heavy_thresh = heavy_thresh_default();
+    g->heavy_thresh = heavy_thresh_default(64);   // set per kernel by cleora_init
     g->rank = (o && o->world > 1) ? o->rank : 0;
     g->world = (o && o->world > 1) ? o->world : 1;
 
@@ -632,22 +669,11 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
     g->r1 = g->cuts[g->rank + 1];
     const bool loopback = g->world > 1 && o && (o->flags & CLEORA_F_LOOPBACK);
     if (loopback) {
-        // every rank's schedule lives here; g->sched aliases this rank's
-        g->sched_p.resize(g->world);
-        for (int p = 0; p < g->world; p++) {
-            CL_TRY(build_schedule(g->row_ptr, N, g->cuts[p], g->cuts[p + 1], g->heavy_thresh, g->stream,
-                                  &g->sched_p[p]));
-            g->max_items = std::max(g->max_items, g->sched_p[p].n_items);
-        }
-        g->sched = g->sched_p[g->rank];
+        g->sched_p.resize(g->world);        // every rank's schedule lives here (built by init)
         g->rep.assign(g->world, {nullptr, nullptr});
         g->xmode = X_LOOPBACK;
-    } else {
-        CL_TRY(build_schedule(g->row_ptr, N, g->r0, g->r1, g->heavy_thresh, g->stream, &g->sched));
-        g->max_items = g->sched.n_items;
     }
-    trace("build: schedule", g->stream, true);
-    g->bytes += g->sched.n_items * (int64_t)sizeof(HeavyItem) + g->sched.n_heavy_rows * 4;
+    // the iteration schedule depends on the kernel, i.e. on d: cleora_init builds it
 
     if (g->world > 1 && !loopback) {
         g->xmode = (o->flags & CLEORA_F_EXCHANGE_NCCL) ? X_NCCL : X_PEER;
@@ -837,14 +863,6 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
                 return fail(s);
             }
         }
-        if (g->max_items > 0) {
-            Status s = dalloc((void**)&g->partials, (size_t)g->max_items * dp * sizeof(float), g->stream,
-                              "heavy-row partials");
-            if (!s.good()) {
-                free_T(g);
-                return fail(s);
-            }
-        }
         if (g->xmode == X_LOOPBACK) {
             g->rep[g->rank] = {g->T[0], g->T[1]};
             for (int p = 0; p < g->world; p++) {
@@ -871,6 +889,23 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     g->cur = 0;
     g->iters = 0;
     g->zclean[0] = g->zclean[1] = false;
+    // heavy rows: > 64 entries on the TMA kernel, > 256 on the register kernel (measured: c2 12.68 vs
+    // 12.80 ms per step with 64 / 256; c5 427 -> 375 ms with 256); every sequential fp32 run stays
+    // <= 256 terms (256-entry blocks keep the error ~3e-7)
+    g->heavy_thresh = heavy_thresh_default(tma_path_supported(dp) ? 64 : 256);
+    if (g->sched_thresh != g->heavy_thresh) {
+        Status s = make_schedules(g);
+        if (!s.good()) return fail(s);
+    }
+    if (g->max_items > 0 && g->partials_floats < (size_t)g->max_items * dp) {
+        dfree(g->partials, g->stream);
+        g->partials = nullptr;
+        g->partials_floats = 0;
+        Status s = dalloc((void**)&g->partials, (size_t)g->max_items * dp * sizeof(float), g->stream,
+                          "heavy-row partials");
+        if (!s.good()) return fail(s);
+        g->partials_floats = (size_t)g->max_items * dp;
+    }
     if (g->tag_dp != dp && !getenv("CLEORA_NO_HOT") && g->nnz > 0) {
         // L2 residency hints: tag (bit 31 of col, in place) the columns whose rows are re-read
         // most (highest in-degree) so that their gathers use an evict_last policy, within a
@@ -1226,8 +1261,9 @@ int cleora_info(const cleora_graph* g, cleora_info_t* o) {
     o->n_graphs = g->n_graphs;
     o->referenced_rows = g->n_ref;
     o->exchange = g->xmode;
-    o->device_bytes = g->bytes + (g->T[0] ? 2 * (int64_t)g->n * g->dp * 4 : 0) +
-                      (g->partials ? g->sched.n_items * (int64_t)g->dp * 4 : 0);
+    o->device_bytes = g->bytes + (g->T[0] ? 2 * (int64_t)g->n * g->dp * 4 : 0) + (int64_t)g->partials_floats * 4 +
+                      g->sched.n_items * (int64_t)sizeof(HeavyItem) + g->sched.n_heavy_rows * 4 +
+                      (g->sched.n_light + 1) * 8;
     DeviceGuard guard(g->device);
     cudaError_t e = cudaStreamSynchronize(g->stream);
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_info: ") + cudaGetErrorString(e)));
@@ -1271,18 +1307,7 @@ void cleora_destroy(cleora_graph* g) {
         dfree(g->col, g->stream);
         dfree(g->val, g->stream);
         dfree(g->deg, g->stream);
-        if (g->sched_p.empty()) {
-            dfree(g->sched.items, g->stream);
-            dfree(g->sched.counters, g->stream);
-            dfree(g->sched.work, g->stream);
-            dfree(g->sched.light_start, g->stream);
-        }
-        for (auto& sc : g->sched_p) {      // loopback: g->sched aliases sched_p[rank]
-            dfree(sc.items, g->stream);
-            dfree(sc.counters, g->stream);
-            dfree(sc.work, g->stream);
-            dfree(sc.light_start, g->stream);
-        }
+        free_schedules(g);
         dfree(g->d_flag, g->stream);
         dfree(g->occ, g->stream);
         dfree(g->d_base, g->stream);

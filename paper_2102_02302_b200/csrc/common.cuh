@@ -65,6 +65,7 @@ static_assert(sizeof(HeavyItem) == 32, "HeavyItem layout");
 
 constexpr int kWarpsPerCta = 8;     // 256 threads
 constexpr int kMaxPeers = 7;        // other replicas a launch writes into (8 GPUs per box)
+constexpr int kMaxDevices = 64;     // per-device launch configuration tables
 constexpr int kMaxV = 8;            // float4 per lane per column slice (slice = 1024 floats)
 
 struct SpmmArgs {

@@ -21,6 +21,8 @@
 //     sequential fp32 summation to <= heavy_thresh terms (the precision requirement of
 //     SURVEY.md §0.4 / DESIGN.md §Precision).
 //   Rows whose product is the zero vector (no out-edges) are written as zeros (reading RZ).
+#include <mutex>
+
 #include "common.cuh"
 #include "spmm_common.cuh"
 
@@ -298,15 +300,24 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_norm(const SpmmAr
 template <int V>
 Status launch_v(const SpmmArgs& a, cudaStream_t s) {
     const size_t smem = (size_t)kWarpsPerCta * 32 * V * sizeof(float4);
-    static int blocks_per_sm = 0, sms = 0;
-    if (!blocks_per_sm) {
-        CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_norm<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int dev = 0;
-        CL_CUDA_TRY(cudaGetDevice(&dev));
-        CL_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm_norm<V>,
-                                                                  kWarpsPerCta * 32, smem));
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    // per device: the smem attribute and the occupancy are per device
+    static int bps[kMaxDevices], nsm[kMaxDevices];
+    static std::mutex mu;
+    int dev = 0;
+    CL_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev >= kMaxDevices) return Status::make(4, "k_spmm_norm: device ordinal beyond kMaxDevices");
+    int blocks_per_sm = 0, sms = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!bps[dev]) {
+            CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_norm<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CL_CUDA_TRY(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
+            int b = 0;
+            CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmm_norm<V>, kWarpsPerCta * 32, smem));
+            bps[dev] = b < 1 ? 1 : b;
+        }
+        blocks_per_sm = bps[dev];
+        sms = nsm[dev];
     }
     if (a.r1 <= a.r0 && a.n_items == 0) return Status::ok();
     const int grid = sms * blocks_per_sm;                // one persistent wave

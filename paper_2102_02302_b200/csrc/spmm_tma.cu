@@ -18,6 +18,7 @@
 // Each row accumulates its entries in ascending order from 0, exactly as spmm_norm.cu does, so
 // both kernels produce bitwise identical results.
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "spmm_common.cuh"
@@ -367,29 +368,38 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
 struct TmaCfg {
     int blocks_per_sm = 0, sms = 0, S = 0;
     size_t smem = 0;
+    int dp = -1;
 };
 
+// Launch configuration per device (the smem attribute is per device) and row stride.
 template <int V, bool FULL>
 Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
-    static TmaCfg cfg[2];   // [0]: default, keyed by dp below
-    static int cfg_dp = -1;
-    TmaCfg& c = cfg[0];
-    if (cfg_dp != a.dp) {
-        const int slot = a.dp * 4;
-        // per-CTA ring budget ~96 KB so that two CTAs (16 warps) share an SM
-        int S = (96 * 1024) / (kWarpsPerCta * slot);
-        if (S > 16) S = 16;
-        if (S < 2) S = 2;
-        c.S = S;
-        c.smem = (size_t)kWarpsPerCta * S * slot + (size_t)kWarpsPerCta * S * sizeof(uint64_t);
-        CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_tma<V, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
-        int dev = 0;
-        CL_CUDA_TRY(cudaGetDevice(&dev));
-        CL_CUDA_TRY(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
-        CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.blocks_per_sm, k_spmm_tma<V, FULL>,
-                                                                  kWarpsPerCta * 32, c.smem));
-        if (c.blocks_per_sm < 1) c.blocks_per_sm = 1;
-        cfg_dp = a.dp;
+    static TmaCfg cfg[kMaxDevices];
+    static std::mutex mu;
+    int dev = 0;
+    CL_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev >= kMaxDevices) return Status::make(4, "k_spmm_tma: device ordinal beyond kMaxDevices");
+    TmaCfg c;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        TmaCfg& cc = cfg[dev];
+        if (cc.dp != a.dp) {
+            const int slot = a.dp * 4;
+            // per-CTA ring budget ~96 KB so that two CTAs (16 warps) share an SM
+            int S = (96 * 1024) / (kWarpsPerCta * slot);
+            if (S > 16) S = 16;
+            if (S < 2) S = 2;
+            cc.S = S;
+            cc.smem = (size_t)kWarpsPerCta * S * slot + (size_t)kWarpsPerCta * S * sizeof(uint64_t);
+            CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_tma<V, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)cc.smem));
+            CL_CUDA_TRY(cudaDeviceGetAttribute(&cc.sms, cudaDevAttrMultiProcessorCount, dev));
+            CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cc.blocks_per_sm, k_spmm_tma<V, FULL>,
+                                                                      kWarpsPerCta * 32, cc.smem));
+            if (cc.blocks_per_sm < 1) cc.blocks_per_sm = 1;
+            cc.dp = a.dp;
+        }
+        c = cc;
     }
     if (a.r1 <= a.r0 && a.n_items == 0) return Status::ok();
     k_spmm_tma<V, FULL><<<c.sms * c.blocks_per_sm, kWarpsPerCta * 32, c.smem, s>>>(a, c.S);

@@ -233,6 +233,9 @@ def test_info_and_stats(cl):
     deg = np.bincount(np.concatenate([g.src, g.dst]), minlength=g.n)
     assert info["zero_rows"] == int((deg == 0).sum()) and info["max_degree"] == int(deg.max())
     cl.cleora_init(G, 128, 0)
+    assert cl.cleora_info(G)["heavy_rows"] == int((deg > 256).sum())    # register kernel: > 256 entries
+    cl.cleora_init(G, 1024, 0)
+    assert cl.cleora_info(G)["heavy_rows"] == int((deg > 64).sum())     # TMA kernel: > 64 entries
     cl.cleora_iterate(G, 3)
     st = cl.cleora_stats(G, reset=True)
     assert st["spmm_launches"] == 3 and st["spmm_ms_total"] > 0
@@ -245,6 +248,7 @@ def test_tma_and_register_kernels_bitwise_equal(cl, d, monkeypatch):
     """The TMA-gather kernel (spmm_tma.cu) and the register-gather kernel (spmm_norm.cu) run the
     same per-row arithmetic in the same order, so their outputs are bitwise identical."""
     g = gen.chung_lu(30000, 90000, 2.1, 9.5388, 233115.5 * 30000 / 1134890, seed=3)
+    monkeypatch.setenv("CLEORA_HEAVY_THRESH", "64")       # the same schedule for both kernels
     outs = []
     for no_tma in (False, True):
         if no_tma:
