@@ -983,6 +983,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
                 for (int q = 0; q < g->world - 1; q++) a.peer_out[a.n_peers++] = g->peer_T[out][q];
             }
             a.skip_zero_rows = (g->zclean[out] && !getenv("CLEORA_WRITE_ZERO_ROWS")) ? 1 : 0;
+            a.csr_prefetch = getenv("CLEORA_CSR_PREFETCH") ? atoi(getenv("CLEORA_CSR_PREFETCH")) : 1;
             Status s = launch_spmm_norm(a, g->stream);
             if (!s.good()) return fail(s);
         }
@@ -1155,6 +1156,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
         a.n_peers = 0;
         for (int q = 0; q < kMaxPeers; q++) a.peer_out[q] = nullptr;
         a.skip_zero_rows = 0;
+        a.csr_prefetch = 0;
         st = launch_spmm_norm(a, s);
     }
     if (st.good()) {

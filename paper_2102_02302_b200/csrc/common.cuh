@@ -92,6 +92,7 @@ struct SpmmArgs {
     float* peer_out[kMaxPeers];
     // Rows without entries are already 0 in T_out (written by an earlier iteration): skip them.
     int32_t skip_zero_rows;
+    int32_t csr_prefetch;   // register kernel: L1-prefetch each light chunk's CSR words
 };
 
 // Store float4 f of row `row` of the iteration's output into T_out and every peer replica.

@@ -83,8 +83,13 @@ __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, int64_t k0, i
         int32_t mc = 0;
         float mw = 0.0f;
         if (lane < n) {
-            mc = ldcsr_i32(a.col + kb + lane, pol.csr);     // bit 31: hot row
-            mw = ldcsr_f32(a.val + kb + lane, pol.csr);
+            if (a.csr_prefetch) {                           // prefetched into L1 by the chunk
+                mc = __ldg(a.col + kb + lane);              // bit 31: hot row
+                mw = __ldg(a.val + kb + lane);
+            } else {
+                mc = ldcsr_i32(a.col + kb + lane, pol.csr);
+                mw = ldcsr_f32(a.val + kb + lane, pol.csr);
+            }
         }
         int j = 0;
         for (; j + U <= n; j += U) {
@@ -253,8 +258,13 @@ __device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* 
 // the counters are 0 again at the next launch.  Which warp computes a row never changes its
 // arithmetic, so results stay bitwise deterministic.
 
+// rows of <= 512 bytes (V = 1) are latency-bound with one row at a time per warp: 4 CTAs (32 warps)
+// per SM at <= 64 registers; wider rows need the registers for their accumulators (2 CTAs)
 template <int V>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_norm(const SpmmArgs a) {
+constexpr int kNormMinBlocks = V == 1 ? 4 : 2;   // V = 2 at 3 CTAs spills: c5 357 -> 478 ms
+
+template <int V>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_norm(const SpmmArgs a) {
     extern __shared__ float4 red[];
     __shared__ double scratch[kWarpsPerCta];
     __shared__ int flag;
@@ -279,6 +289,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_norm(const SpmmAr
         const int64_t rb = a.light_start[c];
         const int64_t re = a.light_start[c + 1];
         const int64_t rpl = (lane <= re - rb) ? a.row_ptr[rb + lane] : 0;
+        if (a.csr_prefetch) {
+            // bring the chunk's CSR words into L1 up front, so each row's col/val load is an L1 hit
+            // instead of one more dependent memory round trip per (short) row
+            const int64_t eb = __shfl_sync(kFull, rpl, 0), ee = __shfl_sync(kFull, rpl, (int)(re - rb));
+            if (ee - eb <= 4096)
+                for (int64_t off = (eb & ~31ll) + 32 * lane; off < ee; off += 32 * 32) {
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.col + off));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.val + off));
+                }
+        }
         for (int64_t r = rb; r < re; r++) {
             const int64_t k0 = __shfl_sync(kFull, rpl, (int)(r - rb));
             const int64_t k1 = __shfl_sync(kFull, rpl, (int)(r - rb + 1));
@@ -286,6 +306,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_norm(const SpmmAr
             light_row<V>(a, r, k0, k1, lane);
         }
     }
+    // peer stores (multi-GPU) are system-scope visible before this launch counts as done; the
+    // rank barrier that follows on the stream then publishes them to the other ranks
+    if (a.n_peers > 0) __threadfence_system();
     if (lane == 0) {
         __threadfence();
         const unsigned done = atomicAdd(a.work + 2, 1u);

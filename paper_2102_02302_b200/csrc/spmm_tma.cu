@@ -354,6 +354,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
             row = z;
         }
     }
+    // peer stores (multi-GPU) are system-scope visible before this launch counts as done; the
+    // rank barrier that follows on the stream then publishes them to the other ranks
+    if (a.n_peers > 0) __threadfence_system();
     if (lane == 0) {
         __threadfence();
         const unsigned done = atomicAdd(a.work + 2, 1u);
