@@ -222,13 +222,13 @@ struct IsHeavy {
     __host__ __device__ bool operator()(int64_t r) const { return rp[r + 1] - rp[r] > thresh; }
 };
 
-// r starts a light chunk: the first row, every kChunkRows-th row, or the first row whose entries
+// r starts a light chunk: the first row, every `rows`-th row (<= kChunkRows), or the first row whose entries
 // begin in a new window of `win` entries (counted from the shard's first entry)
 struct IsChunkStart {
     const int64_t* rp;
-    int64_t r0, win;
+    int64_t r0, win, rows;
     __host__ __device__ bool operator()(int64_t r) const {
-        if (r == r0 || (r - r0) % kChunkRows == 0) return true;
+        if (r == r0 || (r - r0) % rows == 0) return true;
         return (rp[r] - rp[r0]) / win != (rp[r - 1] - rp[r0]) / win;
     }
 };
@@ -458,7 +458,16 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         CL_TRY(starts.alloc(nr + 1, s, "light chunk starts"));
         CL_TRY(cnt1.alloc(1, s, "scalars"));
         thrust::counting_iterator<int64_t> it(r0);
-        IsChunkStart pred{d_row_ptr, r0, win};
+        // small graphs: fewer rows per chunk, so that every warp of the persistent grid gets work
+        // (c1, 10k rows: 31-row chunks left most of the 2,368 warps idle and one warp walked 31
+        // short rows one after another); ~4 chunks per warp of a 148-SM grid at 16 warps per SM
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int64_t rows = nr / ((int64_t)sms * 16 * 4);
+        if (rows < 1) rows = 1;
+        if (rows > kChunkRows) rows = kChunkRows;
+        IsChunkStart pred{d_row_ptr, r0, win, rows};
         size_t tmp_bytes = 0;
         CL_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, it, starts.p, cnt1.p, nr, pred, s));
         DevBuf<uint8_t> tmp;
