@@ -224,6 +224,17 @@ CLEORA_API int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx,
                                   const float* weight, int64_t n_edges, int32_t n_new, int32_t inputs_on_device,
                                   float* out, int32_t out_on_device);
 
+/*
+ * cleora_fetch_async -- as cleora_fetch, but only enqueued: the copy runs on a library-owned copy
+ * stream once the work enqueued so far on the handle's stream is done, concurrently with whatever
+ * is enqueued afterwards (e.g. the next graph's build and iterations), so PCIe transfers overlap
+ * compute.  `out` must stay valid until cleora_sync(g) or cleora_destroy(g), which wait for it;
+ * later cleora_init / cleora_iterate / cleora_set_rows on g are stream-ordered after the copy.
+ *   Errors: as cleora_fetch (checked at enqueue time); a copy failure is reported by cleora_sync.
+ */
+CLEORA_API int cleora_fetch_async(cleora_graph* g, int64_t row_begin, int64_t row_end, float* out,
+                                  int32_t out_on_device);
+
 /* Facts about a handle (all sizes in elements). */
 typedef struct cleora_info_t {
     int64_t n_nodes;        /* N                                                        */
@@ -257,7 +268,7 @@ typedef struct cleora_stats_t {
 } cleora_stats_t;
 CLEORA_API int cleora_stats(cleora_graph* g, cleora_stats_t* out, int32_t reset);
 
-/* Wait for all work enqueued on the handle's stream. */
+/* Wait for all work enqueued on the handle's stream and for its asynchronous fetches. */
 CLEORA_API int cleora_sync(const cleora_graph* g);
 
 /* Release everything the handle owns.  Safe on NULL. */

@@ -21,6 +21,7 @@ __all__ = [
     "CleoraError", "Graph", "LIB_PATH",
     "cleora_build", "cleora_init", "cleora_iterate", "cleora_fetch", "cleora_info", "cleora_stats",
     "cleora_sync", "cleora_destroy", "cleora_last_error", "cleora_fetch_csr", "cleora_set_rows", "cleora_fetch_replica",
+    "cleora_fetch_async",
     "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
     "cleora_release_cached_memory", "cleora_merge_chunks", "cleora_reconstruct", "cleora_build_batch",
     "cleora_expand", "EXPAND_CLIQUE", "EXPAND_STAR",
@@ -68,6 +69,7 @@ _SIGS = {
     "cleora_build_batch": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, ctypes.POINTER(_Opts), ctypes.POINTER(_vp)]),
     "cleora_iterate": (ctypes.c_int, [_vp, _i32]),
     "cleora_fetch": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i32]),
+    "cleora_fetch_async": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i32]),
     "cleora_info": (ctypes.c_int, [_vp, ctypes.POINTER(_Info)]),
     "cleora_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_Stats), _i32]),
     "cleora_sync": (ctypes.c_int, [_vp]),
@@ -294,6 +296,17 @@ def cleora_fetch(g: Graph, row_begin: int = 0, row_end: int | None = None, out=N
     if keep is not out:
         raise CleoraError(EUSAGE, "out must be a contiguous fp32 array")
     _check(_lib.cleora_fetch(g.handle, int(row_begin), int(row_end), p, 1 if on_dev else 0))
+    return out
+
+
+def cleora_fetch_async(g: Graph, row_begin: int, row_end: int, out):
+    """Enqueue the copy of rows [row_begin, row_end) into `out` (a preallocated pinned host or CUDA
+    tensor / array) on the library's copy stream; returns at once.  Keep `out` alive until
+    cleora_sync(g) or g.close()."""
+    p, on_dev, keep = _ptr(out, np.float32)
+    if keep is not out:
+        raise CleoraError(EUSAGE, "out must be a contiguous fp32 array")
+    _check(_lib.cleora_fetch_async(g.handle, int(row_begin), int(row_end), p, 1 if on_dev else 0))
     return out
 
 

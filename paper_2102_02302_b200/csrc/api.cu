@@ -39,6 +39,40 @@ void trace(const char* what, cudaStream_t s, bool sync) {
     last = now;
 }
 
+// ---------------------------------------------------------------- small readbacks
+namespace {
+__global__ void k_read_small(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    __threadfence_system();
+}
+struct Mapped {
+    std::mutex mu;
+    uint8_t* h = nullptr;
+    uint8_t* d = nullptr;
+};
+Mapped g_mapped[kMaxDevices];
+}  // namespace
+
+Status read_small(void* h_dst, const void* d_src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return Status::ok();
+    if (bytes > 4096) return Status::make(4, "read_small: more than 4096 bytes");
+    int dev = 0;
+    CL_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev >= kMaxDevices) return Status::make(4, "read_small: device ordinal beyond kMaxDevices");
+    Mapped& m = g_mapped[dev];
+    std::lock_guard<std::mutex> lk(m.mu);
+    if (!m.h) {
+        CL_CUDA_TRY(cudaHostAlloc((void**)&m.h, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
+        CL_CUDA_TRY(cudaHostGetDevicePointer((void**)&m.d, m.h, 0));
+    }
+    k_read_small<<<1, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(d_src), m.d, (int)bytes);
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    memcpy(h_dst, m.h, bytes);
+    return Status::ok();
+}
+
 // ---------------------------------------------------------------- device memory
 // Small buffers come from the device's default stream-ordered pool.  Large ones (>= 1 MiB:
 // the T replicas, CSR arrays, sort buffers) go through a process-wide cache of freed blocks,
@@ -290,6 +324,10 @@ struct cleora_graph {
     float* T[2] = {nullptr, nullptr};
     float* partials = nullptr;
     int32_t tag_dp = 0;             // row stride the hot-row tags in col (bit 31) were chosen for
+    // cleora_fetch_async: D2H on a copy stream, concurrent with later work on `stream`
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_copied = nullptr;
+    bool copy_pending = false;
     int32_t* occ = nullptr;         // chunked builds: endpoint occurrences per node (reading R14)
     int32_t n_graphs = 0;           // batched handles (cleora_build_batch): graphs in the batch
     int64_t* d_base = nullptr;      //   [n_graphs + 1] first row of every graph (device)
@@ -439,7 +477,17 @@ Status make_schedules(cleora_graph* g) {
     return Status::ok();
 }
 
+// An asynchronous fetch may still be reading T: stream-order the next write of T after it.
+void order_after_copy(cleora_graph* g) {
+    if (g->copy_pending) {
+        cudaStreamWaitEvent(g->stream, g->ev_copied, 0);
+        g->copy_pending = false;
+    }
+}
+
 void free_T(cleora_graph* g) {
+    if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);    // the blocks go back to the cache
+    g->copy_pending = false;
     close_peers(g);
     for (size_t p = 0; p < g->rep.size(); p++)
         if ((int)p != g->rank)
@@ -852,6 +900,7 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     if (!g) return usage("cleora_init: graph is NULL");
     if (d < 1 || d > CLEORA_MAX_D) return usage("cleora_init: d must be in [1, CLEORA_MAX_D]");
     DeviceGuard guard(g->device);
+    order_after_copy(g);
     const int32_t dp = (d + 3) / 4 * 4;
     if (dp != g->dp || !g->T[0]) {
         free_T(g);
@@ -941,6 +990,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
     if (k < 0) return usage("cleora_iterate: k must be >= 0");
     if (!g->T[0]) return usage("cleora_iterate: call cleora_init first");
     DeviceGuard guard(g->device);
+    order_after_copy(g);
     const int nsh = g->xmode == X_LOOPBACK ? g->world : 1;
     for (int32_t i = 0; i < k; i++) {
         const int in = g->cur, out = 1 - g->cur;
@@ -1029,6 +1079,37 @@ int cleora_fetch(const cleora_graph* g, int64_t row_begin, int64_t row_end, floa
                               (size_t)g->d * sizeof(float), (size_t)(row_end - row_begin), kind, g->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_fetch: ") + cudaGetErrorString(e)));
+    return CLEORA_OK;
+}
+
+int cleora_fetch_async(cleora_graph* g, int64_t row_begin, int64_t row_end, float* out, int32_t out_on_device) {
+    if (!g || !out) return usage("cleora_fetch_async: NULL argument");
+    if (!g->T[0]) return usage("cleora_fetch_async: call cleora_init first");
+    if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_fetch_async: rows outside [0, N]");
+    if (row_end == row_begin) return CLEORA_OK;
+    DeviceGuard guard(g->device);
+    cudaError_t e = cudaSuccess;
+    if (!g->copy_stream) {
+        e = cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_ready, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_copied, cudaEventDisableTiming);
+        if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_fetch_async: ") + cudaGetErrorString(e)));
+    }
+    // the copy starts when the work enqueued so far on the handle's stream is done
+    e = cudaEventRecord(g->ev_ready, g->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(g->copy_stream, g->ev_ready, 0);
+    const float* src = g->T[g->cur] + row_begin * (int64_t)g->dp;
+    const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (e == cudaSuccess) {
+        if (g->d == g->dp)
+            e = cudaMemcpyAsync(out, src, (size_t)(row_end - row_begin) * g->d * sizeof(float), kind, g->copy_stream);
+        else
+            e = cudaMemcpy2DAsync(out, (size_t)g->d * sizeof(float), src, (size_t)g->dp * sizeof(float),
+                                  (size_t)g->d * sizeof(float), (size_t)(row_end - row_begin), kind, g->copy_stream);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(g->ev_copied, g->copy_stream);
+    if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_fetch_async: ") + cudaGetErrorString(e)));
+    g->copy_pending = true;
     return CLEORA_OK;
 }
 
@@ -1125,10 +1206,9 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
     if (st.good() && n_new < N2) {
         // rows in [n_new, N2) must be empty: a new_idx >= n_new is out of range
         int64_t tail[2] = {0, 0};
-        cudaMemcpyAsync(&tail[0], b.row_ptr + n_new, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(&tail[1], b.row_ptr + N2, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
-        if (tail[1] != tail[0]) st = Status::make(3, "cleora_reconstruct: new_idx outside [0, n_new)");
+        st = read_small(&tail[0], b.row_ptr + n_new, sizeof(int64_t), s);
+        if (st.good()) st = read_small(&tail[1], b.row_ptr + N2, sizeof(int64_t), s);
+        if (st.good() && tail[1] != tail[0]) st = Status::make(3, "cleora_reconstruct: new_idx outside [0, n_new)");
     }
     if (st.good()) st = build_schedule(b.row_ptr, N2, 0, n_new, g->heavy_thresh, s, &sc);
     if (st.good()) st = dalloc((void**)&Tnew, (size_t)n_new * g->dp * sizeof(float), s, "reconstructed rows");
@@ -1210,6 +1290,7 @@ int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const f
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_set_rows: rows outside [0, N]");
     if (row_end == row_begin) return CLEORA_OK;
     DeviceGuard guard(g->device);
+    order_after_copy(g);
     // loopback: every emulated rank sets the same rows in its own replica
     const int nrep = g->xmode == X_LOOPBACK ? g->world : 1;
     cudaError_t e = cudaSuccess;
@@ -1295,6 +1376,7 @@ int cleora_sync(const cleora_graph* g) {
     if (!g) return usage("cleora_sync: graph is NULL");
     DeviceGuard guard(g->device);
     cudaError_t e = cudaStreamSynchronize(g->stream);
+    if (e == cudaSuccess && g->copy_stream) e = cudaStreamSynchronize(g->copy_stream);
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_sync: ") + cudaGetErrorString(e)));
     return CLEORA_OK;
 }
@@ -1318,6 +1400,9 @@ void cleora_destroy(cleora_graph* g) {
     for (auto& p : g->ev_spmm) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto& p : g->ev_x) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto e : g->ev_pool) cudaEventDestroy(e);
+    if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
+    if (g->ev_ready) cudaEventDestroy(g->ev_ready);
+    if (g->ev_copied) cudaEventDestroy(g->ev_copied);
     if (g->comm) nccl().CommDestroy(g->comm);
     if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
     delete g;

@@ -327,9 +327,8 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     count_launches(1);
     unsigned long long h_scal[2];
     int h_kind = 0;
-    CL_CUDA_TRY(cudaMemcpyAsync(h_scal, scal.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    CL_CUDA_TRY(cudaMemcpyAsync(&h_kind, err_kind.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    CL_TRY(read_small(h_scal, scal.p, 2 * sizeof(unsigned long long), s));
+    CL_TRY(read_small(&h_kind, err_kind.p, sizeof(int), s));
     if (h_kind) {
         char buf[256];
         snprintf(buf, sizeof buf, "cleora_build: edge %llu: %s", (unsigned long long)h_scal[0],
@@ -375,8 +374,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     }
     dfree(flags.release(), s);
     unsigned long long h_nnz = 0;
-    CL_CUDA_TRY(cudaMemcpyAsync(&h_nnz, scal.p + 4, sizeof h_nnz, cudaMemcpyDeviceToHost, s));
-    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    CL_TRY(read_small(&h_nnz, scal.p + 4, sizeof h_nnz, s));
     const int64_t nnz = (int64_t)h_nnz;
     trace("csr: run select", s, false);
 
@@ -421,8 +419,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     unsigned long long h_zm[2];
-    CL_CUDA_TRY(cudaMemcpyAsync(h_zm, scal.p + 2, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    CL_TRY(read_small(h_zm, scal.p + 2, 2 * sizeof(unsigned long long), s));
 
     out->nnz = nnz;
     out->zero_rows = (int64_t)h_zm[0];
@@ -475,8 +472,7 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, starts.p, cnt1.p, nr, pred, s));
         count_launches(2);
         int64_t nl = 0;
-        CL_CUDA_TRY(cudaMemcpyAsync(&nl, cnt1.p, sizeof nl, cudaMemcpyDeviceToHost, s));
-        CL_CUDA_TRY(cudaStreamSynchronize(s));
+        CL_TRY(read_small(&nl, cnt1.p, sizeof nl, s));
         const int64_t end = r1;
         CL_CUDA_TRY(cudaMemcpyAsync(starts.p + nl, &end, sizeof end, cudaMemcpyHostToDevice, s));
         CL_CUDA_TRY(cudaStreamSynchronize(s));   // `end` lives on this stack frame
@@ -497,8 +493,7 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         count_launches(2);
     }
     int64_t nh = 0;
-    CL_CUDA_TRY(cudaMemcpyAsync(&nh, cnt.p, sizeof nh, cudaMemcpyDeviceToHost, s));
-    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    CL_TRY(read_small(&nh, cnt.p, sizeof nh, s));
     out->n_heavy_rows = nh;
     if (nh == 0) return Status::ok();
     const int64_t per_item = (int64_t)heavy_thresh * kWarpsPerCta;
@@ -517,9 +512,8 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         count_launches(2);
     }
     int64_t last[2];
-    CL_CUDA_TRY(cudaMemcpyAsync(&last[0], first.p + nh - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    CL_CUDA_TRY(cudaMemcpyAsync(&last[1], nit.p + nh - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    CL_TRY(read_small(&last[0], first.p + nh - 1, sizeof(int64_t), s));
+    CL_TRY(read_small(&last[1], nit.p + nh - 1, sizeof(int64_t), s));
     const int64_t n_items = last[0] + last[1];
     DevBuf<HeavyItem> items;
     DevBuf<unsigned> counters;
@@ -597,8 +591,7 @@ Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_
     if (K > N) K = N;
     int32_t t = INT32_MAX;
     if (K > 0) {
-        CL_CUDA_TRY(cudaMemcpyAsync(&t, sorted.p + (N - K), sizeof t, cudaMemcpyDeviceToHost, s));
-        CL_CUDA_TRY(cudaStreamSynchronize(s));
+        CL_TRY(read_small(&t, sorted.p + (N - K), sizeof t, s));
         if (t < 2) t = 2;                 // a row read once or never gains nothing from pinning
     }
     CL_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, 3 * sizeof(unsigned long long), s));
@@ -606,8 +599,7 @@ Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     unsigned long long c[3];
-    CL_CUDA_TRY(cudaMemcpyAsync(c, cnt.p, sizeof c, cudaMemcpyDeviceToHost, s));
-    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    CL_TRY(read_small(c, cnt.p, sizeof c, s));
     int64_t nh = (int64_t)c[0];           // rows with in-degree >= t
     if (t != INT32_MAX && nh > K + K / 4) {
         t += 1;
@@ -664,8 +656,7 @@ Status batch_global_ids(const int32_t* d_src, const int32_t* d_dst, int64_t E, c
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     unsigned long long h = 0;
-    CL_CUDA_TRY(cudaMemcpyAsync(&h, err.p, sizeof h, cudaMemcpyDeviceToHost, s));
-    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    CL_TRY(read_small(&h, err.p, sizeof h, s));
     if (h != ~0ull) {
         char buf[160];
         snprintf(buf, sizeof buf, "cleora_build_batch: edge %llu: node id outside [0, node_count) of its graph", h);
@@ -680,8 +671,7 @@ Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s
     k_cuts<<<1, 128, 0, s>>>(d_row_ptr, N, world, cuts.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
-    CL_CUDA_TRY(cudaMemcpyAsync(h_cuts, cuts.p, (world + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    CL_CUDA_TRY(cudaStreamSynchronize(s));
+    CL_TRY(read_small(h_cuts, cuts.p, (world + 1) * sizeof(int64_t), s));
     return Status::ok();
 }
 

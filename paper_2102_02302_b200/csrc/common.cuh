@@ -33,6 +33,11 @@ struct Status {
         if (!_s.good()) return _s;                                                         \
     } while (0)
 
+// Read `bytes` (<= 4096) of device memory into host memory, in stream order, then wait for the
+// stream.  A kernel stores them into mapped pinned memory, so the read never queues behind a large
+// device-to-host DMA on the copy engine (cleora_fetch_async of another handle).
+Status read_small(void* h_dst, const void* d_src, size_t bytes, cudaStream_t s);
+
 // Host-side phase trace (stderr) when CLEORA_TRACE is set; `sync` waits for the stream first.
 void trace(const char* what, cudaStream_t s, bool sync);
 

@@ -99,10 +99,9 @@ Status expand_hypergraph(const int64_t* d_ptr, const int32_t* d_nodes, const flo
         k_expand_check<<<warp_grid((n + 31) / 32), kThreads, 0, s>>>(d_nodes, n_members, n_nodes, d_w, n_he, bad);
         count_launches(1);
         unsigned long long h[2];
-        cudaError_t e = cudaMemcpyAsync(h, bad, sizeof h, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        Status rs = read_small(h, bad, sizeof h, s);
         dfree(bad, s);
-        CL_CUDA_TRY(e);
+        CL_TRY(rs);
         char buf[160];
         if (h[0] != ~0ull) {
             snprintf(buf, sizeof buf, "cleora_expand: member %llu: node id outside [0, n_nodes)", h[0]);
@@ -141,9 +140,7 @@ Status expand_hypergraph(const int64_t* d_ptr, const int32_t* d_nodes, const flo
     if (st.good()) {
         cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, n_he + 1, s);
         count_launches(2);
-        cudaError_t e = cudaMemcpyAsync(&total, off + n_he, sizeof total, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) st = Status::make(4, std::string("cleora_expand: ") + cudaGetErrorString(e));
+        st = read_small(&total, off + n_he, sizeof total, s);
     }
     if (st.good()) {
         *n_out = total;

@@ -262,3 +262,29 @@ def test_tma_and_register_kernels_bitwise_equal(cl, d, monkeypatch):
         outs.append(cl.cleora_fetch(G))
         G.close()
     assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_fetch_async_overlaps_and_is_ordered(cl):
+    """cleora_fetch_async copies the current T while later work runs; later iterations of the same
+    handle are ordered after the copy (the copied rows are T_2, not a mix with T_3 / T_4)."""
+    import torch
+    g = gen.config("c1")
+    G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0)
+    cl.cleora_init(G, 128, 0)
+    cl.cleora_iterate(G, 2)
+    ref2 = cl.cleora_fetch(G)
+    out = torch.empty((g.n, 128), dtype=torch.float32).pin_memory()
+    cl.cleora_fetch_async(G, 0, g.n, out)
+    cl.cleora_iterate(G, 2)                           # overwrites both buffers after the copy
+    cl.cleora_sync(G)
+    assert out.numpy().tobytes() == ref2.tobytes()
+    ref4 = cl.cleora_fetch(G)
+    G2 = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0)
+    cl.cleora_init(G2, 128, 0)
+    cl.cleora_iterate(G2, 4)
+    assert cl.cleora_fetch(G2).tobytes() == ref4.tobytes()
+    part = torch.empty((100, 128), dtype=torch.float32, device="cuda")
+    cl.cleora_fetch_async(G2, 50, 150, part)          # device destination, row range
+    G2.close()                                        # destroy waits for the copy
+    assert part.cpu().numpy().tobytes() == ref4[50:150].tobytes()
+    G.close()
