@@ -938,10 +938,10 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     g->cur = 0;
     g->iters = 0;
     g->zclean[0] = g->zclean[1] = false;
-    // heavy rows: > 64 entries on the TMA kernel, > 256 on the register kernel (measured: c2 12.68 vs
-    // 12.80 ms per step with 64 / 256; c5 427 -> 375 ms with 256); every sequential fp32 run stays
-    // <= 256 terms (256-entry blocks keep the error ~3e-7)
-    g->heavy_thresh = heavy_thresh_default(tma_path_supported(dp) ? 64 : 256);
+    // heavy rows: > 64 entries with TMA bulk gathers, > 256 with cp.async / LDG gathers (measured:
+    // c2 12.68 vs 12.80 ms per step with 64 / 256; c5 427 -> 375 ms, c4@256 8.10 -> 7.27 ms with 256);
+    // every sequential fp32 run stays <= 256 terms (256-entry blocks keep the error ~3e-7)
+    g->heavy_thresh = heavy_thresh_default(gather_mode(dp) == kGatherBulk ? 64 : 256);
     if (g->sched_thresh != g->heavy_thresh) {
         Status s = make_schedules(g);
         if (!s.good()) return fail(s);

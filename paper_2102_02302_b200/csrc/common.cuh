@@ -177,7 +177,9 @@ Status batch_global_ids(const int32_t* d_src, const int32_t* d_dst, int64_t E, c
 
 // spmm_norm.cu (register gathers; any d) and spmm_tma.cu (TMA bulk gathers; dp <= 1024)
 Status launch_spmm_norm(const SpmmArgs& a, cudaStream_t s);
-bool tma_path_supported(int dp);
+enum { kGatherLdg = 0, kGatherBulk = 1, kGatherAsync = 2 };
+int gather_mode(int dp);          // which gather engine serves rows of dp floats
+bool tma_path_supported(int dp);  // gather_mode(dp) uses the shared-memory ring kernel
 Status launch_spmm_tma(const SpmmArgs& a, cudaStream_t s);
 
 }  // namespace cleora

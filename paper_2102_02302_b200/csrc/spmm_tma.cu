@@ -18,6 +18,7 @@
 // Each row accumulates its entries in ascending order from 0, exactly as spmm_norm.cu does, so
 // both kernels produce bitwise identical results.
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -112,11 +113,49 @@ struct Ring {
 
 // c: column index, bit 31 set when the row is "hot" (high in-degree, see hot_tag in build.cu):
 // hot rows are gathered with an evict_last L2 policy so the most re-read rows stay resident.
+//
+// Two ways to fill a slot.  SA == 0: lane 0 issues one 1-D bulk copy (TMA, cp.async.bulk) that
+// completes on the slot's mbarrier.  SA > 0 (rows below 2 KB, where the bulk-copy engine's issue
+// rate binds): every lane copies its own float4 columns with 16-byte cp.async (LDGSTS) and
+// commits one cp.async group per slot; a lane only ever reads the columns it copied, so
+// `cp.async.wait_group SA-1` (all but the SA-1 most recent groups complete) is the whole
+// handshake.  Exactly one group is committed per issue -- an empty one past the end of the
+// stream -- so that positional wait always names the slot being consumed.
+template <int V, bool FULL, int SA>
 __device__ __forceinline__ void ring_issue(const SpmmArgs& a, Ring& r, int slot, int32_t c, int lane) {
+    if (SA > 0) {
+        const int dp = FULL ? 128 * V : a.dp;
+        const float4* src = reinterpret_cast<const float4*>(a.T_in + (int64_t)(c & 0x7fffffff) * dp) + lane;
+        float4* dst = r.buf + (size_t)slot * r.slot_f4 + lane;
+        const uint64_t pol = c < 0 ? r.pol_hot : r.pol_cold;
+#pragma unroll
+        for (int v = 0; v < V; v++)
+            if (FULL || 4 * (lane + 32 * v) < dp)
+                asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(saddr(dst + 32 * v)),
+                             "l"(src + 32 * v), "l"(pol)
+                             : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        return;
+    }
     if (lane == 0) {
         mbar_expect_tx(r.bar + slot, r.bytes);
         bulk_g2s_hint(r.buf + (size_t)slot * r.slot_f4, a.T_in + (int64_t)(c & 0x7fffffff) * a.dp, r.bytes,
                       r.bar + slot, c < 0 ? r.pol_hot : r.pol_cold);
+    }
+}
+
+template <int SA>
+__device__ __forceinline__ void ring_skip() {       // keep one group per issue (see ring_issue)
+    if (SA > 0) asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int SA>
+__device__ __forceinline__ void ring_wait(Ring& r, int sl) {
+    if (SA > 0) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(SA > 0 ? SA - 1 : 0) : "memory");
+    } else {
+        mbar_wait(r.bar + sl, (r.ph >> sl) & 1u);
+        r.ph ^= 1u << sl;
     }
 }
 
@@ -144,7 +183,7 @@ __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, f
 // Stream CSR entries [E0, E1) through the warp's ring into acc.  ROWS: the entries belong to
 // rows [ra, rz) whose bounds are in rpl (lane i holds row_ptr[rb + i]); rows are finalised at
 // their boundaries (zero rows included).  On return every issued copy has been consumed.
-template <int V, bool FULL, bool ROWS>
+template <int V, bool FULL, bool ROWS, int SA>
 __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E1, float4 (&acc)[V], int64_t rb,
                                int64_t rpl, int64_t ra, int64_t rz, int lane) {
     const int dp = FULL ? 128 * V : a.dp;
@@ -161,15 +200,16 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
         mc1 = ld_stream_i32(colp + E0 + 32 + lane, r.pol_csr);
         mw1 = ld_stream_f32(a.val + E0 + 32 + lane, r.pol_csr);
     }
-    // prologue: the first min(S, n) entries
+    // prologue: the first min(S, n) entries (cp.async mode: S groups, empty ones past the end)
     {
         const int pro = (int)min((int64_t)r.S, E1 - E0);
         int sl = r.cs;
         for (int i = 0; i < pro; i++) {
             const int32_t c = __shfl_sync(kFull, mc0, i);
-            ring_issue(a, r, sl, c, lane);
+            ring_issue<V, FULL, SA>(a, r, sl, c, lane);
             sl = (sl + 1 == r.S) ? 0 : sl + 1;
         }
+        for (int i = pro; i < (SA > 0 ? SA : 0); i++) ring_skip<SA>();
     }
     for (int64_t kb = E0; kb < E1; kb += 32) {
         const int n = (int)min((int64_t)32, E1 - kb);
@@ -185,8 +225,7 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
             }
             const float w = __shfl_sync(kFull, mw0, j);
             const int sl = r.cs;
-            mbar_wait(r.bar + sl, (r.ph >> sl) & 1u);
-            r.ph ^= 1u << sl;
+            ring_wait<SA>(r, sl);
             const float4* src = r.buf + (size_t)sl * r.slot_f4 + lane;
 #pragma unroll
             for (int v = 0; v < V; v++)
@@ -195,7 +234,10 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
             // refill the slot just consumed with entry e + S (S <= 32, so it is in block 0 or 1)
             const int jp = j + r.S;
             const int32_t cp = (jp < 32) ? __shfl_sync(kFull, mc0, jp) : __shfl_sync(kFull, mc1, jp - 32);
-            if (e + r.S < E1) ring_issue(a, r, sl, cp, lane);
+            if (e + r.S < E1)
+                ring_issue<V, FULL, SA>(a, r, sl, cp, lane);
+            else
+                ring_skip<SA>();
             r.cs = (sl + 1 == r.S) ? 0 : sl + 1;
         }
         mc0 = mc1;
@@ -217,7 +259,7 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
     }
 }
 
-template <int V, bool FULL>
+template <int V, bool FULL, int SA>
 __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* smem, int ring_f4, double* scratch,
                              int* flag) {
     const HeavyItem it = a.items[idx];
@@ -230,7 +272,7 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
     float4 acc[V];
 #pragma unroll
     for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    stream_entries<V, FULL, false>(a, r, wk0, wk1, acc, 0, 0, 0, 0, lane);
+    stream_entries<V, FULL, false, SA>(a, r, wk0, wk1, acc, 0, 0, 0, 0, lane);
     // this warp's partial vector -> slot 0 of its ring (drained), combined in warp order
     float4* red = r.buf;
 #pragma unroll
@@ -284,7 +326,7 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
     fence_proxy_async_smem();     // accesses before the async-proxy writes
 }
 
-template <int V, bool FULL>
+template <int V, bool FULL, int SA>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArgs a, int S) {
     extern __shared__ __align__(128) float4 smem[];
     __shared__ double scratch[kWarpsPerCta];
@@ -306,9 +348,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
     r.pol_hot = policy_evict_last();
     r.pol_cold = a.cold_first ? policy_evict_first() : policy_evict_normal();
     r.pol_csr = policy_evict_first();
-    if (lane == 0)
-        for (int i = 0; i < S; i++) mbar_init(r.bar + i, 1);
-    mbar_fence_init();
+    if (SA == 0) {
+        if (lane == 0)
+            for (int i = 0; i < S; i++) mbar_init(r.bar + i, 1);
+        mbar_fence_init();
+    }
     __syncthreads();
 
     if (a.n_items > 0) {
@@ -318,7 +362,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
             const int64_t it = s_item;
             __syncthreads();
             if (it >= a.n_items) break;
-            heavy_item_t<V, FULL>(a, it, r, smem, ring_f4, scratch, &flag);
+            heavy_item_t<V, FULL, SA>(a, it, r, smem, ring_f4, scratch, &flag);
         }
     }
     const int64_t nchunks = a.n_light;
@@ -350,7 +394,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
                 z++;
             }
             const int64_t E1 = __shfl_sync(kFull, rpl, (int)(z - rb));
-            stream_entries<V, FULL, true>(a, r, E0, E1, acc, rb, rpl, row, z, lane);
+            stream_entries<V, FULL, true, SA>(a, r, E0, E1, acc, rb, rpl, row, z, lane);
             row = z;
         }
     }
@@ -375,7 +419,7 @@ struct TmaCfg {
 };
 
 // Launch configuration per device (the smem attribute is per device) and row stride.
-template <int V, bool FULL>
+template <int V, bool FULL, int SA>
 Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
     static TmaCfg cfg[kMaxDevices];
     static std::mutex mu;
@@ -389,15 +433,15 @@ Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
         if (cc.dp != a.dp) {
             const int slot = a.dp * 4;
             // per-CTA ring budget ~96 KB so that two CTAs (16 warps) share an SM
-            int S = (96 * 1024) / (kWarpsPerCta * slot);
-            if (S > 16) S = 16;
+            int S = SA > 0 ? SA : (96 * 1024) / (kWarpsPerCta * slot);
+            if (S > 16 && SA == 0) S = 16;
             if (S < 2) S = 2;
             cc.S = S;
-            cc.smem = (size_t)kWarpsPerCta * S * slot + (size_t)kWarpsPerCta * S * sizeof(uint64_t);
-            CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_tma<V, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cc.smem = (size_t)kWarpsPerCta * S * slot + (SA > 0 ? 0 : (size_t)kWarpsPerCta * S * sizeof(uint64_t));
+            CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_tma<V, FULL, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)cc.smem));
             CL_CUDA_TRY(cudaDeviceGetAttribute(&cc.sms, cudaDevAttrMultiProcessorCount, dev));
-            CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cc.blocks_per_sm, k_spmm_tma<V, FULL>,
+            CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cc.blocks_per_sm, k_spmm_tma<V, FULL, SA>,
                                                                       kWarpsPerCta * 32, cc.smem));
             if (cc.blocks_per_sm < 1) cc.blocks_per_sm = 1;
             cc.dp = a.dp;
@@ -405,32 +449,55 @@ Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
         c = cc;
     }
     if (a.r1 <= a.r0 && a.n_items == 0) return Status::ok();
-    k_spmm_tma<V, FULL><<<c.sms * c.blocks_per_sm, kWarpsPerCta * 32, c.smem, s>>>(a, c.S);
+    k_spmm_tma<V, FULL, SA><<<c.sms * c.blocks_per_sm, kWarpsPerCta * 32, c.smem, s>>>(a, c.S);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     return Status::ok();
 }
 
-}  // namespace
+// cp.async ring depth by row width (~96 KB of ring per CTA; <= 32 for the CSR register windows)
+template <int V>
+constexpr int kAsyncSlots = V == 1 ? 24 : (V == 2 ? 12 : 6);
 
-// TMA bulk gathers win for rows of >= 2 KB; below that the per-copy issue rate of the bulk-copy
-// engine binds (~6.7e9 copies/s on B200: c5 at d = 256 made 2.84e9 copies in 0.43 s with DRAM
-// 58% busy) and the register kernel's 16-byte LDGs are faster (measured, c4 at d = 64 / 128 /
-// 256: 5.7 / 6.4 / 8.3 ms vs 7.8 / 8.9 / 9.4 ms; equal at d = 512; TMA 2.78 vs 3.48 ms at 1024).
-bool tma_path_supported(int dp) {
-    if (dp > 1024 || getenv("CLEORA_NO_TMA")) return false;
-    return dp >= 512 || getenv("CLEORA_FORCE_TMA") != nullptr;
+template <int V, bool FULL>
+Status launch_mode(const SpmmArgs& a, cudaStream_t s, int mode) {
+    if (mode == kGatherAsync) return launch_tma_v<V, FULL, kAsyncSlots<V>>(a, s);
+    return launch_tma_v<V, FULL, 0>(a, s);
 }
 
+}  // namespace
+
+// Gather engine by row size (measured on B200, ms per SpMM launch):
+//  - rows of 2-4 KB (512 <= dp <= 1024): TMA bulk copies, one per neighbour row issued by one lane
+//    (c2 2.78 vs LDG 3.48);
+//  - 0.5-2 KB (128 < dp < 512): the bulk-copy engine's issue rate binds (~6.7e9 copies/s: c5 made
+//    2.84e9 copies in 0.43 s with DRAM 58% busy), per-lane 16-byte cp.async into the same ring
+//    does not (c5 332 vs bulk 432 vs LDG 357; c4 at d = 256: 7.27 vs 9.45 vs 8.16);
+//  - <= 512 B (dp <= 128): the register kernel at 32 warps per SM (c4 at d = 128: LDG 5.10 vs
+//    cp.async 6.55 vs bulk 8.93);
+//  - > 4 KB: the register kernel (column slices).
+// CLEORA_GATHER=bulk|async|ldg overrides (CLEORA_NO_TMA = ldg, CLEORA_FORCE_TMA = bulk).
+int gather_mode(int dp) {
+    const char* e = getenv("CLEORA_GATHER");
+    if (dp > 1024 || getenv("CLEORA_NO_TMA") || (e && !strcmp(e, "ldg"))) return kGatherLdg;
+    if (getenv("CLEORA_FORCE_TMA") || (e && !strcmp(e, "bulk"))) return kGatherBulk;
+    if (e && !strcmp(e, "async")) return kGatherAsync;
+    if (dp >= 512) return kGatherBulk;
+    return dp > 128 ? kGatherAsync : kGatherLdg;
+}
+
+bool tma_path_supported(int dp) { return gather_mode(dp) != kGatherLdg; }
+
 Status launch_spmm_tma(const SpmmArgs& a, cudaStream_t s) {
-    if (a.dp == 1024) return launch_tma_v<8, true>(a, s);
-    if (a.dp == 512) return launch_tma_v<4, true>(a, s);
-    if (a.dp == 256) return launch_tma_v<2, true>(a, s);
-    if (a.dp == 128) return launch_tma_v<1, true>(a, s);
-    if (a.dp < 128) return launch_tma_v<1, false>(a, s);
-    if (a.dp < 256) return launch_tma_v<2, false>(a, s);
-    if (a.dp < 512) return launch_tma_v<4, false>(a, s);
-    return launch_tma_v<8, false>(a, s);
+    const int mode = gather_mode(a.dp);
+    if (a.dp == 1024) return launch_mode<8, true>(a, s, mode);
+    if (a.dp == 512) return launch_mode<4, true>(a, s, mode);
+    if (a.dp == 256) return launch_mode<2, true>(a, s, mode);
+    if (a.dp == 128) return launch_mode<1, true>(a, s, mode);
+    if (a.dp < 128) return launch_mode<1, false>(a, s, mode);
+    if (a.dp < 256) return launch_mode<2, false>(a, s, mode);
+    if (a.dp < 512) return launch_mode<4, false>(a, s, mode);
+    return launch_mode<8, false>(a, s, mode);
 }
 
 }  // namespace cleora

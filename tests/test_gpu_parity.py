@@ -233,9 +233,9 @@ def test_info_and_stats(cl):
     deg = np.bincount(np.concatenate([g.src, g.dst]), minlength=g.n)
     assert info["zero_rows"] == int((deg == 0).sum()) and info["max_degree"] == int(deg.max())
     cl.cleora_init(G, 128, 0)
-    assert cl.cleora_info(G)["heavy_rows"] == int((deg > 256).sum())    # register kernel: > 256 entries
+    assert cl.cleora_info(G)["heavy_rows"] == int((deg > 256).sum())    # LDG / cp.async gathers: > 256 entries
     cl.cleora_init(G, 1024, 0)
-    assert cl.cleora_info(G)["heavy_rows"] == int((deg > 64).sum())     # TMA kernel: > 64 entries
+    assert cl.cleora_info(G)["heavy_rows"] == int((deg > 64).sum())     # TMA bulk gathers: > 64 entries
     cl.cleora_iterate(G, 3)
     st = cl.cleora_stats(G, reset=True)
     assert st["spmm_launches"] == 3 and st["spmm_ms_total"] > 0
@@ -244,24 +244,21 @@ def test_info_and_stats(cl):
 
 
 @pytest.mark.parametrize("d", [100, 256, 600, 1024])
-def test_tma_and_register_kernels_bitwise_equal(cl, d, monkeypatch):
-    """The TMA-gather kernel (spmm_tma.cu) and the register-gather kernel (spmm_norm.cu) run the
-    same per-row arithmetic in the same order, so their outputs are bitwise identical."""
+def test_gather_engines_bitwise_equal(cl, d, monkeypatch):
+    """The three gather engines -- TMA bulk copies, per-lane cp.async into the same shared-memory
+    ring (spmm_tma.cu), and register LDGs (spmm_norm.cu) -- run the same per-row arithmetic in the
+    same order, so their outputs are bitwise identical."""
     g = gen.chung_lu(30000, 90000, 2.1, 9.5388, 233115.5 * 30000 / 1134890, seed=3)
-    monkeypatch.setenv("CLEORA_HEAVY_THRESH", "64")       # the same schedule for both kernels
+    monkeypatch.setenv("CLEORA_HEAVY_THRESH", "64")       # the same schedule for every engine
     outs = []
-    for no_tma in (False, True):
-        if no_tma:
-            monkeypatch.delenv("CLEORA_FORCE_TMA", raising=False)
-            monkeypatch.setenv("CLEORA_NO_TMA", "1")
-        else:
-            monkeypatch.setenv("CLEORA_FORCE_TMA", "1")    # TMA also below its default dp >= 512
+    for mode in ("bulk", "async", "ldg"):
+        monkeypatch.setenv("CLEORA_GATHER", mode)
         G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0)
         cl.cleora_init(G, d, 0)
         cl.cleora_iterate(G, 3)
         outs.append(cl.cleora_fetch(G))
         G.close()
-    assert outs[0].tobytes() == outs[1].tobytes()
+    assert outs[0].tobytes() == outs[1].tobytes() == outs[2].tobytes()
 
 
 def test_fetch_async_overlaps_and_is_ordered(cl):
