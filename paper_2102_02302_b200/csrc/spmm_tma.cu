@@ -457,7 +457,7 @@ Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
 
 // cp.async ring depth by row width (~96 KB of ring per CTA; <= 32 for the CSR register windows)
 template <int V>
-constexpr int kAsyncSlots = V == 1 ? 24 : (V == 2 ? 12 : 6);
+constexpr int kAsyncSlots = V == 1 ? 24 : (V == 2 ? 12 : (V == 4 ? 6 : 3));
 
 template <int V, bool FULL>
 Status launch_mode(const SpmmArgs& a, cudaStream_t s, int mode) {
@@ -468,11 +468,12 @@ Status launch_mode(const SpmmArgs& a, cudaStream_t s, int mode) {
 }  // namespace
 
 // Gather engine by row size (measured on B200, ms per SpMM launch):
-//  - rows of 2-4 KB (512 <= dp <= 1024): TMA bulk copies, one per neighbour row issued by one lane
-//    (c2 2.78 vs LDG 3.48);
-//  - 0.5-2 KB (128 < dp < 512): the bulk-copy engine's issue rate binds (~6.7e9 copies/s: c5 made
+//  - 4 KB rows (dp = 1024): TMA bulk copies, one per neighbour row issued by one lane (c2 2.54 min,
+//    cp.async the same, LDG 3.48 mean);
+//  - 0.5-4 KB (128 < dp < 1024): the bulk-copy engine's issue rate binds (~6.7e9 copies/s: c5 made
 //    2.84e9 copies in 0.43 s with DRAM 58% busy), per-lane 16-byte cp.async into the same ring
-//    does not (c5 332 vs bulk 432 vs LDG 357; c4 at d = 256: 7.27 vs 9.45 vs 8.16);
+//    does not (c5 332 vs bulk 432 vs LDG 357; c4 at d = 256: 7.27 vs 9.45 vs 8.16; at d = 512:
+//    12.8 vs 18.9 vs 16.3);
 //  - <= 512 B (dp <= 128): the register kernel at 32 warps per SM (c4 at d = 128: LDG 5.10 vs
 //    cp.async 6.55 vs bulk 8.93);
 //  - > 4 KB: the register kernel (column slices).
@@ -482,7 +483,7 @@ int gather_mode(int dp) {
     if (dp > 1024 || getenv("CLEORA_NO_TMA") || (e && !strcmp(e, "ldg"))) return kGatherLdg;
     if (getenv("CLEORA_FORCE_TMA") || (e && !strcmp(e, "bulk"))) return kGatherBulk;
     if (e && !strcmp(e, "async")) return kGatherAsync;
-    if (dp >= 512) return kGatherBulk;
+    if (dp == 1024) return kGatherBulk;
     return dp > 128 ? kGatherAsync : kGatherLdg;
 }
 
