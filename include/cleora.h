@@ -283,7 +283,7 @@ CLEORA_API int64_t cleora_kernel_launches(void);
 
 /* Device blocks of >= 1 MiB freed by cleora_destroy (T replicas, CSR, sort buffers) are kept
  * in a process-wide cache and reused by later handles of the same sizes (no allocator growth
- * between repeated build/embed/destroy cycles), up to CLEORA_CACHE_MAX_FRAC (default 0.6) of
+ * between repeated build/embed/destroy cycles), up to CLEORA_CACHE_MAX_FRAC (default 0.8) of
  * device memory; CLEORA_NO_CACHE=1 disables it.  This call returns every cached block to the
  * driver (e.g. before handing the memory to another library).  Returns CLEORA_OK or
  * EINTERNAL. */

@@ -129,6 +129,29 @@ void release_cached(int dev /* -1: all */, cudaStream_t s) {
     if (cur >= 0) cudaSetDevice(cur);
     (void)s;
 }
+
+// Return the largest cached block of `dev` to the driver; false when there is none.
+bool release_largest(int dev) {
+    Block b{};
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        size_t best = 0;
+        int at = -1;
+        for (size_t i = 0; i < g_cache.size(); i++)
+            if (g_cache[i].dev == dev && g_cache[i].bytes > best) {
+                best = g_cache[i].bytes;
+                at = (int)i;
+            }
+        if (at < 0) return false;
+        b = g_cache[at];
+        g_cached_bytes -= b.bytes;
+        g_cache.erase(g_cache.begin() + at);
+    }
+    cudaEventSynchronize(b.ready);
+    cudaEventDestroy(b.ready);
+    cudaFree(b.p);
+    return true;
+}
 }  // namespace
 
 Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what) {
@@ -164,7 +187,7 @@ Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what) {
             }
         }
     }
-    for (int attempt = 0; attempt < 2; attempt++) {
+    for (;;) {
         cudaError_t e;
         if (big) {
             // cached blocks are plain device allocations (not pool memory): they outlive streams
@@ -175,11 +198,9 @@ Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what) {
         if (e == cudaSuccess) break;
         cudaGetLastError();
         *p = nullptr;
-        if (e == cudaErrorMemoryAllocation && attempt == 0) {
-            cudaStreamSynchronize(s);
-            release_cached(dev, s);
-            continue;
-        }
+        // out of memory: give cached blocks back to the driver, largest first, until it fits (the
+        // rest stays cached for the next graph of the same shape)
+        if (e == cudaErrorMemoryAllocation && release_largest(dev)) continue;
         char buf[256];
         snprintf(buf, sizeof buf, "cudaMalloc(%zu bytes) for %s: %s", bytes, what, cudaGetErrorString(e));
         return Status::make(4, buf);
@@ -205,7 +226,7 @@ static size_t cache_cap_bytes(int dev) {
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
         const char* e = getenv("CLEORA_CACHE_MAX_FRAC");
-        const double f = e ? atof(e) : 0.6;
+        const double f = e ? atof(e) : 0.8;
         cap[dev] = (size_t)(f * (double)tot) + 1;
     }
     return cap[dev];
@@ -961,7 +982,8 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
         // budget of the 126 MB L2
         const char* e = getenv("CLEORA_HOT_MB");
         const int64_t budget = (int64_t)(e ? atof(e) : 72.0) * 1024 * 1024;
-        Status s = hot_tag(g->col, g->nnz, g->n, (int64_t)dp * 4, budget, g->stream, &g->n_hot, &g->n_ref);
+        Status s = hot_tag(g->col, g->nnz, g->n, (int64_t)dp * 4, budget, g->stream, &g->n_hot, &g->n_ref,
+                           g->directed ? nullptr : g->row_ptr);
         if (!s.good()) {
             free_T(g);
             return fail(s);

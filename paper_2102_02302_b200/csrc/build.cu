@@ -57,7 +57,7 @@ __global__ void k_validate_expand(const int32_t* __restrict__ src, const int32_t
             atomicAdd(occ + v, 1);
         }
         keys[i] = keep ? (uint64_t)(uint32_t)u * (uint64_t)N + (uint64_t)(uint32_t)v : sentinel;
-        pos[i] = (uint32_t)i;
+        if (pos) pos[i] = (uint32_t)i;
         unsigned long long drop = keep ? 0 : 1;
         if (!directed) {
             if (!keep || u == v) {
@@ -66,7 +66,7 @@ __global__ void k_validate_expand(const int32_t* __restrict__ src, const int32_t
             } else {
                 keys[E + i] = (uint64_t)(uint32_t)v * (uint64_t)N + (uint64_t)(uint32_t)u;
             }
-            pos[E + i] = (uint32_t)(E + i);
+            if (pos) pos[E + i] = (uint32_t)(E + i);
         }
         if (drop) atomicAdd(n_drop, drop);
     }
@@ -309,10 +309,15 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     DevBuf<uint32_t> pos, pos2;
     DevBuf<unsigned long long> scal;                     // [0] err_first [1] n_self [2] zero_rows [3] max_deg [4] nnz
     DevBuf<int> err_kind;
+    // unit weights: e_ab is the run length, the same in any order, so the sort needs no payload
+    // (positions only order the fp64 sums of weighted duplicates, reading B2) -- a third less traffic
+    const bool keys_only = d_w == nullptr;
     CL_TRY(keys.alloc(n_ent, s, "sort keys"));
     CL_TRY(keys2.alloc(n_ent, s, "sort keys (alt)"));
-    CL_TRY(pos.alloc(n_ent, s, "sort payload"));
-    CL_TRY(pos2.alloc(n_ent, s, "sort payload (alt)"));
+    if (!keys_only) {
+        CL_TRY(pos.alloc(n_ent, s, "sort payload"));
+        CL_TRY(pos2.alloc(n_ent, s, "sort payload (alt)"));
+    }
     CL_TRY(scal.alloc(8, s, "scalars"));
     CL_TRY(err_kind.alloc(1, s, "scalars"));
     CL_CUDA_TRY(cudaMemsetAsync(scal.p, 0, 8 * sizeof(unsigned long long), s));
@@ -344,13 +349,19 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         cub::DoubleBuffer<uint64_t> kb(keys.p, keys2.p);
         cub::DoubleBuffer<uint32_t> vb(pos.p, pos2.p);
         size_t tmp_bytes = 0;
-        CL_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, n_ent, 0, end_bit, s));
+        if (keys_only)
+            CL_CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, kb, n_ent, 0, end_bit, s));
+        else
+            CL_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, n_ent, 0, end_bit, s));
         DevBuf<uint8_t> tmp;
         CL_TRY(tmp.alloc(tmp_bytes, s, "radix sort temp"));
-        CL_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kb, vb, n_ent, 0, end_bit, s));
+        if (keys_only)
+            CL_CUDA_TRY(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, kb, n_ent, 0, end_bit, s));
+        else
+            CL_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kb, vb, n_ent, 0, end_bit, s));
         count_launches(2 + (end_bit + 7) / 8);            // histogram, exclusive sum, one onesweep pass per 8 bits
         if (kb.Current() != keys.p) std::swap(keys.p, keys2.p);
-        if (vb.Current() != pos.p) std::swap(pos.p, pos2.p);
+        if (!keys_only && vb.Current() != pos.p) std::swap(pos.p, pos2.p);
     }
     dfree(keys2.release(), s);
     trace("csr: radix sort", s, true);
@@ -530,6 +541,12 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
 }
 
 namespace {
+// undirected graphs: M's pattern is symmetric, so a node's in-degree is its row length
+__global__ void k_row_lengths(const int64_t* __restrict__ rp, int32_t N, int32_t* __restrict__ len) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < N; v += stride)
+        len[v] = (int32_t)(rp[v + 1] - rp[v]);
+}
 __global__ void k_indegree(const int32_t* __restrict__ col, int64_t nnz, int32_t* __restrict__ indeg) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride)
@@ -566,7 +583,7 @@ __global__ void k_tag(int32_t* __restrict__ col, int64_t nnz, const int32_t* __r
 }  // namespace
 
 Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes, cudaStream_t s,
-               int64_t* n_hot, int64_t* n_ref) {
+               int64_t* n_hot, int64_t* n_ref, const int64_t* d_row_ptr_sym) {
     // hot rows = the K = budget / row_bytes rows of largest in-degree (exact threshold: the K-th
     // largest in-degree, from a radix sort of the in-degrees; ties at the threshold are kept
     // unless they overshoot the budget by more than a quarter)
@@ -575,8 +592,12 @@ Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_
     CL_TRY(indeg.alloc(N, s, "in-degree"));
     CL_TRY(sorted.alloc(N, s, "sorted in-degree"));
     CL_TRY(cnt.alloc(3, s, "hot count"));
-    CL_CUDA_TRY(cudaMemsetAsync(indeg.p, 0, (size_t)N * 4, s));
-    k_indegree<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p);
+    if (d_row_ptr_sym) {                       // no atomics (c5: 36 ms of contended hub counters)
+        k_row_lengths<<<grid_for(N, 4), kThreads, 0, s>>>(d_row_ptr_sym, N, indeg.p);
+    } else {
+        CL_CUDA_TRY(cudaMemsetAsync(indeg.p, 0, (size_t)N * 4, s));
+        k_indegree<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p);
+    }
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     {

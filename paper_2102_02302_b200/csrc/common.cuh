@@ -152,7 +152,8 @@ Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s
 // *n_hot (0 => no row is tagged).  Every reader of col masks bit 31.
 constexpr int32_t kColMask = 0x7fffffff;
 Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes,
-               cudaStream_t s, int64_t* n_hot, int64_t* n_ref /* rows with in-degree > 0, or NULL */);
+               cudaStream_t s, int64_t* n_hot, int64_t* n_ref /* rows with in-degree > 0, or NULL */,
+               const int64_t* d_row_ptr_sym /* undirected graphs: in-degree = row length, else NULL */);
 
 // chunks.cu: out = sum_q w_qv Tq[q] (Algorithm 1 lines 10-12); d_Tq / d_occ are device arrays
 // of Q device pointers; out and every Tq[q] are N x dp
