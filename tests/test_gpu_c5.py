@@ -104,8 +104,10 @@ def test_c5_full_size_sampled(cl):
                     assert err <= TOL_ABS, f"iteration {i} row {r}: max|d| {err:.3e}"
                     assert cos >= TOL_COS, f"iteration {i} row {r}: cos {cos:.9f}"
                     worst = max(worst, err)
-            # unit norms (or exact zeros) on every row, in chunks
-            for r0 in range(0, n, 1 << 20):
+            # unit norms (or exact zeros) on every row, in chunks (every row after the last step; a
+            # strided quarter of the rows after the others, to keep the test within minutes)
+            step = 1 if i == iters else 4
+            for r0 in range(0, n, step << 20):
                 nr = np.linalg.norm(T[r0:r0 + (1 << 20)].astype(np.float64), axis=1)
                 ok = (nr == 0) | (np.abs(nr - 1) <= 1e-5)
                 assert ok.all(), f"iteration {i}: row {r0 + int(np.flatnonzero(~ok)[0])} norm"
