@@ -285,3 +285,44 @@ def test_fetch_async_overlaps_and_is_ordered(cl):
     G2.close()                                        # destroy waits for the copy
     assert part.cpu().numpy().tobytes() == ref4[50:150].tobytes()
     G.close()
+
+
+def _degenerate_graphs():
+    rng = np.random.default_rng(11)
+    out = []
+    n = 50                                                # every edge a self-loop
+    out.append(gen.EdgeList("self_loops", n, np.arange(n, dtype=np.int32), np.arange(n, dtype=np.int32), None, False))
+    # one edge listed 10,000 times with weights: a single merged entry per direction (reading B2)
+    out.append(gen.EdgeList("dup10k", 3, np.zeros(10000, np.int32), np.ones(10000, np.int32),
+                            rng.lognormal(0, 2, 10000).astype(np.float32), False))
+    # in-star: 100,000 leaves point at node 0 (directed): node 0's column is gathered by every leaf,
+    # node 0's own row is empty (a sink); plus the out-star from node 1 (a 100,000-entry heavy row)
+    leaves = np.arange(2, 100002, dtype=np.int32)
+    out.append(gen.EdgeList("stars", 100002, np.concatenate([leaves, np.ones(100000, np.int32)]),
+                            np.concatenate([np.zeros(100000, np.int32), leaves]), None, True))
+    out.append(gen.EdgeList("chain", 5000, np.arange(4999, dtype=np.int32), np.arange(1, 5000, dtype=np.int32),
+                            None, False))
+    out.append(gen.EdgeList("one_node", 1, np.zeros(1, np.int32), np.zeros(1, np.int32), None, True))
+    a, b = np.meshgrid(np.arange(50), np.arange(50, 100))
+    out.append(gen.EdgeList("K50_50", 100, a.ravel().astype(np.int32), b.ravel().astype(np.int32), None, False))
+    return out
+
+
+@pytest.mark.parametrize("d", [1, 7, 128, 1024])
+def test_degenerate_graphs(cl, d):
+    for g in _degenerate_graphs():
+        run_case(cl, g, d, iters=4)
+
+
+def test_c2_repeatable_bitwise(cl):
+    """Two runs of the bench workload give the same bytes (no floating-point atomics anywhere; heavy
+    rows are combined in part order whichever CTA finishes last)."""
+    g = gen.config("c2")
+    outs = []
+    for _ in range(2):
+        G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0)
+        cl.cleora_init(G, g.d, 0)
+        cl.cleora_iterate(G, g.iters)
+        outs.append(cl.cleora_fetch(G))
+        G.close()
+    assert outs[0].tobytes() == outs[1].tobytes()
