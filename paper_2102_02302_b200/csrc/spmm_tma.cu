@@ -1,22 +1,24 @@
-// spmm_tma.cu -- one Cleora iteration T_out = normalize_rows(M . T_in) with TMA bulk gathers.
+// spmm_tma.cu -- one Cleora iteration T_out = normalize_rows(M . T_in), gathering neighbour rows
+// through a shared-memory ring.
 //
-// Algorithm 1 lines 6-7.  Same schedule and arithmetic as spmm_norm.cu (which
-// remains the path for d > 1024), but the neighbour rows are not loaded through registers:
-// each warp owns a ring of S shared-memory slots, one row of T_in (dp*4 bytes) per slot, filled
-// by 1-D TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx) that lane 0 issues S entries
-// ahead of the consumer.  Bytes in flight are therefore bounded by shared memory (~190 KB per
-// SM) instead of the register file, which is what a latency-bound gather needs; registers only
-// hold the fp32 accumulator (dp/32 floats per lane).
+// Algorithm 1 lines 6-7.  Same schedule and arithmetic as spmm_norm.cu (the path
+// for rows <= 512 B and > 4 KB), but the neighbour rows are not loaded through registers: each warp
+// owns a ring of S shared-memory slots, one row of T_in (dp*4 bytes) per slot, filled S entries
+// ahead of the consumer either by 1-D TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx,
+// issued by lane 0; 4 KB rows) or by per-lane 16-byte cp.async (0.5-4 KB rows, where the bulk-copy
+// engine's issue rate binds; see gather_mode).  Bytes in flight are therefore bounded by shared
+// memory (~190 KB per SM) instead of the register file, which is what a latency-bound gather
+// needs; registers only hold the fp32 accumulator (dp/32 floats per lane).
 //
 // Light rows (<= heavy_thresh entries): a warp takes a ticket for a light chunk (<= 31 consecutive
-// rows, entry-bounded, see Schedule) and
-// streams their entries flat through its ring -- the pipeline keeps running across row
-// boundaries, where the finished row is reduced (fp64 sum of squares, warp shuffles), scaled
-// and written with 16-byte streaming stores.  Heavy rows: CTA work items; each warp streams a
-// contiguous sub-range, the 8 partial vectors are combined through shared memory in warp order,
-// and multi-item rows finish in the last CTA (atomic ticket) with an fp64 sum in part order.
-// Each row accumulates its entries in ascending order from 0, exactly as spmm_norm.cu does, so
-// both kernels produce bitwise identical results.
+// rows, entry-bounded, see Schedule) and streams their entries flat through its ring -- the
+// pipeline keeps running across row boundaries, where the finished row is reduced (fp64 sum of
+// squares, warp shuffles), scaled and written with 16-byte streaming stores (and, multi-GPU, into
+// every peer replica).  Heavy rows: CTA work items; each warp streams a contiguous sub-range, the 8
+// partial vectors are combined through shared memory in warp order, and multi-item rows finish in
+// the last CTA (atomic ticket) with an fp64 sum in part order.  Each row accumulates its entries
+// in ascending order from 0, exactly as spmm_norm.cu does, so every engine produces bitwise
+// identical results (tested).
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
