@@ -5,6 +5,7 @@
 // spmm_norm.cu); the Python binding only marshals arguments.  There is no CPU fallback.
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <array>
@@ -21,6 +22,12 @@
 #include "common.cuh"
 
 namespace cleora {
+
+// NVTX range around every C-ABI call (header-only NVTX 3: free unless a profiler is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 static thread_local std::string g_err;
 void set_error(const std::string& m) { g_err = m; }
@@ -775,6 +782,7 @@ int cleora_release_cached_memory(void) {
 
 int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, int64_t n_edges, int32_t n_nodes,
                  int32_t directed, const cleora_opts* opts, cleora_graph** out) {
+    NvtxRange _nvtx("cleora_build");
     if (!out) return usage("cleora_build: out is NULL");
     *out = nullptr;
     if (!src || !dst) return usage("cleora_build: src/dst is NULL");
@@ -805,6 +813,7 @@ int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, in
 int cleora_expand(const int64_t* he_ptr, const int32_t* he_nodes, const float* he_weight, int64_t n_hyperedges,
                   int32_t n_nodes, int32_t mode, int32_t device, int32_t on_device, void* stream, int32_t* out_src,
                   int32_t* out_dst, float* out_weight, int64_t capacity, int64_t* n_out) {
+    NvtxRange _nvtx("cleora_expand");
     if (!he_ptr || !he_nodes || !n_out) return usage("cleora_expand: NULL argument");
     if (n_hyperedges < 1 || n_nodes < 1) return usage("cleora_expand: n_hyperedges and n_nodes must be >= 1");
     if (mode != CLEORA_EXPAND_CLIQUE && mode != CLEORA_EXPAND_STAR) return usage("cleora_expand: unknown mode");
@@ -889,6 +898,7 @@ int cleora_expand(const int64_t* he_ptr, const int32_t* he_nodes, const float* h
 int cleora_build_batch(const int32_t* src, const int32_t* dst, const float* weight, const int64_t* edge_ptr,
                        const int32_t* node_count, int32_t n_graphs, int32_t directed, const cleora_opts* opts,
                        cleora_graph** out) {
+    NvtxRange _nvtx("cleora_build_batch");
     if (!out) return usage("cleora_build_batch: out is NULL");
     *out = nullptr;
     if (!src || !dst || !edge_ptr || !node_count) return usage("cleora_build_batch: NULL argument");
@@ -918,6 +928,7 @@ int cleora_build_batch(const int32_t* src, const int32_t* dst, const float* weig
 }
 
 int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
+    NvtxRange _nvtx("cleora_init");
     if (!g) return usage("cleora_init: graph is NULL");
     if (d < 1 || d > CLEORA_MAX_D) return usage("cleora_init: d must be in [1, CLEORA_MAX_D]");
     DeviceGuard guard(g->device);
@@ -1008,6 +1019,7 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
 }
 
 int cleora_iterate(cleora_graph* g, int32_t k) {
+    NvtxRange _nvtx("cleora_iterate");
     if (!g) return usage("cleora_iterate: graph is NULL");
     if (k < 0) return usage("cleora_iterate: k must be >= 0");
     if (!g->T[0]) return usage("cleora_iterate: call cleora_init first");
@@ -1086,6 +1098,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
 }
 
 int cleora_fetch(const cleora_graph* g, int64_t row_begin, int64_t row_end, float* out, int32_t out_on_device) {
+    NvtxRange _nvtx("cleora_fetch");
     if (!g || !out) return usage("cleora_fetch: NULL argument");
     if (!g->T[0]) return usage("cleora_fetch: call cleora_init first");
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_fetch: rows outside [0, N]");
@@ -1105,6 +1118,7 @@ int cleora_fetch(const cleora_graph* g, int64_t row_begin, int64_t row_end, floa
 }
 
 int cleora_fetch_async(cleora_graph* g, int64_t row_begin, int64_t row_end, float* out, int32_t out_on_device) {
+    NvtxRange _nvtx("cleora_fetch_async");
     if (!g || !out) return usage("cleora_fetch_async: NULL argument");
     if (!g->T[0]) return usage("cleora_fetch_async: call cleora_init first");
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_fetch_async: rows outside [0, N]");
@@ -1136,6 +1150,7 @@ int cleora_fetch_async(cleora_graph* g, int64_t row_begin, int64_t row_end, floa
 }
 
 int cleora_merge_chunks(cleora_graph* const* chunks, int32_t n_chunks, float* out, int32_t out_on_device) {
+    NvtxRange _nvtx("cleora_merge_chunks");
     if (!chunks || !out) return usage("cleora_merge_chunks: NULL argument");
     if (n_chunks < 1) return usage("cleora_merge_chunks: n_chunks must be >= 1");
     const cleora_graph* g0 = chunks[0];
@@ -1190,6 +1205,7 @@ int cleora_merge_chunks(cleora_graph* const* chunks, int32_t n_chunks, float* ou
 
 int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int32_t* known_idx, const float* weight,
                        int64_t n_edges, int32_t n_new, int32_t inputs_on_device, float* out, int32_t out_on_device) {
+    NvtxRange _nvtx("cleora_reconstruct");
     if (!g || !new_idx || !known_idx || !out) return usage("cleora_reconstruct: NULL argument");
     if (!g->T[0]) return usage("cleora_reconstruct: call cleora_init first");
     if (n_new < 1) return usage("cleora_reconstruct: n_new must be >= 1");
@@ -1287,6 +1303,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
 }
 
 int cleora_fetch_replica(const cleora_graph* g, int32_t rank, int64_t row_begin, int64_t row_end, float* host_out) {
+    NvtxRange _nvtx("cleora_fetch_replica");
     if (!g || !host_out) return usage("cleora_fetch_replica: NULL argument");
     if (!g->T[0]) return usage("cleora_fetch_replica: call cleora_init first");
     if (g->xmode != X_LOOPBACK) {
@@ -1307,6 +1324,7 @@ int cleora_fetch_replica(const cleora_graph* g, int32_t rank, int64_t row_begin,
 }
 
 int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const float* host_in) {
+    NvtxRange _nvtx("cleora_set_rows");
     if (!g || !host_in) return usage("cleora_set_rows: NULL argument");
     if (!g->T[0]) return usage("cleora_set_rows: call cleora_init first");
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_set_rows: rows outside [0, N]");
@@ -1329,6 +1347,7 @@ int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const f
 }
 
 int cleora_fetch_csr(const cleora_graph* g, int64_t* row_ptr, int32_t* col, float* val, double* deg) {
+    NvtxRange _nvtx("cleora_fetch_csr");
     if (!g) return usage("cleora_fetch_csr: graph is NULL");
     DeviceGuard guard(g->device);
     cudaError_t e = cudaSuccess;

@@ -326,3 +326,23 @@ def test_c2_repeatable_bitwise(cl):
         outs.append(cl.cleora_fetch(G))
         G.close()
     assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_cached_memory_release_and_reuse(cl):
+    """Blocks freed by destroy are reused by the next handle of the same shape; releasing the cache
+    returns them to the driver and everything still works afterwards."""
+    import torch
+    g = gen.config("c1")
+    ref = None
+    for release in (False, True, False):
+        G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0)
+        cl.cleora_init(G, 256, 0)
+        cl.cleora_iterate(G, 2)
+        T = cl.cleora_fetch(G)
+        G.close()
+        ref = T if ref is None else ref
+        assert T.tobytes() == ref.tobytes()
+        if release:
+            free_before = torch.cuda.mem_get_info()[0]
+            cl.cleora_release_cached_memory()
+            assert torch.cuda.mem_get_info()[0] >= free_before
