@@ -101,3 +101,59 @@ def test_zero_rows_not_rewritten_same_bytes(cl, monkeypatch):
         R = oracle.step(M, R)
     assert float(np.abs(outs[0].astype(np.float64) - R).max()) <= 1e-5
     assert np.array_equal(~outs[0].any(1), ~R.any(1))
+
+
+def _nccl_worker(rank, world, port, exchange_nccl, q):
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    import gen as gen_
+    import paper_2102_02302_b200 as cl_
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        obj = [cl_.cleora_nccl_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        g = gen_.chung_lu(20000, 60000, 2.1, 9.5388, 233115.5 * 20000 / 1134890, seed=2)
+        G = cl_.cleora_build(g.src, g.dst, None, g.n, False, device=rank, rank=rank, world=world, nccl_id=obj[0],
+                             exchange_nccl=exchange_nccl)
+        cl_.cleora_init(G, 256, 0)
+        cl_.cleora_iterate(G, 3)
+        T = cl_.cleora_fetch(G)
+        mode = cl_.cleora_info(G)["exchange"]
+        G.close()
+        q.put((rank, mode, T.tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("exchange_nccl", [False, True])
+def test_real_multi_gpu_if_available(cl, exchange_nccl):
+    """On a box with >= 2 GPUs: torchrun-style ranks over NCCL, the fused peer-store exchange (or
+    the NCCL all-gather fallback); every rank's replica is bitwise the 1-GPU result."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    world = min(4, torch.cuda.device_count())
+    if world < 2:
+        pytest.skip("needs >= 2 GPUs (this pool has one; covered by the loopback tests above)")
+    g = gen.chung_lu(20000, 60000, 2.1, 9.5388, 233115.5 * 20000 / 1134890, seed=2)
+    ref, _ = _run(cl, g, 256, 3)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, world, port, exchange_nccl, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, mode, T in res:
+        assert mode == 1 if exchange_nccl else mode in (1, 2)      # 2: peer stores, 1: NCCL (fallback)
+        assert T == ref.tobytes(), f"rank {rank} (exchange mode {mode}) differs from 1 GPU"
