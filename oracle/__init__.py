@@ -18,7 +18,9 @@ What each function computes, with the paper passage it follows
   (Alg. 1 lines 6-7).
 * :func:`embed` -- Algorithm 1 with Q = 1 chunk.
 * :func:`chunk_assign`, :func:`chunk_occurrences`, :func:`merge`, :func:`embed_chunked` --
-  Algorithm 1 with Q > 1 chunks (lines 1-2 and 10-12), readings R13/R14.
+  Algorithm 1 with Q > 1 chunks (lines 1-2 and 10-12), readings R13/R14.  The
+  exact edge-to-chunk assignment (R13) is **parity unpinned by the paper**, which gives no rule;
+  its properties (partition, determinism, uniformity) are pinned.
 * :func:`reconstruct` -- a new node's embedding as the normalised weighted average of its
   neighbours' rows (§3.2): one row of normalize(M T) over the
   new nodes' own transition rows.
