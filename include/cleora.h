@@ -256,7 +256,7 @@ typedef struct cleora_info_t {
     int32_t exchange;       /* 0 one GPU, 1 NCCL all-gather, 2 fused peer stores, 3 loopback */
     int32_t n_graphs;       /* graphs in a batched handle (cleora_build_batch), else 0   */
 } cleora_info_t;
-CLEORA_API int cleora_info(const cleora_graph* g, cleora_info_t* out);
+CLEORA_API int cleora_info(cleora_graph* g, cleora_info_t* out);
 
 /* Device-time statistics (requires CLEORA_F_TIMING; otherwise counts stay 0). */
 typedef struct cleora_stats_t {

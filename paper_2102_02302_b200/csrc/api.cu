@@ -340,7 +340,8 @@ struct cleora_graph {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int32_t n = 0;
-    int64_t nnz = 0, n_edges_in = 0, zero_rows = 0, max_degree = 0;
+    int64_t nnz = 0, n_edges_in = 0, zero_rows = -1, max_degree = -1;   // -1: not read back yet
+    unsigned long long* d_scal = nullptr;   // the build's device scalars ([2] zero rows, [3] max degree)
     int directed = 0;
     int64_t* row_ptr = nullptr;
     int32_t* col = nullptr;
@@ -355,7 +356,7 @@ struct cleora_graph {
     // cleora_fetch_async: D2H on a copy stream, concurrent with later work on `stream`
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_copied = nullptr;
-    bool copy_pending = false;
+    mutable bool copy_pending = false;
     int32_t* occ = nullptr;         // chunked builds: endpoint occurrences per node (reading R14)
     int32_t n_graphs = 0;           // batched handles (cleora_build_batch): graphs in the batch
     int64_t* d_base = nullptr;      //   [n_graphs + 1] first row of every graph (device)
@@ -505,8 +506,8 @@ Status make_schedules(cleora_graph* g) {
     return Status::ok();
 }
 
-// An asynchronous fetch may still be reading T: stream-order the next write of T after it.
-void order_after_copy(cleora_graph* g) {
+// An asynchronous fetch may still be reading T: stream-order the next use of T after it.
+void order_after_side(const cleora_graph* g) {
     if (g->copy_pending) {
         cudaStreamWaitEvent(g->stream, g->ev_copied, 0);
         g->copy_pending = false;
@@ -731,8 +732,7 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
     g->col = b.col;
     g->val = b.val;
     g->deg = b.deg;
-    g->zero_rows = b.zero_rows;
-    g->max_degree = b.max_degree;
+    g->d_scal = b.d_scal;
     g->bytes = (int64_t)(N + 1) * 8 + b.nnz * 8 + (int64_t)N * 8;
 
     g->cuts.assign(g->world + 1, 0);
@@ -761,7 +761,8 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
         memcpy(id.internal, o->nccl_id, NCCL_UNIQUE_ID_BYTES);
         CL_NCCL_TRY(nc.CommInitRank(&g->comm, g->world, id, g->rank));
     }
-    CL_CUDA_TRY(cudaStreamSynchronize(g->stream));
+    // no final synchronisation: the CSR's last kernels run on while the caller goes on to
+    // cleora_init (stream order keeps everything that reads them behind them)
     return Status::ok();
 }
 
@@ -932,7 +933,7 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     if (!g) return usage("cleora_init: graph is NULL");
     if (d < 1 || d > CLEORA_MAX_D) return usage("cleora_init: d must be in [1, CLEORA_MAX_D]");
     DeviceGuard guard(g->device);
-    order_after_copy(g);
+    order_after_side(g);
     const int32_t dp = (d + 3) / 4 * 4;
     if (dp != g->dp || !g->T[0]) {
         free_T(g);
@@ -970,6 +971,17 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     g->cur = 0;
     g->iters = 0;
     g->zclean[0] = g->zclean[1] = false;
+    // a9: T_0
+    {
+        Status s = launch_hash_init(g->T[0], g->n, d, dp, seed, g->stream, g->d_base, g->n_graphs);
+        if (!s.good()) return fail(s);
+        if (g->xmode == X_LOOPBACK)   // every emulated rank initialises its own replica
+            for (int p = 0; p < g->world; p++)
+                if (p != g->rank) {
+                    s = launch_hash_init(g->rep[p][0], g->n, d, dp, seed, g->stream, g->d_base, g->n_graphs);
+                    if (!s.good()) return fail(s);
+                }
+    }
     // heavy rows: > 64 entries with TMA bulk gathers, > 256 with cp.async / LDG gathers (measured:
     // c2 12.68 vs 12.80 ms per step with 64 / 256; c5 427 -> 375 ms, c4@256 8.10 -> 7.27 ms with 256);
     // every sequential fp32 run stays <= 256 terms (256-entry blocks keep the error ~3e-7)
@@ -1001,18 +1013,10 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
         }
         g->tag_dp = dp;
     }
-    Status s = launch_hash_init(g->T[0], g->n, d, dp, seed, g->stream, g->d_base, g->n_graphs);
-    if (!s.good()) return fail(s);
-    if (g->xmode == X_LOOPBACK)   // every emulated rank initialises its own replica
-        for (int p = 0; p < g->world; p++)
-            if (p != g->rank) {
-                s = launch_hash_init(g->rep[p][0], g->n, d, dp, seed, g->stream, g->d_base, g->n_graphs);
-                if (!s.good()) return fail(s);
-            }
     if (g->xmode == X_PEER) {
         // no rank may store into another's replicas before that rank is done with its
         // previous steps and has re-initialised
-        s = rank_barrier(g);
+        Status s = rank_barrier(g);
         if (!s.good()) return fail(s);
     }
     return CLEORA_OK;
@@ -1024,7 +1028,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
     if (k < 0) return usage("cleora_iterate: k must be >= 0");
     if (!g->T[0]) return usage("cleora_iterate: call cleora_init first");
     DeviceGuard guard(g->device);
-    order_after_copy(g);
+    order_after_side(g);
     const int nsh = g->xmode == X_LOOPBACK ? g->world : 1;
     for (int32_t i = 0; i < k; i++) {
         const int in = g->cur, out = 1 - g->cur;
@@ -1104,6 +1108,7 @@ int cleora_fetch(const cleora_graph* g, int64_t row_begin, int64_t row_end, floa
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_fetch: rows outside [0, N]");
     if (row_end == row_begin) return CLEORA_OK;
     DeviceGuard guard(g->device);
+    order_after_side(g);
     const float* src = g->T[g->cur] + row_begin * (int64_t)g->dp;
     const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     cudaError_t e;
@@ -1132,6 +1137,7 @@ int cleora_fetch_async(cleora_graph* g, int64_t row_begin, int64_t row_end, floa
         if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_fetch_async: ") + cudaGetErrorString(e)));
     }
     // the copy starts when the work enqueued so far on the handle's stream is done
+    order_after_side(g);
     e = cudaEventRecord(g->ev_ready, g->stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(g->copy_stream, g->ev_ready, 0);
     const float* src = g->T[g->cur] + row_begin * (int64_t)g->dp;
@@ -1165,6 +1171,7 @@ int cleora_merge_chunks(cleora_graph* const* chunks, int32_t n_chunks, float* ou
     }
     DeviceGuard guard(g0->device);
     cudaStream_t s = g0->stream;
+    for (int q = 0; q < n_chunks; q++) order_after_side(chunks[q]);
     for (int q = 1; q < n_chunks; q++)
         if (chunks[q]->stream != s) {
             cudaError_t e = cudaStreamSynchronize(chunks[q]->stream);
@@ -1211,6 +1218,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
     if (n_new < 1) return usage("cleora_reconstruct: n_new must be >= 1");
     if (n_edges < 1) return usage("cleora_reconstruct: n_edges must be >= 1");
     DeviceGuard guard(g->device);
+    order_after_side(g);
     cudaStream_t s = g->stream;
     const int32_t N2 = std::max(n_new, g->n);   // row space of the new nodes' transition rows
     void *bs = nullptr, *bd = nullptr, *bw = nullptr;
@@ -1295,6 +1303,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
     dfree(b.col, s);
     dfree(b.val, s);
     dfree(b.deg, s);
+    dfree(b.d_scal, s);
     dfree(bs, s);
     dfree(bd, s);
     dfree(bw, s);
@@ -1314,6 +1323,7 @@ int cleora_fetch_replica(const cleora_graph* g, int32_t rank, int64_t row_begin,
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_fetch_replica: rows outside [0, N]");
     if (row_end == row_begin) return CLEORA_OK;
     DeviceGuard guard(g->device);
+    order_after_side(g);
     const float* src = g->rep[rank][g->cur] + row_begin * (int64_t)g->dp;
     cudaError_t e = cudaMemcpy2DAsync(host_out, (size_t)g->d * sizeof(float), src, (size_t)g->dp * sizeof(float),
                                       (size_t)g->d * sizeof(float), (size_t)(row_end - row_begin),
@@ -1330,7 +1340,7 @@ int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const f
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_set_rows: rows outside [0, N]");
     if (row_end == row_begin) return CLEORA_OK;
     DeviceGuard guard(g->device);
-    order_after_copy(g);
+    order_after_side(g);
     // loopback: every emulated rank sets the same rows in its own replica
     const int nrep = g->xmode == X_LOOPBACK ? g->world : 1;
     cudaError_t e = cudaSuccess;
@@ -1364,7 +1374,7 @@ int cleora_fetch_csr(const cleora_graph* g, int64_t* row_ptr, int32_t* col, floa
     return CLEORA_OK;
 }
 
-int cleora_info(const cleora_graph* g, cleora_info_t* o) {
+int cleora_info(cleora_graph* g, cleora_info_t* o) {
     if (!g || !o) return usage("cleora_info: NULL argument");
     memset(o, 0, sizeof *o);
     o->n_nodes = g->n;
@@ -1373,6 +1383,14 @@ int cleora_info(const cleora_graph* g, cleora_info_t* o) {
     o->d = g->d;
     o->d_stride = g->dp;
     o->iterations = g->iters;
+    if (g->zero_rows < 0 && g->d_scal) {
+        DeviceGuard g0(g->device);
+        unsigned long long f[2] = {0, 0};
+        Status s = read_small(f, g->d_scal + 2, sizeof f, g->stream);
+        if (!s.good()) return fail(s);
+        g->zero_rows = (int64_t)f[0];
+        g->max_degree = (int64_t)f[1];
+    }
     o->zero_rows = g->zero_rows;
     o->max_degree = g->max_degree;
     o->heavy_rows = g->sched.n_heavy_rows;
@@ -1434,6 +1452,7 @@ void cleora_destroy(cleora_graph* g) {
         dfree(g->deg, g->stream);
         free_schedules(g);
         dfree(g->d_flag, g->stream);
+        dfree(g->d_scal, g->stream);
         dfree(g->occ, g->stream);
         dfree(g->d_base, g->stream);
         cudaStreamSynchronize(g->stream);

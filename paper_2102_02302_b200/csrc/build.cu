@@ -429,12 +429,8 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     k_values<<<grid_for(nnz, 4), kThreads, 0, s>>>(rows.p, e_ab.p, deg.p, nnz, val.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
-    unsigned long long h_zm[2];
-    CL_TRY(read_small(h_zm, scal.p + 2, 2 * sizeof(unsigned long long), s));
-
     out->nnz = nnz;
-    out->zero_rows = (int64_t)h_zm[0];
-    out->max_degree = (int64_t)h_zm[1];
+    out->d_scal = scal.release();
     out->row_ptr = row_ptr.release();
     out->col = col.release();
     out->val = val.release();

@@ -114,7 +114,9 @@ struct BuildOut {
     int32_t* col = nullptr;
     float* val = nullptr;
     double* deg = nullptr;
-    int64_t zero_rows = 0, max_degree = 0;
+    // device scalars of the build ([2] rows without entries, [3] largest row), left on the device so
+    // that the build needs no host round trip after its last kernel; the caller frees the buffer
+    unsigned long long* d_scal = nullptr;
 };
 // Optional parts of a build: keep only the edges of chunk `chunk` of `n_chunks` (Algorithm 1
 // line 1, reading R13), count every node's endpoint occurrences among the kept edges (reading
