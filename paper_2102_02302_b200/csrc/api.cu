@@ -382,6 +382,8 @@ struct cleora_graph {
     std::vector<Schedule> sched_p;
     int64_t max_items = 0;
     int sched_thresh = -1;          // heavy_thresh the current schedule(s) were built with
+    int chunk_rows = kChunkRows;    // light-chunk row cap for the current gather engine
+    int sched_rows = -1;            // chunk_rows the current schedule(s) were built with
     size_t partials_floats = 0;     // capacity of `partials`
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_spmm, ev_x;
@@ -485,6 +487,7 @@ void free_schedules(cleora_graph* g) {
     }
     g->max_items = 0;
     g->sched_thresh = -1;
+    g->sched_rows = -1;
 }
 
 // The schedule (heavy-row CTA items, light chunks) for this handle's rows -- for every emulated
@@ -493,16 +496,17 @@ Status make_schedules(cleora_graph* g) {
     free_schedules(g);
     if (!g->sched_p.empty()) {
         for (int p = 0; p < g->world; p++) {
-            CL_TRY(build_schedule(g->row_ptr, g->n, g->cuts[p], g->cuts[p + 1], g->heavy_thresh, g->stream,
-                                  &g->sched_p[p]));
+            CL_TRY(build_schedule(g->row_ptr, g->n, g->cuts[p], g->cuts[p + 1], g->heavy_thresh, g->chunk_rows,
+                                  g->stream, &g->sched_p[p]));
             g->max_items = std::max(g->max_items, g->sched_p[p].n_items);
         }
         g->sched = g->sched_p[g->rank];
     } else {
-        CL_TRY(build_schedule(g->row_ptr, g->n, g->r0, g->r1, g->heavy_thresh, g->stream, &g->sched));
+        CL_TRY(build_schedule(g->row_ptr, g->n, g->r0, g->r1, g->heavy_thresh, g->chunk_rows, g->stream, &g->sched));
         g->max_items = g->sched.n_items;
     }
     g->sched_thresh = g->heavy_thresh;
+    g->sched_rows = g->chunk_rows;
     return Status::ok();
 }
 
@@ -986,7 +990,11 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     // c2 12.68 vs 12.80 ms per step with 64 / 256; c5 427 -> 375 ms, c4@256 8.10 -> 7.27 ms with 256);
     // every sequential fp32 run stays <= 256 terms (256-entry blocks keep the error ~3e-7)
     g->heavy_thresh = heavy_thresh_default(gather_mode(dp) == kGatherBulk ? 64 : 256);
-    if (g->sched_thresh != g->heavy_thresh) {
+    // light chunks: <= 6 rows with TMA bulk gathers, <= 8 with cp.async, 31 with LDG (measured,
+    // c3 d=1024: 2.04 -> 1.42 ms per launch at 6 rows; c3 d=512 0.86 -> 0.79 ms at 8; the register
+    // kernel is fastest at 31: c3 d=256 0.545 ms vs 0.61 at 8, c4 d=256 6.56 vs 6.82)
+    g->chunk_rows = gather_mode(dp) == kGatherBulk ? 6 : gather_mode(dp) == kGatherAsync ? 8 : kChunkRows;
+    if (g->sched_thresh != g->heavy_thresh || g->sched_rows != g->chunk_rows) {
         Status s = make_schedules(g);
         if (!s.good()) return fail(s);
     }
@@ -1256,7 +1264,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
         if (st.good()) st = read_small(&tail[1], b.row_ptr + N2, sizeof(int64_t), s);
         if (st.good() && tail[1] != tail[0]) st = Status::make(3, "cleora_reconstruct: new_idx outside [0, n_new)");
     }
-    if (st.good()) st = build_schedule(b.row_ptr, N2, 0, n_new, g->heavy_thresh, s, &sc);
+    if (st.good()) st = build_schedule(b.row_ptr, N2, 0, n_new, g->heavy_thresh, g->chunk_rows, s, &sc);
     if (st.good()) st = dalloc((void**)&Tnew, (size_t)n_new * g->dp * sizeof(float), s, "reconstructed rows");
     if (st.good() && sc.n_items > 0)
         st = dalloc((void**)&parts, (size_t)sc.n_items * g->dp * sizeof(float), s, "reconstruct partials");

@@ -438,7 +438,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     return Status::ok();
 }
 
-Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int heavy_thresh,
+Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int heavy_thresh, int chunk_rows,
                       cudaStream_t s, Schedule* out) {
     (void)N;
     const int64_t nr = r1 - r0;
@@ -468,9 +468,15 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // at most `chunk_rows` (the caller's, per gather engine: fewer rows per chunk keep the rows
+        // in flight across the grid close to row order, so rows that share neighbours fetch them
+        // close together in time -- cf. DESIGN §7)
+        int64_t cap = chunk_rows;
+        if (const char* cr = getenv("CLEORA_CHUNK_ROWS")) cap = atoll(cr);   // measurement override
+        if (cap < 1 || cap > kChunkRows) cap = kChunkRows;
         int64_t rows = nr / ((int64_t)sms * 16 * 4);
         if (rows < 1) rows = 1;
-        if (rows > kChunkRows) rows = kChunkRows;
+        if (rows > cap) rows = cap;
         IsChunkStart pred{d_row_ptr, r0, win, rows};
         size_t tmp_bytes = 0;
         CL_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, it, starts.p, cnt1.p, nr, pred, s));

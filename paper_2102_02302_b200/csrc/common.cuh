@@ -145,7 +145,7 @@ struct Schedule {
     int64_t n_light = 0;
 };
 Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int heavy_thresh,
-                      cudaStream_t s, Schedule* out);
+                      int chunk_rows, cudaStream_t s, Schedule* out);
 Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts);
 
 // Hot-row tagging for L2 residency hints, in place: col[k] = (col[k] & 0x7fffffff) |
