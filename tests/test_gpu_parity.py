@@ -346,3 +346,25 @@ def test_cached_memory_release_and_reuse(cl):
             free_before = torch.cuda.mem_get_info()[0]
             cl.cleora_release_cached_memory()
             assert torch.cuda.mem_get_info()[0] >= free_before
+
+
+@pytest.mark.parametrize("mode,d", [("bulk", 1024), ("async", 512), ("ldg", 256), ("ldg", 100)])
+def test_light_chunk_rows_do_not_change_bytes(cl, mode, d, monkeypatch):
+    """Light rows are computed one at a time in entry order whatever the light-chunk length, so the
+    per-engine chunk-row caps (6 / 8 / 31) change only the processing order of rows, never
+    a value: 1-, 6- and 31-row chunks give bitwise the same T.  Graphs large enough (300k+ rows)
+    that the caps bind, a lattice (the row-order locality case) and a power law (heavy rows)."""
+    import torch
+    monkeypatch.setenv("CLEORA_GATHER", mode)
+    graphs = [gen.lattice(560, 0.3, 0.02, seed=5),
+              gen.chung_lu(320000, 900000, 2.1, 9.5388, 233115.5 * 320000 / 1134890, seed=6)]
+    for g in graphs:
+        outs = []
+        for rows in ("1", "6", "31"):
+            monkeypatch.setenv("CLEORA_CHUNK_ROWS", rows)
+            G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0)
+            cl.cleora_init(G, d, 0)
+            cl.cleora_iterate(G, 2)
+            outs.append(cl.cleora_fetch(G, out=torch.empty((g.n, d), dtype=torch.float32, device="cuda")))
+            G.close()
+        assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2]), f"{g.name} {mode} d={d}"
