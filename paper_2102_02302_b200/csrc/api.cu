@@ -48,8 +48,14 @@ void trace(const char* what, cudaStream_t s, bool sync) {
 
 // ---------------------------------------------------------------- small readbacks
 namespace {
-__global__ void k_read_small(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int n) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+struct SmallSegs {
+    const uint8_t* src[kMaxSmallReads];
+    int off[kMaxSmallReads], len[kMaxSmallReads];
+    int n;
+};
+__global__ void k_read_small(const SmallSegs sg, uint8_t* __restrict__ dst) {
+    for (int q = 0; q < sg.n; q++)
+        for (int i = threadIdx.x; i < sg.len[q]; i += blockDim.x) dst[sg.off[q] + i] = sg.src[q][i];
     __threadfence_system();
 }
 struct Mapped {
@@ -61,8 +67,25 @@ Mapped g_mapped[kMaxDevices];
 }  // namespace
 
 Status read_small(void* h_dst, const void* d_src, size_t bytes, cudaStream_t s) {
+    const SmallRead r{h_dst, d_src, bytes};
+    return read_small_n(&r, 1, s);
+}
+
+// Several small device ranges in one kernel and one stream synchronisation (each host round trip
+// leaves the GPU idle until the next launch: the build merges its readbacks with this).
+Status read_small_n(const SmallRead* r, int n, cudaStream_t s) {
+    if (n < 1 || n > kMaxSmallReads) return Status::make(4, "read_small: 1..kMaxSmallReads ranges");
+    SmallSegs sg{};
+    size_t bytes = 0;
+    for (int q = 0; q < n; q++) {
+        sg.src[q] = reinterpret_cast<const uint8_t*>(r[q].d_src);
+        sg.off[q] = (int)bytes;
+        sg.len[q] = (int)r[q].bytes;
+        bytes += (r[q].bytes + 7) / 8 * 8;
+        if (bytes > 4096) return Status::make(4, "read_small: more than 4096 bytes");
+    }
+    sg.n = n;
     if (bytes == 0) return Status::ok();
-    if (bytes > 4096) return Status::make(4, "read_small: more than 4096 bytes");
     int dev = 0;
     CL_CUDA_TRY(cudaGetDevice(&dev));
     if (dev >= kMaxDevices) return Status::make(4, "read_small: device ordinal beyond kMaxDevices");
@@ -72,11 +95,11 @@ Status read_small(void* h_dst, const void* d_src, size_t bytes, cudaStream_t s) 
         CL_CUDA_TRY(cudaHostAlloc((void**)&m.h, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
         CL_CUDA_TRY(cudaHostGetDevicePointer((void**)&m.d, m.h, 0));
     }
-    k_read_small<<<1, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(d_src), m.d, (int)bytes);
+    k_read_small<<<1, 256, 0, s>>>(sg, m.d);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     CL_CUDA_TRY(cudaStreamSynchronize(s));
-    memcpy(h_dst, m.h, bytes);
+    for (int q = 0; q < n; q++) memcpy(r[q].h_dst, m.h + sg.off[q], r[q].bytes);
     return Status::ok();
 }
 

@@ -233,6 +233,10 @@ struct IsChunkStart {
     }
 };
 
+__global__ void k_put_end(int64_t* __restrict__ starts, const int64_t* __restrict__ n, int64_t end) {
+    starts[*n] = end;
+}
+
 __global__ void k_items_per_row(const int64_t* __restrict__ rp, const int64_t* __restrict__ hrows, int64_t nh,
                                 int64_t per_item, int64_t* __restrict__ nit) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -330,18 +334,6 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
                                                           scal.p + 1, x.n_chunks, x.chunk, x.chunk_key, x.occ);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
-    unsigned long long h_scal[2];
-    int h_kind = 0;
-    CL_TRY(read_small(h_scal, scal.p, 2 * sizeof(unsigned long long), s));
-    CL_TRY(read_small(&h_kind, err_kind.p, sizeof(int), s));
-    if (h_kind) {
-        char buf[256];
-        snprintf(buf, sizeof buf, "cleora_build: edge %llu: %s", (unsigned long long)h_scal[0],
-                 (h_kind & 1) ? (x.dst_limit >= 0 ? "node id outside its range" : "node id outside [0, n_nodes)")
-                              : "weight not finite or <= 0");
-        return Status::make(3, buf);
-    }
-    const int64_t n_valid = n_ent - (int64_t)h_scal[1];
     trace("csr: validate+expand", s, false);
 
     // B1: stable radix sort by (src, dst) over the bits the keys use
@@ -364,6 +356,22 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         if (!keys_only && vb.Current() != pos.p) std::swap(pos.p, pos2.p);
     }
     dfree(keys2.release(), s);
+    // the validation verdict, read once the sort is enqueued (one host round trip for both; on
+    // invalid input the sort's work is simply discarded)
+    unsigned long long h_scal[2];
+    int h_kind = 0;
+    {
+        const SmallRead rd[2] = {{h_scal, scal.p, 2 * sizeof(unsigned long long)}, {&h_kind, err_kind.p, sizeof(int)}};
+        CL_TRY(read_small_n(rd, 2, s));
+    }
+    if (h_kind) {
+        char buf[256];
+        snprintf(buf, sizeof buf, "cleora_build: edge %llu: %s", (unsigned long long)h_scal[0],
+                 (h_kind & 1) ? (x.dst_limit >= 0 ? "node id outside its range" : "node id outside [0, n_nodes)")
+                              : "weight not finite or <= 0");
+        return Status::make(3, buf);
+    }
+    const int64_t n_valid = n_ent - (int64_t)h_scal[1];
     trace("csr: radix sort", s, true);
 
     // B2: run starts of equal keys, merged weights
@@ -453,12 +461,13 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         out->work = work.release();
     }
     if (nr <= 0) return Status::ok();
+    DevBuf<int64_t> cnt1;                 // number of light chunks
     {
         // light chunks (see Schedule); window from CLEORA_CHUNK_ENTRIES, default 1024 entries
         const char* e = getenv("CLEORA_CHUNK_ENTRIES");
         int64_t win = e ? atoll(e) : 1024;
         if (win < 1) win = 1;
-        DevBuf<int64_t> starts, cnt1;
+        DevBuf<int64_t> starts;
         CL_TRY(starts.alloc(nr + 1, s, "light chunk starts"));
         CL_TRY(cnt1.alloc(1, s, "scalars"));
         thrust::counting_iterator<int64_t> it(r0);
@@ -483,13 +492,9 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         DevBuf<uint8_t> tmp;
         CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
         CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, starts.p, cnt1.p, nr, pred, s));
-        count_launches(2);
-        int64_t nl = 0;
-        CL_TRY(read_small(&nl, cnt1.p, sizeof nl, s));
-        const int64_t end = r1;
-        CL_CUDA_TRY(cudaMemcpyAsync(starts.p + nl, &end, sizeof end, cudaMemcpyHostToDevice, s));
-        CL_CUDA_TRY(cudaStreamSynchronize(s));   // `end` lives on this stack frame
-        out->n_light = nl;
+        k_put_end<<<1, 1, 0, s>>>(starts.p, cnt1.p, r1);       // starts[n_light] = r1
+        CL_CUDA_TRY(cudaGetLastError());
+        count_launches(3);
         out->light_start = starts.release();
     }
     DevBuf<int64_t> hrows, cnt;
@@ -505,8 +510,12 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, hrows.p, cnt.p, nr, pred, s));
         count_launches(2);
     }
-    int64_t nh = 0;
-    CL_TRY(read_small(&nh, cnt.p, sizeof nh, s));
+    int64_t nl = 0, nh = 0;   // both counts in one host round trip
+    {
+        const SmallRead rd[2] = {{&nl, cnt1.p, sizeof nl}, {&nh, cnt.p, sizeof nh}};
+        CL_TRY(read_small_n(rd, 2, s));
+    }
+    out->n_light = nl;
     out->n_heavy_rows = nh;
     if (nh == 0) return Status::ok();
     const int64_t per_item = (int64_t)heavy_thresh * kWarpsPerCta;
@@ -525,8 +534,10 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         count_launches(2);
     }
     int64_t last[2];
-    CL_TRY(read_small(&last[0], first.p + nh - 1, sizeof(int64_t), s));
-    CL_TRY(read_small(&last[1], nit.p + nh - 1, sizeof(int64_t), s));
+    {
+        const SmallRead rd[2] = {{&last[0], first.p + nh - 1, sizeof(int64_t)}, {&last[1], nit.p + nh - 1, sizeof(int64_t)}};
+        CL_TRY(read_small_n(rd, 2, s));
+    }
     const int64_t n_items = last[0] + last[1];
     DevBuf<HeavyItem> items;
     DevBuf<unsigned> counters;
@@ -555,7 +566,10 @@ __global__ void k_indegree(const int32_t* __restrict__ col, int64_t nnz, int32_t
         atomicAdd(indeg + (col[k] & kColMask), 1);
 }
 // c[0] += #rows with indeg >= t, c[1] += #rows with indeg >= t + 1, c[2] += #rows with indeg > 0
-__global__ void k_count_ge(const int32_t* __restrict__ indeg, int32_t N, int32_t t, unsigned long long* __restrict__ c) {
+// t = max(2, *kth) (the K-th largest in-degree, read on the device), or INT32_MAX without one
+__global__ void k_count_ge(const int32_t* __restrict__ indeg, int32_t N, const int32_t* __restrict__ kth,
+                           unsigned long long* __restrict__ c) {
+    const int32_t t = kth ? max(*kth, 2) : INT32_MAX;
     unsigned long long a = 0, b = 0, z = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < N; v += stride) {
@@ -612,17 +626,22 @@ Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_
     }
     int64_t K = budget_bytes / (row_bytes > 0 ? row_bytes : 1);
     if (K > N) K = N;
-    int32_t t = INT32_MAX;
-    if (K > 0) {
-        CL_TRY(read_small(&t, sorted.p + (N - K), sizeof t, s));
-        if (t < 2) t = 2;                 // a row read once or never gains nothing from pinning
-    }
+    // threshold t = the K-th largest in-degree, at least 2 (a row read once or never gains nothing
+    // from pinning); counted on the device, then read back with the counts in one round trip
+    const int32_t* kth = K > 0 ? sorted.p + (N - K) : nullptr;
     CL_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, 3 * sizeof(unsigned long long), s));
-    k_count_ge<<<grid_for(N, 8), kThreads, 0, s>>>(indeg.p, N, t, cnt.p);
+    k_count_ge<<<grid_for(N, 8), kThreads, 0, s>>>(indeg.p, N, kth, cnt.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     unsigned long long c[3];
-    CL_TRY(read_small(c, cnt.p, sizeof c, s));
+    int32_t t = INT32_MAX;
+    if (kth) {
+        const SmallRead rd[2] = {{c, cnt.p, sizeof c}, {&t, kth, sizeof t}};
+        CL_TRY(read_small_n(rd, 2, s));
+        if (t < 2) t = 2;
+    } else {
+        CL_TRY(read_small(c, cnt.p, sizeof c, s));
+    }
     int64_t nh = (int64_t)c[0];           // rows with in-degree >= t
     if (t != INT32_MAX && nh > K + K / 4) {
         t += 1;

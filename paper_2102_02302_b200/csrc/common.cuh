@@ -37,6 +37,13 @@ struct Status {
 // stream.  A kernel stores them into mapped pinned memory, so the read never queues behind a large
 // device-to-host DMA on the copy engine (cleora_fetch_async of another handle).
 Status read_small(void* h_dst, const void* d_src, size_t bytes, cudaStream_t s);
+constexpr int kMaxSmallReads = 4;
+struct SmallRead {
+    void* h_dst;
+    const void* d_src;
+    size_t bytes;
+};
+Status read_small_n(const SmallRead* r, int n, cudaStream_t s);
 
 // Host-side phase trace (stderr) when CLEORA_TRACE is set; `sync` waits for the stream first.
 void trace(const char* what, cudaStream_t s, bool sync);
