@@ -35,7 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp,
+    extra = os.environ.get("CLEORA_NVCC_EXTRA", "").split()   # measurement builds (-D switches)
+    cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", tmp,
            *[os.path.join(CSRC, f) for f in SOURCES], "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

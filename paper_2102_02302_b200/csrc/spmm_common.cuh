@@ -21,6 +21,12 @@ __device__ __forceinline__ double sq4(const float4& y) {
     return (double)y.x * y.x + (double)y.y * y.y + (double)y.z * y.z + (double)y.w * y.w;
 }
 
+// 1 / ||y|| from the fp64 sum of squares (0 for the zero vector: reading RZ).  rsqrt in fp64
+// (within an ulp or two of 2^-53 relative, far below the fp32 output's 2^-24) instead of a
+// correctly rounded 1.0 / sqrt(): the IEEE division and square root were 6.6% of the register
+// kernel's instructions on short rows (ncu, f4 batch)
+__device__ __forceinline__ double inv_norm(double ss) { return ss > 0.0 ? rsqrt(ss) : 0.0; }
+
 __device__ __forceinline__ float4 scale4(const float4& y, double inv) {
     return make_float4((float)((double)y.x * inv), (float)((double)y.y * inv), (float)((double)y.z * inv),
                        (float)((double)y.w * inv));

@@ -69,9 +69,8 @@ __device__ __forceinline__ float ldcsr_f32(const float* p, uint64_t pol) {
 
 // acc[v] += sum_{k in [k0,k1)} val[k] * T_in[col[k]][cbase + 4*(lane + 32 v) .. +3], ascending k.
 template <int V>
-__device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, int64_t k0, int64_t k1, int cbase, int lane,
-                                                float4 (&acc)[V]) {
-    const Pol pol = make_pol(a);
+__device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, const Pol& pol, int64_t k0, int64_t k1, int cbase,
+                                                int lane, float4 (&acc)[V]) {
     constexpr int U = (16 / V > 8) ? 8 : 16 / V;  // neighbours per batch: U*V 16-byte loads in flight
     const int dp = a.dp;
     bool ok[V];
@@ -122,7 +121,7 @@ __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, int64_t k0, i
 }
 
 template <int V>
-__device__ void light_row(const SpmmArgs& a, int64_t row, int64_t k0, int64_t k1, int lane) {
+__device__ void light_row(const SpmmArgs& a, const Pol& pol, int64_t row, int64_t k0, int64_t k1, int lane) {
     constexpr int SW = 128 * V;                   // floats per column slice
     const int dp = a.dp;
     const int ns = (dp + SW - 1) / SW;
@@ -134,7 +133,7 @@ __device__ void light_row(const SpmmArgs& a, int64_t row, int64_t k0, int64_t k1
         const int cbase = sl * SW;
 #pragma unroll
         for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        accumulate_warp<V>(a, k0, k1, cbase, lane, acc);
+        accumulate_warp<V>(a, pol, k0, k1, cbase, lane, acc);
 #pragma unroll
         for (int v = 0; v < V; v++) {
             const int f = cbase / 4 + lane + 32 * v;
@@ -145,7 +144,7 @@ __device__ void light_row(const SpmmArgs& a, int64_t row, int64_t k0, int64_t k1
         }
     }
     ss = warp_sum(ss);
-    const double inv = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+    const double inv = inv_norm(ss);
     if (ns == 1) {
 #pragma unroll
         for (int v = 0; v < V; v++) {
@@ -158,7 +157,7 @@ __device__ void light_row(const SpmmArgs& a, int64_t row, int64_t k0, int64_t k1
 }
 
 template <int V>
-__device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* scratch, int* flag) {
+__device__ void heavy_item(const SpmmArgs& a, const Pol& pol, int64_t idx, float4* red, double* scratch, int* flag) {
     constexpr int SW = 128 * V;
     constexpr int Q = 32 * V;                     // float4 per slice
     const HeavyItem it = a.items[idx];
@@ -177,7 +176,7 @@ __device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* 
         float4 acc[V];
 #pragma unroll
         for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        accumulate_warp<V>(a, wk0, wk1, sl * SW, lane, acc);
+        accumulate_warp<V>(a, pol, wk0, wk1, sl * SW, lane, acc);
 #pragma unroll
         for (int v = 0; v < V; v++) red[warp * Q + lane + 32 * v] = acc[v];
         __syncthreads();
@@ -199,7 +198,7 @@ __device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* 
     }
     if (single) {
         const double tot = block_sum(ss, scratch);
-        const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+        const double inv = inv_norm(tot);
         if (ns == 1) {
             if (t < Q && t < nq) put_out4(a, it.row, t, scale4(y, inv));
         } else {
@@ -232,7 +231,7 @@ __device__ void heavy_item(const SpmmArgs& a, int64_t idx, float4* red, double* 
         ss2 += zx * zx + zy * zy + zz * zz + zw * zw;
     }
     const double tot = block_sum(ss2, scratch);
-    const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+    const double inv = inv_norm(tot);
     if (nq <= (int)blockDim.x) {
         if (t < nq)
             put_out4(a, it.row, t,
@@ -270,6 +269,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_n
     __shared__ int flag;
     __shared__ unsigned s_item;
     const int lane = threadIdx.x & 31;
+    const Pol pol = make_pol(a);                  // once per thread, not per row
     if (a.n_items > 0) {
         for (;;) {
             if (threadIdx.x == 0) s_item = atomicAdd(a.work + 0, 1u);
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_n
             const int64_t it = s_item;
             __syncthreads();
             if (it >= a.n_items) break;
-            heavy_item<V>(a, it, red, scratch, &flag);
+            heavy_item<V>(a, pol, it, red, scratch, &flag);
         }
     }
     const int64_t nchunks = a.n_light;
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_n
             const int64_t k0 = __shfl_sync(kFull, rpl, (int)(r - rb));
             const int64_t k1 = __shfl_sync(kFull, rpl, (int)(r - rb + 1));
             if (k1 - k0 > a.heavy_thresh) continue;
-            light_row<V>(a, r, k0, k1, lane);
+            light_row<V>(a, pol, r, k0, k1, lane);
         }
     }
     // peer stores (multi-GPU) are system-scope visible before this launch counts as done; the

@@ -173,7 +173,7 @@ __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, f
     for (int v = 0; v < V; v++)
         if (FULL || 4 * (lane + 32 * v) < dp) ss += sq4(acc[v]);
     ss = warp_sum(ss);
-    const double inv = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+    const double inv = inv_norm(ss);
 #pragma unroll
     for (int v = 0; v < V; v++) {
         const int f = lane + 32 * v;
@@ -294,7 +294,7 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
     }
     if (it.nparts == 1) {
         const double tot = block_sum(ss, scratch);
-        const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+        const double inv = inv_norm(tot);
         if (t < nq) put_out4(a, it.row, t, scale4(y, inv));
     } else {
         float4* part = reinterpret_cast<float4*>(a.partials + idx * (int64_t)dp);
@@ -317,7 +317,7 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
                 }
             }
             const double tot = block_sum(zx * zx + zy * zy + zz * zz + zw * zw, scratch);
-            const double inv = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+            const double inv = inv_norm(tot);
             if (t < nq)
                 put_out4(a, it.row, t,
                          make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
