@@ -26,6 +26,13 @@
 #include "common.cuh"
 #include "spmm_common.cuh"
 
+#ifndef CLEORA_V1_U
+#define CLEORA_V1_U 8          // rows of <= 512 B: neighbours per load batch
+#endif
+#ifndef CLEORA_V1_BLOCKS
+#define CLEORA_V1_BLOCKS 4     // rows of <= 512 B: resident CTAs per SM
+#endif
+
 namespace cleora {
 
 namespace {
@@ -36,8 +43,10 @@ struct Pol {
     uint64_t hot, cold, csr;
 };
 
+template <bool H>
 __device__ __forceinline__ Pol make_pol(const SpmmArgs& a) {
-    Pol p;
+    Pol p{0, 0, 0};
+    if (!H) return p;                              // no hot rows: loads without cache hints
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p.hot));
     if (a.cold_first)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p.cold));
@@ -67,11 +76,35 @@ __device__ __forceinline__ float ldcsr_f32(const float* p, uint64_t pol) {
     return x;
 }
 
+// H = false (no hot rows, so every gather would carry evict_normal): plain loads -- no 64-bit
+// policy registers live across the row loop (at V = 1 the 64-register budget of 4 CTAs per SM
+// spilled the row-loop state: ncu on the f4 batch counted ~54 local loads/stores per row)
+template <bool H, int V>
+__device__ __forceinline__ float4 gather4(const float4* p, int32_t ct, const Pol& pol) {
+    if (H) return ldg4_pol(p, ct < 0 ? pol.hot : pol.cold);
+    return __ldg(p);
+}
+template <bool H>
+__device__ __forceinline__ int32_t csr_i32(const int32_t* p, const Pol& pol) {
+    if (H) return ldcsr_i32(p, pol.csr);
+    int32_t x;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(x) : "l"(p));
+    return x;
+}
+template <bool H>
+__device__ __forceinline__ float csr_f32(const float* p, const Pol& pol) {
+    if (H) return ldcsr_f32(p, pol.csr);
+    float x;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(x) : "l"(p));
+    return x;
+}
+
 // acc[v] += sum_{k in [k0,k1)} val[k] * T_in[col[k]][cbase + 4*(lane + 32 v) .. +3], ascending k.
-template <int V>
+template <int V, bool H>
 __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, const Pol& pol, int64_t k0, int64_t k1, int cbase,
                                                 int lane, float4 (&acc)[V]) {
-    constexpr int U = (16 / V > 8) ? 8 : 16 / V;  // neighbours per batch: U*V 16-byte loads in flight
+    // neighbours per batch: U*V 16-byte loads in flight
+    constexpr int U = V == 1 ? CLEORA_V1_U : ((16 / V > 8) ? 8 : 16 / V);
     const int dp = a.dp;
     bool ok[V];
 #pragma unroll
@@ -86,8 +119,8 @@ __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, const Pol& po
                 mc = __ldg(a.col + kb + lane);              // bit 31: hot row
                 mw = __ldg(a.val + kb + lane);
             } else {
-                mc = ldcsr_i32(a.col + kb + lane, pol.csr);
-                mw = ldcsr_f32(a.val + kb + lane, pol.csr);
+                mc = csr_i32<H>(a.col + kb + lane, pol);
+                mw = csr_f32<H>(a.val + kb + lane, pol);
             }
         }
         int j = 0;
@@ -98,10 +131,10 @@ __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, const Pol& po
             for (int u = 0; u < U; u++) {
                 const int ct = __shfl_sync(kFull, mc, j + u);
                 w[u] = __shfl_sync(kFull, mw, j + u);
-                const uint64_t pl = ct < 0 ? pol.hot : pol.cold;
                 const float4* p = reinterpret_cast<const float4*>(tb + (int64_t)(ct & kColMask) * dp);
 #pragma unroll
-                for (int v = 0; v < V; v++) x[u][v] = ok[v] ? ldg4_pol(p + 32 * v, pl) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int v = 0; v < V; v++)
+                    x[u][v] = ok[v] ? gather4<H, V>(p + 32 * v, ct, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
             for (int u = 0; u < U; u++)
@@ -111,16 +144,15 @@ __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, const Pol& po
         for (; j < n; j++) {
             const int ct = __shfl_sync(kFull, mc, j);
             const float w = __shfl_sync(kFull, mw, j);
-            const uint64_t pl = ct < 0 ? pol.hot : pol.cold;
             const float4* p = reinterpret_cast<const float4*>(tb + (int64_t)(ct & kColMask) * dp);
 #pragma unroll
             for (int v = 0; v < V; v++)
-                if (ok[v]) fma4(acc[v], w, ldg4_pol(p + 32 * v, pl));
+                if (ok[v]) fma4(acc[v], w, gather4<H, V>(p + 32 * v, ct, pol));
         }
     }
 }
 
-template <int V>
+template <int V, bool H>
 __device__ void light_row(const SpmmArgs& a, const Pol& pol, int64_t row, int64_t k0, int64_t k1, int lane) {
     constexpr int SW = 128 * V;                   // floats per column slice
     const int dp = a.dp;
@@ -133,7 +165,7 @@ __device__ void light_row(const SpmmArgs& a, const Pol& pol, int64_t row, int64_
         const int cbase = sl * SW;
 #pragma unroll
         for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        accumulate_warp<V>(a, pol, k0, k1, cbase, lane, acc);
+        accumulate_warp<V, H>(a, pol, k0, k1, cbase, lane, acc);
 #pragma unroll
         for (int v = 0; v < V; v++) {
             const int f = cbase / 4 + lane + 32 * v;
@@ -156,7 +188,7 @@ __device__ void light_row(const SpmmArgs& a, const Pol& pol, int64_t row, int64_
     }
 }
 
-template <int V>
+template <int V, bool H>
 __device__ void heavy_item(const SpmmArgs& a, const Pol& pol, int64_t idx, float4* red, double* scratch, int* flag) {
     constexpr int SW = 128 * V;
     constexpr int Q = 32 * V;                     // float4 per slice
@@ -176,7 +208,7 @@ __device__ void heavy_item(const SpmmArgs& a, const Pol& pol, int64_t idx, float
         float4 acc[V];
 #pragma unroll
         for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        accumulate_warp<V>(a, pol, wk0, wk1, sl * SW, lane, acc);
+        accumulate_warp<V, H>(a, pol, wk0, wk1, sl * SW, lane, acc);
 #pragma unroll
         for (int v = 0; v < V; v++) red[warp * Q + lane + 32 * v] = acc[v];
         __syncthreads();
@@ -260,16 +292,16 @@ __device__ void heavy_item(const SpmmArgs& a, const Pol& pol, int64_t idx, float
 // rows of <= 512 bytes (V = 1) are latency-bound with one row at a time per warp: 4 CTAs (32 warps)
 // per SM at <= 64 registers; wider rows need the registers for their accumulators (2 CTAs)
 template <int V>
-constexpr int kNormMinBlocks = V == 1 ? 4 : 2;   // V = 2 at 3 CTAs spills: c5 357 -> 478 ms
+constexpr int kNormMinBlocks = V == 1 ? CLEORA_V1_BLOCKS : 2;   // V = 2 at 3 CTAs spills: c5 357 -> 478 ms
 
-template <int V>
+template <int V, bool H>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_norm(const SpmmArgs a) {
     extern __shared__ float4 red[];
     __shared__ double scratch[kWarpsPerCta];
     __shared__ int flag;
     __shared__ unsigned s_item;
     const int lane = threadIdx.x & 31;
-    const Pol pol = make_pol(a);                  // once per thread, not per row
+    const Pol pol = make_pol<H>(a);               // once per thread, not per row
     if (a.n_items > 0) {
         for (;;) {
             if (threadIdx.x == 0) s_item = atomicAdd(a.work + 0, 1u);
@@ -277,7 +309,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_n
             const int64_t it = s_item;
             __syncthreads();
             if (it >= a.n_items) break;
-            heavy_item<V>(a, pol, it, red, scratch, &flag);
+            heavy_item<V, H>(a, pol, it, red, scratch, &flag);
         }
     }
     const int64_t nchunks = a.n_light;
@@ -303,7 +335,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_n
             const int64_t k0 = __shfl_sync(kFull, rpl, (int)(r - rb));
             const int64_t k1 = __shfl_sync(kFull, rpl, (int)(r - rb + 1));
             if (k1 - k0 > a.heavy_thresh) continue;
-            light_row<V>(a, pol, r, k0, k1, lane);
+            light_row<V, H>(a, pol, r, k0, k1, lane);
         }
     }
     // peer stores (multi-GPU) are system-scope visible before this launch counts as done; the
@@ -320,8 +352,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_n
     }
 }
 
-template <int V>
-Status launch_v(const SpmmArgs& a, cudaStream_t s) {
+template <int V, bool H>
+Status launch_vh(const SpmmArgs& a, cudaStream_t s) {
     const size_t smem = (size_t)kWarpsPerCta * 32 * V * sizeof(float4);
     // per device: the smem attribute and the occupancy are per device
     static int bps[kMaxDevices], nsm[kMaxDevices];
@@ -333,10 +365,10 @@ Status launch_v(const SpmmArgs& a, cudaStream_t s) {
     {
         std::lock_guard<std::mutex> lk(mu);
         if (!bps[dev]) {
-            CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_norm<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_norm<V, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             CL_CUDA_TRY(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
             int b = 0;
-            CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmm_norm<V>, kWarpsPerCta * 32, smem));
+            CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmm_norm<V, H>, kWarpsPerCta * 32, smem));
             bps[dev] = b < 1 ? 1 : b;
         }
         blocks_per_sm = bps[dev];
@@ -344,10 +376,16 @@ Status launch_v(const SpmmArgs& a, cudaStream_t s) {
     }
     if (a.r1 <= a.r0 && a.n_items == 0) return Status::ok();
     const int grid = sms * blocks_per_sm;                // one persistent wave
-    k_spmm_norm<V><<<grid, kWarpsPerCta * 32, smem, s>>>(a);
+    k_spmm_norm<V, H><<<grid, kWarpsPerCta * 32, smem, s>>>(a);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     return Status::ok();
+}
+
+// cache hints only when there are hot rows (a.cold_first: hot_tag pinned some rows)
+template <int V>
+Status launch_v(const SpmmArgs& a, cudaStream_t s) {
+    return a.cold_first ? launch_vh<V, true>(a, s) : launch_vh<V, false>(a, s);
 }
 
 }  // namespace

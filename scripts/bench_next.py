@@ -136,20 +136,25 @@ for name, x, mode, d3 in (("c2_star", g, cl.EXPAND_STAR, 1024), ("c1_clique", ge
         b.synchronize()
         ts.append(a.elapsed_time(b))
     nn = n0 + (hp.numel() - 1 if mode == cl.EXPAND_STAR else 0)
-    a, b = ev(), ev()
-    a.record(s)
-    es, ed = cl.cleora_expand(hp, hn, n0, mode, stream=s.cuda_stream)
-    G3 = cl.cleora_build(es, ed, None, nn, False, device=0, stream=s.cuda_stream)
-    cl.cleora_init(G3, d3, 0)
-    cl.cleora_iterate(G3, 4)
-    b.record(s)
-    b.synchronize()
-    nnz3 = cl.cleora_info(G3)["nnz"]
-    G3.close()
+    pts = []
+    for _ in range(3):                  # the first run allocates the expanded graph's buffers
+        a, b = ev(), ev()
+        a.record(s)
+        es, ed = cl.cleora_expand(hp, hn, n0, mode, stream=s.cuda_stream)
+        G3 = cl.cleora_build(es, ed, None, nn, False, device=0, stream=s.cuda_stream)
+        cl.cleora_init(G3, d3, 0)
+        cl.cleora_iterate(G3, 4)
+        b.record(s)
+        b.synchronize()
+        pts.append(a.elapsed_time(b))
+        nnz3 = cl.cleora_info(G3)["nnz"]
+        G3.close()
+    print(f"f3 {name} pipeline ms per run: {pts}", file=sys.stderr)
     f3[name] = {"hyperedges": hp.numel() - 1, "members": int(hn.numel()), "expanded_edges": int(es.numel()),
                 "expanded_nodes": nn, "nnz": nnz3, "d": d3, "expand_ms": min(ts),
                 "expanded_edges_per_s": es.numel() / (min(ts) / 1e3),
-                "pipeline_ms": a.elapsed_time(b), "pipeline": "expand + build + init + 4 iterations"}
+                "pipeline_ms": min(pts[1:]), "pipeline_first_run_ms": pts[0],
+                "pipeline": "expand + build + init + 4 iterations (min of 2 runs after a first, allocating one)"}
 
 # ---------------------------------------------------------------- f4
 rng = np.random.default_rng(1)
