@@ -27,7 +27,7 @@
 #include "spmm_common.cuh"
 
 #ifndef CLEORA_V1_U
-#define CLEORA_V1_U 8          // rows of <= 512 B: neighbours per load batch
+#define CLEORA_V1_U 4          // rows of <= 512 B: neighbours per load batch (8 spilled at 64 regs)
 #endif
 #ifndef CLEORA_V1_BLOCKS
 #define CLEORA_V1_BLOCKS 4     // rows of <= 512 B: resident CTAs per SM
