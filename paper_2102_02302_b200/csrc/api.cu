@@ -1013,10 +1013,15 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     // c2 12.68 vs 12.80 ms per step with 64 / 256; c5 427 -> 375 ms, c4@256 8.10 -> 7.27 ms with 256);
     // every sequential fp32 run stays <= 256 terms (256-entry blocks keep the error ~3e-7)
     g->heavy_thresh = heavy_thresh_default(gather_mode(dp) == kGatherBulk ? 64 : 256);
-    // light chunks: <= 6 rows with TMA bulk gathers, <= 8 with cp.async, 31 with LDG (measured,
-    // c3 d=1024: 2.04 -> 1.42 ms per launch at 6 rows; c3 d=512 0.86 -> 0.79 ms at 8; the register
-    // kernel is fastest at 31: c3 d=256 0.545 ms vs 0.61 at 8, c4 d=256 6.56 vs 6.82)
-    g->chunk_rows = gather_mode(dp) == kGatherBulk ? 6 : gather_mode(dp) == kGatherAsync ? 8 : kChunkRows;
+    // light-chunk row cap per gather engine and row size (measured, scripts/chunk_sweep*.sh, min
+    // launch ms): TMA bulk (d = 1024) 6 rows, c3 2.04 -> 1.42 vs 31; cp.async at d = 512 12 rows, c3
+    // 0.86 -> 0.75; cp.async at d = 256 31 rows (c3 0.518 vs 0.581 at 8); LDG at d <= 128 16 rows,
+    // f4 1.39 -> 1.25, c3@128 0.508 -> 0.490, c4@128 4.296 -> 4.306
+    {
+        const int mode = gather_mode(dp);
+        g->chunk_rows = mode == kGatherBulk ? 6 : mode == kGatherAsync ? (dp > 256 ? 12 : kChunkRows)
+                                                                        : (dp <= 128 ? 16 : kChunkRows);
+    }
     if (g->sched_thresh != g->heavy_thresh || g->sched_rows != g->chunk_rows) {
         Status s = make_schedules(g);
         if (!s.good()) return fail(s);
