@@ -29,6 +29,9 @@
 #ifndef CLEORA_V1_U
 #define CLEORA_V1_U 4          // rows of <= 512 B: neighbours per load batch (8 spilled at 64 regs)
 #endif
+#ifndef CLEORA_V1_PAIR
+#define CLEORA_V1_PAIR 16      // rows of <= 512 B: two rows of <= this many entries per warp
+#endif
 #ifndef CLEORA_V1_BLOCKS
 #define CLEORA_V1_BLOCKS 4     // rows of <= 512 B: resident CTAs per SM
 #endif
@@ -188,6 +191,72 @@ __device__ void light_row(const SpmmArgs& a, const Pol& pol, int64_t row, int64_
     }
 }
 
+// Rows of <= 512 B (dp <= 128): two rows per warp, one per half-warp.  Lane hl of half h owns the
+// float4 columns hl and hl + 16 of row `row`; each loop step gathers PU neighbours of BOTH rows, so the
+// shuffles, address math and loop control of one step serve two rows (ncu on the f4 batch: ~52
+// instructions per entry with one row per warp, bound by issue).  Bitwise the same result as
+// light_row<1>: every element is the same ascending-k fp32 FMA chain, and Σy² is the same fp64
+// tree -- lane hl adds its two columns (= the xor-16 step of the 32-lane butterfly), then the
+// xor 8/4/2/1 steps stay inside the half.  `live` = false: this half has no row (odd tail, heavy
+// row); it still executes every shuffle.
+template <bool H>
+__device__ void light_row_pair(const SpmmArgs& a, const Pol& pol, int64_t row, int64_t k0, int64_t k1, bool live,
+                               int lane) {
+    constexpr int PU = 2;                          // neighbours per half per step
+    const int hl = lane & 15, base = lane & 16;
+    const int dp = a.dp;
+    const bool ok0 = 4 * hl < dp, ok1 = 4 * (hl + 16) < dp;
+    const int64_t n_row = live ? k1 - k0 : 0;
+    const int64_t n_max = max(n_row, __shfl_xor_sync(kFull, n_row, 16));
+    if (n_max == 0 && a.skip_zero_rows) return;    // both rows already 0 in T_out (reading RZ)
+    float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
+    const float* tb = a.T_in + 4 * hl;
+    for (int64_t kb = 0; kb < n_max; kb += 16) {
+        const int n = (int)max((int64_t)0, min((int64_t)16, n_row - kb));   // this half's entries here
+        const int nb = (int)min((int64_t)16, n_max - kb);                   // warp-uniform
+        int32_t mc = 0;
+        float mw = 0.0f;
+        if (hl < n) {
+            if (a.csr_prefetch) {
+                mc = __ldg(a.col + k0 + kb + hl);
+                mw = __ldg(a.val + k0 + kb + hl);
+            } else {
+                mc = csr_i32<H>(a.col + k0 + kb + hl, pol);
+                mw = csr_f32<H>(a.val + k0 + kb + hl, pol);
+            }
+        }
+        for (int j = 0; j < nb; j += PU) {
+            float4 x[PU][2];
+            float w[PU];
+#pragma unroll
+            for (int u = 0; u < PU; u++) {
+                const bool act = j + u < n;
+                const int src = base + (j + u < 16 ? j + u : 0);
+                const int ct = __shfl_sync(kFull, mc, src);
+                w[u] = __shfl_sync(kFull, mw, src);
+                const float4* p = reinterpret_cast<const float4*>(tb + (int64_t)(ct & kColMask) * dp);
+                x[u][0] = act && ok0 ? gather4<H, 1>(p, ct, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
+                x[u][1] = act && ok1 ? gather4<H, 1>(p + 16, ct, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < PU; u++)
+                if (j + u < n) {
+                    fma4(acc0, w[u], x[u][0]);
+                    fma4(acc1, w[u], x[u][1]);
+                }
+        }
+    }
+    double ss = 0.0;
+    if (ok0) ss += sq4(acc0);
+    if (ok1) ss += sq4(acc1);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
+    if (!live || (n_row == 0 && a.skip_zero_rows)) return;
+    const double inv = inv_norm(ss);
+    if (ok0) put_out4(a, row, hl, scale4(acc0, inv));
+    if (ok1) put_out4(a, row, hl + 16, scale4(acc1, inv));
+}
+
 template <int V, bool H>
 __device__ void heavy_item(const SpmmArgs& a, const Pol& pol, int64_t idx, float4* red, double* scratch, int* flag) {
     constexpr int SW = 128 * V;
@@ -331,11 +400,31 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_n
                     asm volatile("prefetch.global.L1 [%0];" ::"l"(a.val + off));
                 }
         }
-        for (int64_t r = rb; r < re; r++) {
-            const int64_t k0 = __shfl_sync(kFull, rpl, (int)(r - rb));
-            const int64_t k1 = __shfl_sync(kFull, rpl, (int)(r - rb + 1));
-            if (k1 - k0 > a.heavy_thresh) continue;
-            light_row<V, H>(a, pol, r, k0, k1, lane);
+        if constexpr (V == 1 && CLEORA_V1_PAIR > 0) {
+            // two consecutive short rows (<= CLEORA_V1_PAIR entries each) share the warp, one per
+            // half; a longer row runs alone (pairing it with a short one would idle half the warp)
+            for (int64_t r = rb; r < re;) {
+                const int i = (int)(r - rb);
+                const int64_t e0 = __shfl_sync(kFull, rpl, i), e1 = __shfl_sync(kFull, rpl, i + 1);
+                const bool two = r + 1 < re;
+                const int64_t e2 = __shfl_sync(kFull, rpl, two ? i + 2 : i + 1);
+                const int64_t lim = min((int64_t)CLEORA_V1_PAIR, (int64_t)a.heavy_thresh);
+                if (two && e1 - e0 <= lim && e2 - e1 <= lim) {
+                    const bool hi = lane >= 16;
+                    light_row_pair<H>(a, pol, r + (hi ? 1 : 0), hi ? e1 : e0, hi ? e2 : e1, true, lane);
+                    r += 2;
+                } else {
+                    if (e1 - e0 <= a.heavy_thresh) light_row<V, H>(a, pol, r, e0, e1, lane);
+                    r += 1;
+                }
+            }
+        } else {
+            for (int64_t r = rb; r < re; r++) {
+                const int64_t k0 = __shfl_sync(kFull, rpl, (int)(r - rb));
+                const int64_t k1 = __shfl_sync(kFull, rpl, (int)(r - rb + 1));
+                if (k1 - k0 > a.heavy_thresh) continue;
+                light_row<V, H>(a, pol, r, k0, k1, lane);
+            }
         }
     }
     // peer stores (multi-GPU) are system-scope visible before this launch counts as done; the
