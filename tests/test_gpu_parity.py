@@ -368,3 +368,31 @@ def test_light_chunk_rows_do_not_change_bytes(cl, mode, d, monkeypatch):
             outs.append(cl.cleora_fetch(G, out=torch.empty((g.n, d), dtype=torch.float32, device="cuda")))
             G.close()
         assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2]), f"{g.name} {mode} d={d}"
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("heavy", ["64", "8"])
+def test_short_row_pairs_bitwise_vs_tma_engines(cl, d, heavy, monkeypatch):
+    """At d <= 128 the register kernel runs two short rows per warp (one per half-warp); its result
+    must be bitwise the cp.async / TMA-bulk kernels' (one row per warp, different code).  Graphs mix
+    odd chunk tails, short rows next to long and heavy ones, and rows without out-edges (directed
+    R-MAT: the zero-row skip from iteration 2 on); heavy threshold 8 makes rows of 9-16 entries
+    heavy items, so pairs and heavy rows interleave."""
+    monkeypatch.setenv("CLEORA_HEAVY_THRESH", heavy)
+    rng = np.random.default_rng(11)
+    n = 5000
+    hub = gen.EdgeList("hub", n, np.concatenate([np.zeros(3000, np.int32), rng.integers(0, n, 15000).astype(np.int32)]),
+                       np.concatenate([np.arange(1, 3001, dtype=np.int32), rng.integers(0, n, 15000).astype(np.int32)]),
+                       None, False)
+    graphs = [hub, gen.rmat_directed(8192, 13, 50000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=12),
+              gen.lattice(90, 0.3, 0.02, seed=13), gen.er(3001, 9000, seed=14)]
+    for g in graphs:
+        outs = []
+        for mode in ("ldg", "async", "bulk"):
+            monkeypatch.setenv("CLEORA_GATHER", mode)
+            G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0)
+            cl.cleora_init(G, d, 5)
+            cl.cleora_iterate(G, 3)
+            outs.append(cl.cleora_fetch(G))
+            G.close()
+        assert outs[0].tobytes() == outs[1].tobytes() == outs[2].tobytes(), f"{g.name} d={d} heavy={heavy}"
