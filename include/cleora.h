@@ -73,7 +73,9 @@ typedef struct cleora_opts {
     int32_t rank;            /* this process's rank in [0, world)                               */
     int32_t world;           /* number of GPUs sharing the work; <= 1 means one GPU            */
     const uint8_t* nccl_id;  /* world > 1: the 128-byte ncclUniqueId, identical on all ranks;
-                                the library initialises its own communicator from it         */
+                                the library initialises a communicator from it on the first
+                                build with this (id, world, rank, device) and reuses it for
+                                every later handle of the process (one init per unique id)  */
     int32_t flags;           /* CLEORA_F_* bit set                                              */
     /* Algorithm 1 with Q > 1 chunks.  n_chunks >= 1: this handle holds chunk
        `chunk` of n_chunks -- the edges i with q(i) = floor(n_chunks * (h_i >> 32) / 2^32) = chunk,

@@ -561,6 +561,38 @@ void free_T(cleora_graph* g) {
 
 // Stream-ordered barrier over all ranks (a 1-int all-reduce): work enqueued after it on any rank
 // runs after every rank's work enqueued before it -- including the SpMM's peer stores.
+// NCCL communicators are process-wide and cached by (unique id, world, rank, device): a job builds
+// many handles from one unique id (every bench step, every graph a service embeds), and NCCL serves
+// one ncclCommInitRank per unique id -- a second init from the same id would wait for a bootstrap
+// root that is gone -- besides costing far more than a step.  Handles share the communicator in
+// stream order (every rank issues its handles' collectives in the same order); it lives until the
+// process ends.
+struct CommEntry {
+    std::string key;
+    ncclComm_t comm;
+};
+static std::mutex g_comm_mu;
+static std::vector<CommEntry> g_comms;
+
+Status comm_get(const uint8_t* id128, int world, int rank, int dev, ncclComm_t* out) {
+    std::string key(reinterpret_cast<const char*>(id128), NCCL_UNIQUE_ID_BYTES);
+    key += ":" + std::to_string(world) + ":" + std::to_string(rank) + ":" + std::to_string(dev);
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    for (auto& e : g_comms)
+        if (e.key == key) {
+            *out = e.comm;
+            return Status::ok();
+        }
+    Nccl& nc = nccl();
+    ncclUniqueId id;
+    memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
+    ncclComm_t c = nullptr;
+    CL_NCCL_TRY(nc.CommInitRank(&c, world, id, rank));
+    g_comms.push_back({key, c});
+    *out = c;
+    return Status::ok();
+}
+
 Status rank_barrier(cleora_graph* g) {
     Nccl& N = nccl();
     CL_NCCL_TRY(N.AllReduce(g->d_flag, g->d_flag, 1, ncclInt32, ncclMax, g->comm, g->stream));
@@ -784,9 +816,7 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
         CL_CUDA_TRY(cudaMemsetAsync(g->d_flag, 0, 16, g->stream));
         Nccl& nc = nccl();
         if (!nc.ok) return Status::make(4, "cleora_build: NCCL unavailable: " + nc.why);
-        ncclUniqueId id;
-        memcpy(id.internal, o->nccl_id, NCCL_UNIQUE_ID_BYTES);
-        CL_NCCL_TRY(nc.CommInitRank(&g->comm, g->world, id, g->rank));
+        CL_TRY(comm_get(o->nccl_id, g->world, g->rank, dev, &g->comm));
     }
     // no final synchronisation: the CSR's last kernels run on while the caller goes on to
     // cleora_init (stream order keeps everything that reads them behind them)
@@ -1499,7 +1529,7 @@ void cleora_destroy(cleora_graph* g) {
     if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
     if (g->ev_ready) cudaEventDestroy(g->ev_ready);
     if (g->ev_copied) cudaEventDestroy(g->ev_copied);
-    if (g->comm) nccl().CommDestroy(g->comm);
+    // g->comm belongs to the process-wide cache (comm_get)
     if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
     delete g;
 }

@@ -118,14 +118,17 @@ def _nccl_worker(rank, world, port, exchange_nccl, q):
         obj = [cl_.cleora_nccl_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         g = gen_.chung_lu(20000, 60000, 2.1, 9.5388, 233115.5 * 20000 / 1134890, seed=2)
-        G = cl_.cleora_build(g.src, g.dst, None, g.n, False, device=rank, rank=rank, world=world, nccl_id=obj[0],
-                             exchange_nccl=exchange_nccl)
-        cl_.cleora_init(G, 256, 0)
-        cl_.cleora_iterate(G, 3)
-        T = cl_.cleora_fetch(G)
-        mode = cl_.cleora_info(G)["exchange"]
-        G.close()
-        q.put((rank, mode, T.tobytes()))
+        outs = []
+        for _ in range(2):   # a second handle from the same unique id reuses the communicator
+            G = cl_.cleora_build(g.src, g.dst, None, g.n, False, device=rank, rank=rank, world=world,
+                                 nccl_id=obj[0], exchange_nccl=exchange_nccl)
+            cl_.cleora_init(G, 256, 0)
+            cl_.cleora_iterate(G, 3)
+            outs.append(cl_.cleora_fetch(G))
+            mode = cl_.cleora_info(G)["exchange"]
+            G.close()
+        assert outs[0].tobytes() == outs[1].tobytes()
+        q.put((rank, mode, outs[1].tobytes()))
     finally:
         dist.destroy_process_group()
 
