@@ -270,6 +270,20 @@ typedef struct cleora_stats_t {
 } cleora_stats_t;
 CLEORA_API int cleora_stats(cleora_graph* g, cleora_stats_t* out, int32_t reset);
 
+/* Keep only the current embedding T_i (the result of the last iteration) and
+ * release everything else the handle holds on the device: the CSR of M, the other T buffer, the
+ * schedules and heavy-row partials, loopback replicas, peer mappings.  For a server embedding
+ * graph after graph near the HBM limit: trim a handle once its last iteration and its
+ * cleora_fetch_async are enqueued, and the next graph can be built while the copy runs.  Stream
+ * ordered: work already enqueued (the iterations, an asynchronous fetch) completes normally and the
+ * memory returns to the library's cache behind it.
+ *   Afterwards cleora_fetch, cleora_fetch_async, cleora_merge_chunks, cleora_info, cleora_sync and
+ *   cleora_destroy remain valid; cleora_init, cleora_iterate, cleora_set_rows, cleora_reconstruct,
+ *   cleora_fetch_csr and cleora_fetch_replica of another rank return CLEORA_EUSAGE.
+ *   Errors: EUSAGE (NULL handle, or cleora_init never called: there is no T to keep).
+ *   Trimming twice is a no-op. */
+CLEORA_API int cleora_trim(cleora_graph* g);
+
 /* Wait for all work enqueued on the handle's stream and for its asynchronous fetches. */
 CLEORA_API int cleora_sync(const cleora_graph* g);
 

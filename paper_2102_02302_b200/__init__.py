@@ -21,7 +21,7 @@ __all__ = [
     "CleoraError", "Graph", "LIB_PATH",
     "cleora_build", "cleora_init", "cleora_iterate", "cleora_fetch", "cleora_info", "cleora_stats",
     "cleora_sync", "cleora_destroy", "cleora_last_error", "cleora_fetch_csr", "cleora_set_rows", "cleora_fetch_replica",
-    "cleora_fetch_async",
+    "cleora_fetch_async", "cleora_trim",
     "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
     "cleora_release_cached_memory", "cleora_merge_chunks", "cleora_reconstruct", "cleora_build_batch",
     "cleora_expand", "EXPAND_CLIQUE", "EXPAND_STAR",
@@ -73,6 +73,7 @@ _SIGS = {
     "cleora_info": (ctypes.c_int, [_vp, ctypes.POINTER(_Info)]),
     "cleora_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_Stats), _i32]),
     "cleora_sync": (ctypes.c_int, [_vp]),
+    "cleora_trim": (ctypes.c_int, [_vp]),
     "cleora_destroy": (None, [_vp]),
     "cleora_last_error": (ctypes.c_char_p, []),
     "cleora_fetch_csr": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
@@ -324,6 +325,12 @@ def cleora_stats(g: Graph, reset: bool = False) -> dict:
 
 def cleora_sync(g: Graph):
     _check(_lib.cleora_sync(g.handle))
+
+
+def cleora_trim(g: Graph):
+    """Keep only the current embedding on the device (see include/cleora.h): afterwards the
+    handle can still be fetched (also asynchronously), merged, queried and closed."""
+    _check(_lib.cleora_trim(g.handle))
 
 
 def cleora_destroy(g: Graph):

@@ -230,7 +230,11 @@ Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what) {
         *p = nullptr;
         // out of memory: give cached blocks back to the driver, largest first, until it fits (the
         // rest stays cached for the next graph of the same shape)
-        if (e == cudaErrorMemoryAllocation && release_largest(dev)) continue;
+        if (e == cudaErrorMemoryAllocation && release_largest(dev)) {
+            static const bool tr = getenv("CLEORA_TRACE") != nullptr;
+            if (tr) fprintf(stderr, "[cleora trace] out of memory for %s (%zu bytes): released a cached block\n", what, bytes);
+            continue;
+        }
         char buf[256];
         snprintf(buf, sizeof buf, "cudaMalloc(%zu bytes) for %s: %s", bytes, what, cudaGetErrorString(e));
         return Status::make(4, buf);
@@ -380,6 +384,7 @@ struct cleora_graph {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_copied = nullptr;
     mutable bool copy_pending = false;
+    bool trimmed = false;           // cleora_trim: only T[cur] (and occ, d_scal) left
     int32_t* occ = nullptr;         // chunked builds: endpoint occurrences per node (reading R14)
     int32_t n_graphs = 0;           // batched handles (cleora_build_batch): graphs in the batch
     int64_t* d_base = nullptr;      //   [n_graphs + 1] first row of every graph (device)
@@ -988,6 +993,7 @@ int cleora_build_batch(const int32_t* src, const int32_t* dst, const float* weig
 int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     NvtxRange _nvtx("cleora_init");
     if (!g) return usage("cleora_init: graph is NULL");
+    if (g->trimmed) return usage("cleora_init: the handle was trimmed (cleora_trim)");
     if (d < 1 || d > CLEORA_MAX_D) return usage("cleora_init: d must be in [1, CLEORA_MAX_D]");
     DeviceGuard guard(g->device);
     order_after_side(g);
@@ -1091,6 +1097,7 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
 int cleora_iterate(cleora_graph* g, int32_t k) {
     NvtxRange _nvtx("cleora_iterate");
     if (!g) return usage("cleora_iterate: graph is NULL");
+    if (g->trimmed) return usage("cleora_iterate: the handle was trimmed (cleora_trim)");
     if (k < 0) return usage("cleora_iterate: k must be >= 0");
     if (!g->T[0]) return usage("cleora_iterate: call cleora_init first");
     DeviceGuard guard(g->device);
@@ -1280,6 +1287,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
                        int64_t n_edges, int32_t n_new, int32_t inputs_on_device, float* out, int32_t out_on_device) {
     NvtxRange _nvtx("cleora_reconstruct");
     if (!g || !new_idx || !known_idx || !out) return usage("cleora_reconstruct: NULL argument");
+    if (g->trimmed) return usage("cleora_reconstruct: the handle was trimmed (cleora_trim)");
     if (!g->T[0]) return usage("cleora_reconstruct: call cleora_init first");
     if (n_new < 1) return usage("cleora_reconstruct: n_new must be >= 1");
     if (n_edges < 1) return usage("cleora_reconstruct: n_edges must be >= 1");
@@ -1380,6 +1388,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
 int cleora_fetch_replica(const cleora_graph* g, int32_t rank, int64_t row_begin, int64_t row_end, float* host_out) {
     NvtxRange _nvtx("cleora_fetch_replica");
     if (!g || !host_out) return usage("cleora_fetch_replica: NULL argument");
+    if (g->trimmed && rank != g->rank) return usage("cleora_fetch_replica: the handle was trimmed (cleora_trim)");
     if (!g->T[0]) return usage("cleora_fetch_replica: call cleora_init first");
     if (g->xmode != X_LOOPBACK) {
         if (rank != g->rank) return usage("cleora_fetch_replica: only this rank's replica is local");
@@ -1402,6 +1411,7 @@ int cleora_fetch_replica(const cleora_graph* g, int32_t rank, int64_t row_begin,
 int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const float* host_in) {
     NvtxRange _nvtx("cleora_set_rows");
     if (!g || !host_in) return usage("cleora_set_rows: NULL argument");
+    if (g->trimmed) return usage("cleora_set_rows: the handle was trimmed (cleora_trim)");
     if (!g->T[0]) return usage("cleora_set_rows: call cleora_init first");
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_set_rows: rows outside [0, N]");
     if (row_end == row_begin) return CLEORA_OK;
@@ -1425,6 +1435,7 @@ int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const f
 int cleora_fetch_csr(const cleora_graph* g, int64_t* row_ptr, int32_t* col, float* val, double* deg) {
     NvtxRange _nvtx("cleora_fetch_csr");
     if (!g) return usage("cleora_fetch_csr: graph is NULL");
+    if (g->trimmed) return usage("cleora_fetch_csr: the handle was trimmed (cleora_trim)");
     DeviceGuard guard(g->device);
     cudaError_t e = cudaSuccess;
     if (row_ptr && e == cudaSuccess)
@@ -1469,9 +1480,10 @@ int cleora_info(cleora_graph* g, cleora_info_t* o) {
     o->n_graphs = g->n_graphs;
     o->referenced_rows = g->n_ref;
     o->exchange = g->xmode;
-    o->device_bytes = g->bytes + (g->T[0] ? 2 * (int64_t)g->n * g->dp * 4 : 0) + (int64_t)g->partials_floats * 4 +
+    o->device_bytes = g->bytes + ((g->T[0] ? 1 : 0) + (g->T[1] ? 1 : 0)) * (int64_t)g->n * g->dp * 4 +
+                      (int64_t)g->partials_floats * 4 +
                       g->sched.n_items * (int64_t)sizeof(HeavyItem) + g->sched.n_heavy_rows * 4 +
-                      (g->sched.n_light + 1) * 8;
+                      (g->sched.light_start ? (g->sched.n_light + 1) * 8 : 0);
     DeviceGuard guard(g->device);
     cudaError_t e = cudaStreamSynchronize(g->stream);
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_info: ") + cudaGetErrorString(e)));
@@ -1494,6 +1506,46 @@ int cleora_stats(cleora_graph* g, cleora_stats_t* o, int32_t reset) {
         g->ms_spmm = g->ms_x = g->ms_max = 0;
         g->ms_min = 1e300;
     }
+    return CLEORA_OK;
+}
+
+int cleora_trim(cleora_graph* g) {
+    NvtxRange _nvtx("cleora_trim");
+    if (!g) return usage("cleora_trim: graph is NULL");
+    if (!g->T[0]) return usage("cleora_trim: call cleora_init first");
+    if (g->trimmed) return CLEORA_OK;
+    DeviceGuard guard(g->device);
+    order_after_side(g);   // an asynchronous fetch of T[cur] keeps running; the frees below follow it
+    close_peers(g);
+    for (size_t p = 0; p < g->rep.size(); p++)
+        if ((int)p != g->rank)
+            for (int i = 0; i < 2; i++) {
+                dfree(g->rep[p][i], g->stream);
+                g->rep[p][i] = nullptr;
+            }
+    const int other = 1 - g->cur;
+    dfree(g->T[other], g->stream);
+    g->T[other] = nullptr;
+    if (g->cur == 1) {          // the kept buffer becomes T[0] ("initialised" checks look at T[0])
+        g->T[0] = g->T[1];
+        g->T[1] = nullptr;
+        g->cur = 0;
+    }
+    if (!g->rep.empty()) g->rep[g->rank] = {g->T[0], nullptr};
+    dfree(g->partials, g->stream);
+    g->partials = nullptr;
+    g->partials_floats = 0;
+    free_schedules(g);
+    dfree(g->row_ptr, g->stream);
+    dfree(g->col, g->stream);
+    dfree(g->val, g->stream);
+    dfree(g->deg, g->stream);
+    g->row_ptr = nullptr;
+    g->col = nullptr;
+    g->val = nullptr;
+    g->deg = nullptr;
+    g->bytes = 0;
+    g->trimmed = true;
     return CLEORA_OK;
 }
 

@@ -396,3 +396,33 @@ def test_short_row_pairs_bitwise_vs_tma_engines(cl, d, heavy, monkeypatch):
             outs.append(cl.cleora_fetch(G))
             G.close()
         assert outs[0].tobytes() == outs[1].tobytes() == outs[2].tobytes(), f"{g.name} d={d} heavy={heavy}"
+
+
+def test_trim_keeps_the_embedding_and_frees_the_rest(cl):
+    """cleora_trim keeps only T_I: an asynchronous fetch enqueued before it completes with the same
+    bytes, a blocking fetch after it too, device_bytes drops to one T buffer, and every call that
+    needs the CSR or the other buffer is a usage error.  Odd and even iteration counts (the kept
+    buffer is T[1] or T[0])."""
+    import torch
+    g = gen.config("c1")
+    for iters in (3, 4):
+        G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0)
+        cl.cleora_init(G, 128, 0)
+        cl.cleora_iterate(G, iters)
+        ref = cl.cleora_fetch(G)
+        out = torch.empty((g.n, 128), dtype=torch.float32).pin_memory()
+        cl.cleora_fetch_async(G, 0, g.n, out)
+        before = cl.cleora_info(G)["device_bytes"]
+        cl.cleora_trim(G)
+        cl.cleora_trim(G)                                   # no-op
+        after = cl.cleora_info(G)["device_bytes"]
+        assert after == g.n * 128 * 4 < before
+        cl.cleora_sync(G)
+        assert out.numpy().tobytes() == ref.tobytes()
+        assert cl.cleora_fetch(G).tobytes() == ref.tobytes()
+        for call in (lambda: cl.cleora_iterate(G, 1), lambda: cl.cleora_init(G, 128, 0),
+                     lambda: cl.cleora_fetch_csr(G), lambda: cl.cleora_set_rows(G, 0, ref[:4])):
+            with pytest.raises(cl.CleoraError) as e:
+                call()
+            assert e.value.code == 2
+        G.close()
