@@ -32,6 +32,9 @@
 #ifndef CLEORA_V1_PAIR
 #define CLEORA_V1_PAIR 16      // rows of <= 512 B: two rows of <= this many entries per warp
 #endif
+#ifndef CLEORA_PAIR_PU
+#define CLEORA_PAIR_PU 3       // paired rows: neighbours per half-warp per step (A/B: 1-4)
+#endif
 #ifndef CLEORA_V1_BLOCKS
 #define CLEORA_V1_BLOCKS 4     // rows of <= 512 B: resident CTAs per SM
 #endif
@@ -202,7 +205,7 @@ __device__ void light_row(const SpmmArgs& a, const Pol& pol, int64_t row, int64_
 template <bool H>
 __device__ void light_row_pair(const SpmmArgs& a, const Pol& pol, int64_t row, int64_t k0, int64_t k1, bool live,
                                int lane) {
-    constexpr int PU = 2;                          // neighbours per half per step
+    constexpr int PU = CLEORA_PAIR_PU;             // neighbours per half per step
     const int hl = lane & 15, base = lane & 16;
     const int dp = a.dp;
     const bool ok0 = 4 * hl < dp, ok1 = 4 * (hl + 16) < dp;
