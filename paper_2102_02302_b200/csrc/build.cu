@@ -72,10 +72,12 @@ __global__ void k_validate_expand(const int32_t* __restrict__ src, const int32_t
     }
 }
 
-__global__ void k_head_flags(const uint64_t* __restrict__ keys, int64_t n, uint8_t* __restrict__ flags) {
+// over all n_ent sorted keys: the dropped entries (sentinel keys, sorted last) start no run
+__global__ void k_head_flags(const uint64_t* __restrict__ keys, int64_t n, uint64_t sentinel,
+                             uint8_t* __restrict__ flags) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+        flags[i] = (keys[i] != sentinel && (i == 0 || keys[i] != keys[i - 1])) ? 1 : 0;
 }
 
 // B2: one thread per (a,b) run: sequential fp64 sum in stable order.
@@ -356,13 +358,35 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         if (!keys_only && vb.Current() != pos.p) std::swap(pos.p, pos2.p);
     }
     dfree(keys2.release(), s);
-    // the validation verdict, read once the sort is enqueued (one host round trip for both; on
-    // invalid input the sort's work is simply discarded)
-    unsigned long long h_scal[2];
+    trace("csr: radix sort", s, true);
+
+    // B2: run starts of equal keys, merged weights.  Over all n_ent keys (the dropped entries carry
+    // the sentinel and start no run), so the validation verdict and the run count come back to the
+    // host together below -- on invalid input this work is simply discarded
+    DevBuf<uint8_t> flags;
+    DevBuf<int64_t> run_start;
+    CL_TRY(flags.alloc(n_ent, s, "head flags"));
+    CL_TRY(run_start.alloc(n_ent, s, "run starts"));
+    k_head_flags<<<grid_for(n_ent, 4), kThreads, 0, s>>>(keys.p, n_ent, sentinel, flags.p);
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    {
+        thrust::counting_iterator<int64_t> it(0);
+        size_t tmp_bytes = 0;
+        CL_CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flags.p, run_start.p, scal.p + 4, n_ent, s));
+        DevBuf<uint8_t> tmp;
+        CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
+        CL_CUDA_TRY(cub::DeviceSelect::Flagged(tmp.p, tmp_bytes, it, flags.p, run_start.p, scal.p + 4, n_ent, s));
+        count_launches(2);
+    }
+    dfree(flags.release(), s);
+    // one host round trip: validation verdict (first bad edge, dropped entries, kind) and run count
+    unsigned long long h_scal[2], h_nnz = 0;
     int h_kind = 0;
     {
-        const SmallRead rd[2] = {{h_scal, scal.p, 2 * sizeof(unsigned long long)}, {&h_kind, err_kind.p, sizeof(int)}};
-        CL_TRY(read_small_n(rd, 2, s));
+        const SmallRead rd[3] = {{h_scal, scal.p, 2 * sizeof(unsigned long long)}, {&h_kind, err_kind.p, sizeof(int)},
+                                 {&h_nnz, scal.p + 4, sizeof h_nnz}};
+        CL_TRY(read_small_n(rd, 3, s));
     }
     if (h_kind) {
         char buf[256];
@@ -372,28 +396,6 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         return Status::make(3, buf);
     }
     const int64_t n_valid = n_ent - (int64_t)h_scal[1];
-    trace("csr: radix sort", s, true);
-
-    // B2: run starts of equal keys, merged weights
-    DevBuf<uint8_t> flags;
-    DevBuf<int64_t> run_start;
-    CL_TRY(flags.alloc(n_valid, s, "head flags"));
-    CL_TRY(run_start.alloc(n_valid, s, "run starts"));
-    k_head_flags<<<grid_for(n_valid, 4), kThreads, 0, s>>>(keys.p, n_valid, flags.p);
-    CL_CUDA_TRY(cudaGetLastError());
-    count_launches(1);
-    {
-        thrust::counting_iterator<int64_t> it(0);
-        size_t tmp_bytes = 0;
-        CL_CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flags.p, run_start.p, scal.p + 4, n_valid, s));
-        DevBuf<uint8_t> tmp;
-        CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
-        CL_CUDA_TRY(cub::DeviceSelect::Flagged(tmp.p, tmp_bytes, it, flags.p, run_start.p, scal.p + 4, n_valid, s));
-        count_launches(2);
-    }
-    dfree(flags.release(), s);
-    unsigned long long h_nnz = 0;
-    CL_TRY(read_small(&h_nnz, scal.p + 4, sizeof h_nnz, s));
     const int64_t nnz = (int64_t)h_nnz;
     trace("csr: run select", s, false);
 
