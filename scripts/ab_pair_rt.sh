@@ -1,5 +1,6 @@
 #!/bin/bash
-# runtime pairing on/off (CLEORA_PAIR_ROWS) with the same binary
+# runtime pairing on/off (CLEORA_PAIR_ROWS) with the same binary -- the experiment of a reverted
+# variant (a pair_rows kernel argument); kept as the record of DESIGN §7's measurement
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 for p in 1 0; do
   export CLEORA_PAIR_ROWS=$p

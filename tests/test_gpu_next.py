@@ -211,3 +211,26 @@ def test_expansion_errors(cl):
     with pytest.raises(cl.CleoraError) as e:
         cl.cleora_expand(ptr, np.array([0, 1], np.int32), 5, cl.EXPAND_STAR, np.array([-1.0], np.float32))
     assert e.value.code == cl.EDATA
+
+
+def test_merge_after_trim(cl):
+    """Chunk handles trimmed to their results (cleora_trim keeps T_I and the occurrence counts) merge
+    to the same bytes as untrimmed ones: the memory-lean way to embed Q chunks one after another."""
+    g = gen.config("c1")
+    Q, cseed = 3, 21
+    outs = []
+    for trim in (False, True):
+        hs = []
+        try:
+            for q in range(Q):
+                G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0, n_chunks=Q, chunk=q, chunk_seed=cseed)
+                hs.append(G)
+                cl.cleora_init(G, 96, 2)
+                cl.cleora_iterate(G, 3 if q != 1 else 4)    # odd and even counts: either buffer is kept
+                if trim:
+                    cl.cleora_trim(G)
+            outs.append(cl.cleora_merge_chunks(hs))
+        finally:
+            for G in hs:
+                G.close()
+    assert outs[0].tobytes() == outs[1].tobytes()
