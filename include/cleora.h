@@ -258,6 +258,9 @@ typedef struct cleora_info_t {
     int32_t exchange;       /* 0 one GPU, 1 NCCL all-gather, 2 fused peer stores, 3 loopback */
     int32_t n_graphs;       /* graphs in a batched handle (cleora_build_batch), else 0   */
 } cleora_info_t;
+/* Fill *out.  Synchronises the handle's stream (zero_rows and max_degree are computed on the device
+ * by cleora_build and read back here, on first use; the handle caches them -- hence non-const).
+ *   Errors: EUSAGE (NULL argument); EINTERNAL (a CUDA error of earlier asynchronous work). */
 CLEORA_API int cleora_info(cleora_graph* g, cleora_info_t* out);
 
 /* Device-time statistics (requires CLEORA_F_TIMING; otherwise counts stay 0). */
