@@ -121,6 +121,16 @@ def dist_env():
     return world, rank, local
 
 
+def e2e_schedule(handle_bytes, t_bytes, total_hbm):
+    """How the e2e steps overlap: "full" = two whole handles alive (step i's copy beside step i+1),
+    "trim" = step i trimmed to its result T first (cleora_trim), None = serial."""
+    if 2 * handle_bytes < 0.85 * total_hbm:
+        return "full"
+    if handle_bytes + t_bytes < 0.9 * total_hbm:
+        return "trim"
+    return None
+
+
 def cpu_baseline(g, M_holder, d, iters, budget_s=12.0):
     """The oracle as it stands on this host.  Small graphs: full CSR build, T_0 and all I
     iterations when that fits ~budget_s, else one iteration over a leading block of rows with
@@ -420,13 +430,7 @@ def main():
         # fit in HBM (c5: one is ~110 GB of the 180 GB), the previous handle is trimmed to its result
         # (cleora_trim) once its fetch is enqueued, so only its T buffer overlaps the next build.
         total_hbm = torch.cuda.get_device_properties(local).total_memory
-        t_bytes = g.n * ((d + 3) // 4 * 4) * 4
-        if 2 * info["device_bytes"] < 0.85 * total_hbm:
-            pipe_mode = "full"
-        elif info["device_bytes"] + t_bytes < 0.9 * total_hbm:
-            pipe_mode = "trim"
-        else:
-            pipe_mode = None
+        pipe_mode = e2e_schedule(info["device_bytes"], g.n * ((d + 3) // 4 * 4) * 4, total_hbm)
         pipelined = pipe_mode is not None
         outs = [torch.empty((g.n, d), dtype=torch.float32).pin_memory() for _ in range(2 if pipelined else 1)]
 

@@ -38,3 +38,15 @@ def test_cpu_baseline_helpers():
     cs = bench.ClockSampler(0)            # no NVML device here: an empty summary, no exception
     s = cs.summary()
     assert s["samples"] == 0 and s["sm_mhz"] is None
+
+
+def test_e2e_schedule_by_memory():
+    """e2e overlap schedule from the handle's footprint (B200: 180 GB): c2 (~14 GB per handle) keeps
+    two whole handles, c5 (~110 GB, T 42.7 GB) trims the previous one to its result, and a handle
+    that leaves no room for another T runs serially."""
+    sys.path.insert(0, ROOT)
+    import bench
+    hbm = 180 * 10**9
+    assert bench.e2e_schedule(14 * 10**9, 4.65 * 10**9, hbm) == "full"
+    assert bench.e2e_schedule(110 * 10**9, 42.7 * 10**9, hbm) == "trim"
+    assert bench.e2e_schedule(150 * 10**9, 42.7 * 10**9, hbm) is None
