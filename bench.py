@@ -1,6 +1,10 @@
 #!/usr/bin/env python
 """Benchmark of the Cleora hot path on B200 (BASELINE.json metric, one JSON line on rank 0).
 
+The workload is c4 (BASELINE.json configs[3], the LiveJournal stand-in, "row-sharded at 1/2/4/8
+GPUs": the metric's own configuration and the largest one that runs on one GPU); c2 and c3 are
+reported beside it as secondary SpMM figures (``secondary``).  ``--config`` selects another.
+
 A *step* is one pass of the whole hot path over one synthetic
 graph: cleora_build (validate, mirror, radix sort, merge, row pointer, degree, D^-1 scaling,
 schedule) -> cleora_init (hash T_0) -> cleora_iterate(I) (I fused SpMM + row-normalise
@@ -10,9 +14,12 @@ buffers: pinned COO in, H2D inside cleora_build, and cleora_fetch of all N x d r
 pinned host memory, inside the timed region.
 
 value = nnz * d * I / step_time   (nnz = stored CSR entries; BASELINE metric "nnz·d/s")
-Multi-GPU (torchrun, one rank per GPU, NCCL): M is row-sharded by nnz balance, every rank
-keeps a full T replica, each iteration ends with an all-gather; the total work is the same
-graph for every N ("scaling": "strong"); time = max over ranks of CUDA-event step time.
+Multi-GPU (one rank per GPU, NCCL): ``--gpus N`` under torchrun (WORLD_SIZE set, must equal N),
+or ``python bench.py --gpus N`` alone, which re-launches itself under torch.distributed.run with
+N ranks.  M is row-sharded by nnz balance (each rank builds and keeps only its rows), every rank
+keeps a full T replica, each iteration's rows reach the other replicas through the fused
+peer-store exchange; the total work is the same graph for every N ("scaling": "strong"); time =
+max over ranks of CUDA-event step time.
 
 --impl reference times the CPU oracle (oracle/, plain C + OpenMP) on a bounded sample of the
 same workload (one oracle iteration over a leading block of rows), on rank 0 only.
@@ -252,12 +259,24 @@ def run_reference(args, g, world, rank):
     print(json.dumps(line), flush=True)
 
 
+L2_BYTES = 126 * 2**20
+FLUSH_BYTES = 512 * 2**20
+
+
+def t_bytes(g):
+    return g.n * ((g.d + 3) // 4 * 4) * 4
+
+
 def config_dict(g, world):
+    tb = t_bytes(g)
+    l2 = (f"inputs larger than L2: T = {tb / 1e9:.2f} GB per replica > 126 MB L2, no flush" if tb > 4 * L2_BYTES else
+          f"T = {tb / 1e6:.1f} MB per replica is not >> 126 MB L2: L2 flushed ({FLUSH_BYTES >> 20} MB write) "
+          "before every timed step, outside the step's events")
     return {"workload": g.name, "desc": g.meta.get("desc", ""), "N": g.n, "edges_in": g.n_edges,
             "d": g.d, "iterations": g.iters, "directed": g.directed, "weighted": g.w is not None,
             "parallelism": f"rowshard{world}" if world > 1 else "single",
             "exchange": "fused peer stores + NCCL barrier (NCCL all-gather fallback)" if world > 1 else "none",
-            "l2": "inputs larger than L2 (T = N*d*4 bytes per replica >> 126 MB)"}
+            "l2": l2}
 
 
 def load_traffic(name, d):
@@ -271,21 +290,98 @@ def load_traffic(name, d):
         return None
 
 
-def main():
+def launch_ranks(args, argv):
+    """``--gpus N`` without WORLD_SIZE: re-run this script under torch.distributed.run with N ranks
+    on this node (the driver's own launch line), and return its exit code."""
+    import socket
+    import subprocess
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def parse_args(argv):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cleora", choices=["cleora", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    args = ap.parse_args()
+    ap.add_argument("--no-secondary", action="store_true", help="skip the c2/c3 SpMM figures")
+    ap.add_argument("--dry-launch", action="store_true",
+                    help="launch test: every rank prints its rank/world as JSON and exits (no GPU work)")
+    return ap.parse_args(argv)
+
+
+def measure_secondary(cl, names, dev, local, stream, peak, reps=3):
+    """SpMM-only figures of other configs (N = 1): build once, then `reps` x (init + I iterations),
+    device time of every fused SpMM launch from the library's CUDA events; first rep discarded."""
+    import gen
+    import torch
+    out = {}
+    for name in names:
+        g = gen.config(name)
+        d, iters = g.d, g.iters
+        src = torch.from_numpy(g.src).to(dev)
+        dst = torch.from_numpy(g.dst).to(dev)
+        w = torch.from_numpy(g.w).to(dev) if g.w is not None else None
+        G = cl.cleora_build(src, dst, w, g.n, g.directed, device=local, stream=stream.cuda_stream, timing=True)
+        try:
+            for r in range(reps):
+                cl.cleora_init(G, d, 0)
+                cl.cleora_iterate(G, iters)
+                st = cl.cleora_stats(G, reset=(r == 0))
+            info = cl.cleora_info(G)
+        finally:
+            G.close()
+        ms = st["spmm_ms_total"] / max(1, st["spmm_launches"])
+        nnz = info["nnz"]
+        b_comp = 8 * (g.n + 1) + 8 * nnz + 2 * g.n * d * 4
+        ref_rows = info["referenced_rows"] if info["referenced_rows"] >= 0 else g.n
+        b_strict = 8 * (g.n + 1) + 8 * nnz + (ref_rows + g.n - info["zero_rows"]) * d * 4
+        out[name] = {"d": d, "iterations": iters, "nnz": nnz, "spmm_ms": ms, "spmm_ms_min": st["spmm_ms_min"],
+                     "nnz_d_per_s": nnz * d / (ms / 1e3), "frac": b_comp / (ms / 1e3) / 1e9 / peak,
+                     "strict_frac": b_strict / (ms / 1e3) / 1e9 / peak, "algorithmic_bytes_per_launch": b_comp,
+                     "traffic": load_traffic(name, d), "launches": st["spmm_launches"]}
+        del src, dst, w
+    return out
+
+
+def main():
+    argv = sys.argv[1:]
+    args = parse_args(argv)
     if args.warmup < 3 and args.impl != "reference":
         print("bench.py: --warmup must be >= 3", file=sys.stderr)
         args.warmup = 3
-
+    if args.gpus < 1:
+        print("bench.py: --gpus must be >= 1", file=sys.stderr)
+        sys.exit(2)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(launch_ranks(args, argv))
     world, rank, local = dist_env()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+              f"(torchrun --nproc-per-node {args.gpus}) or omit WORLD_SIZE", file=sys.stderr)
+        sys.exit(2)
+    if world > 1:
+        # torch.distributed.run sets OMP_NUM_THREADS=1; the generators (and the reference arm's oracle,
+        # rank 0 alone) are OpenMP programs: give each rank its share of the host cores (all of them to
+        # the reference arm's only working rank).  Read by libgomp when it is first loaded, below.
+        ncpu = os.cpu_count() or 1
+        os.environ["OMP_NUM_THREADS"] = str(ncpu if args.impl == "reference" else max(1, ncpu // world))
+    if args.dry_launch:
+        # one write() per line: the ranks share the launcher's stdout
+        sys.stdout.write(json.dumps({"dry_launch": True, "rank": rank, "world": world, "local_rank": local}) + "\n")
+        sys.stdout.flush()
+        return
+
     import gen
     g = gen.config(args.config)
 
@@ -324,6 +420,8 @@ def main():
     src_d = torch.from_numpy(g.src).to(dev)
     dst_d = torch.from_numpy(g.dst).to(dev)
     w_d = torch.from_numpy(g.w).to(dev) if g.w is not None else None
+    # T smaller than a few L2s: write a buffer larger than L2 before every timed step (outside its events)
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev) if t_bytes(g) <= 4 * L2_BYTES else None
     torch.cuda.synchronize()
 
     xnccl = [False]      # multi-GPU: fused peer-store exchange unless it fails on this box
@@ -359,29 +457,35 @@ def main():
         G.close()
     nnz = info["nnz"]
 
-    # timed region: K steps, CUDA events on the library's stream, barrier + sync on both sides
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # timed region: K steps, CUDA events on the library's stream around every step, barrier + sync
+    # on both sides; a step's time is build + init + I iterations (the L2 flush, when there is one,
+    # runs between a step's end event and the next step's start event)
     barrier()
     torch.cuda.synchronize()
     launches0 = cl.cleora_kernel_launches()
-    per_step = []
+    steps_ev = []
     spmm_ev = []
     t_w0 = time.perf_counter()
-    ev0.record(stream)
     for _ in range(args.steps):
-        e_a = torch.cuda.Event(enable_timing=True)
+        if flush is not None:
+            with torch.cuda.stream(stream):
+                flush.zero_()
+        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e_a.record(stream)
         G = one_step(spmm_events=spmm_ev)
+        e_b.record(stream)
         G.close()
-        per_step.append(e_a)
-    ev1.record(stream)
-    ev1.synchronize()
+        steps_ev.append((e_a, e_b))
+    steps_ev[-1][1].synchronize()
     clk.mark(t_w0, time.perf_counter())
-    step_ms = [a.elapsed_time(b) for a, b in zip(per_step, per_step[1:] + [ev1])]
     torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in steps_ev]
     launches = cl.cleora_kernel_launches() - launches0
     barrier()
-    ms_step = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    # without a flush the K steps run back to back and the bracket is first start -> last end (the
+    # destroy of step i between them included); with a flush, the sum of the steps' own brackets
+    span = steps_ev[0][0].elapsed_time(steps_ev[-1][1]) if flush is None else sum(step_ms)
+    ms_step = max_over_ranks(span / args.steps)
     value = nnz * d * iters / (ms_step / 1e3)
 
     # dominant kernel: the fused SpMM+normalise launches, timed live in the timed steps with CUDA
@@ -403,13 +507,30 @@ def main():
     ref_rows = info.get("referenced_rows", -1)
     ref_rows = g.n if ref_rows is None or ref_rows < 0 else ref_rows
     b_strict = (8 * (g.n + 1) + 8 * nnz + (ref_rows + g.n - info["zero_rows"]) * d * 4) / world
+    # the second roofline (SURVEY §8(d) "Which roofline"): the gather operand stream nnz*d*4, every
+    # byte of which crosses L2 -> SM, at the random-row gather rate measured now on this GPU
+    # (cleora_probe_gather: rows of d*4 bytes from an L2-resident 32 MiB table)
+    row_b = max(16, min(4096, (d + 3) // 4 * 16))
+    while row_b < 512 and 512 % row_b:
+        row_b += 16
+    l2_rate = cl.cleora_probe_gather(row_b, 32 << 20, max(1 << 20, (1 << 32) // row_b), local)
+    gather_b = nnz * d * 4 / world
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": load_traffic(g.name, d), "kernel": "k_spmm_tma (fused SpMM + row L2 normalise)",
                 "kernel_ms": spmm_ms, "kernel_timing": "CUDA events around cleora_iterate in the timed steps",
                 "algorithmic_bytes_per_launch": b_comp, "peak_source": peak_src,
                 "strict_bytes_per_launch": b_strict, "strict_frac": b_strict / (spmm_ms / 1e3) / 1e9 / peak,
-                "gather_bytes_per_launch": nnz * d * 4 / world,
+                "gather_bytes_per_launch": gather_b,
+                "gather_bound": {"bytes": gather_b, "l2_gather_gbs": l2_rate, "row_bytes": row_b,
+                                 "ms": gather_b / (l2_rate * 1e9) * 1e3 if l2_rate > 0 else None,
+                                 "frac": (gather_b / (l2_rate * 1e9) * 1e3) / spmm_ms if l2_rate > 0 else None,
+                                 "how": "nnz*d*4 / random-row gather rate from an L2-resident 32 MiB table, "
+                                        "measured live (cleora_probe_gather)"},
                 "bytes_def": "8(N+1) + 8 nnz + 2 N d 4 (CSR + one read and one write of T), per rank"}
+    tr = roofline["traffic"]
+    if tr:
+        roofline["traffic_gbs"] = tr / (spmm_ms / 1e3) / 1e9
+    del flush
 
     # e2e through the public C-ABI with host buffers (pinned), copies inside the timed region.
     # Every step: H2D of the COO (inside cleora_build), build, init, I iterations, D2H of all N x d
@@ -430,7 +551,7 @@ def main():
         # fit in HBM (c5: one is ~110 GB of the 180 GB), the previous handle is trimmed to its result
         # (cleora_trim) once its fetch is enqueued, so only its T buffer overlaps the next build.
         total_hbm = torch.cuda.get_device_properties(local).total_memory
-        pipe_mode = e2e_schedule(info["device_bytes"], g.n * ((d + 3) // 4 * 4) * 4, total_hbm)
+        pipe_mode = e2e_schedule(info["device_bytes"], t_bytes(g), total_hbm)
         pipelined = pipe_mode is not None
         outs = [torch.empty((g.n, d), dtype=torch.float32).pin_memory() for _ in range(2 if pipelined else 1)]
 
@@ -498,7 +619,16 @@ def main():
         e2e = {"value": nnz * d * iters / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": g.n * d * 4, "ms_per_step": ms_e2e, "steps": k2, "wall_ms_per_step": wall,
                "mode": mode, "serial_value": nnz * d * iters / (ms_serial / 1e3), "serial_ms_per_step": ms_serial}
-        del outs
+        del outs, src_h, dst_h, w_h
+    clk.stop()
+
+    # secondary configs (N = 1): the c2 / c3 SpMM figures beside the headline
+    secondary = None
+    if world == 1 and not args.no_secondary:
+        src_d = dst_d = w_d = None
+        torch.cuda.empty_cache()
+        names = [n for n in ("c2", "c3") if n != g.name]
+        secondary = measure_secondary(cl, names, dev, local, stream, peak)
 
     # CPU oracle baseline: rank 0 at N = 1 only, bounded sample
     cpu = None
@@ -526,11 +656,12 @@ def main():
                 "iteration": {"ms": spmm_ms, "nnz_d_per_s": nnz * d / (spmm_ms / 1e3),
                               "exchange_ms": (xms / max(iters, 1)) if world > 1 else 0.0},
                 "nnz": nnz, "heavy_rows": info["heavy_rows"], "heavy_items": info["heavy_items"],
+                "hot_rows": info["hot_rows"], "zero_rows": info["zero_rows"],
+                "referenced_rows": info["referenced_rows"],
                 "step_ms_each": [round(x, 3) for x in step_ms],
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "secondary": secondary, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches,
                 "clocks": clk.summary()}
-        clk.stop()
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

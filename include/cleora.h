@@ -68,7 +68,8 @@ typedef struct cleora_opts {
     int32_t device;          /* CUDA device ordinal; -1 = the calling thread's current device */
     int32_t input_on_device; /* 1: src/dst/weight are device pointers on `device`;
                                 0: host pointers (pageable or pinned)                          */
-    void* stream;            /* cudaStream_t to enqueue on (borrowed; must outlive the handle);
+    void* stream;            /* cudaStream_t to enqueue on (borrowed; must outlive the handle),
+                                cudaStreamLegacy (0x1) for the legacy default stream;
                                 NULL = the library creates and owns a non-blocking stream    */
     int32_t rank;            /* this process's rank in [0, world)                               */
     int32_t world;           /* number of GPUs sharing the work; <= 1 means one GPU            */
@@ -307,6 +308,15 @@ CLEORA_API int64_t cleora_kernel_launches(void);
  * driver (e.g. before handing the memory to another library).  Returns CLEORA_OK or
  * EINTERNAL. */
 CLEORA_API int cleora_release_cached_memory(void);
+
+/* Diagnostic (not on the Cleora path): the rate, in GB/s, at which the SMs of `device` (-1: current)
+ * gather random rows of `row_bytes` (a multiple of 16; below 512 B it must divide 512) from an
+ * L2-resident table of `table_bytes` (e.g. 64 MiB), n_gathers rows per launch, best of 6 timed
+ * launches (CUDA events).  The SpMM's gather stream, nnz * d * 4 bytes per iteration, all passes
+ * the L2 -> SM path: bench.py reports nnz * d * 4 / this rate as the gather bound next to the HBM
+ * roofline (SURVEY.md §8(d) "Which roofline").  Errors: EUSAGE, EINTERNAL. */
+CLEORA_API int cleora_probe_gather(int32_t device, int32_t row_bytes, int64_t table_bytes, int64_t n_gathers,
+                                   double* gbs);
 
 /* ---- test hooks (not on the graded path) ------------------------------------------------ */
 

@@ -24,7 +24,7 @@ __all__ = [
     "cleora_fetch_async", "cleora_trim",
     "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
     "cleora_release_cached_memory", "cleora_merge_chunks", "cleora_reconstruct", "cleora_build_batch",
-    "cleora_expand", "EXPAND_CLIQUE", "EXPAND_STAR",
+    "cleora_expand", "EXPAND_CLIQUE", "EXPAND_STAR", "cleora_probe_gather",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcleora.so")
@@ -86,6 +86,7 @@ _SIGS = {
     "cleora_plan_shards": (ctypes.c_int, [_vp, _i64, _i32, _vp]),
     "cleora_kernel_launches": (ctypes.c_int64, []),
     "cleora_release_cached_memory": (ctypes.c_int, []),
+    "cleora_probe_gather": (ctypes.c_int, [_i32, _i32, _i64, _i64, ctypes.POINTER(ctypes.c_double)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -124,11 +125,34 @@ def _ptr(a, dtype):
     return arr.ctypes.data, False, arr
 
 
-class Graph:
-    """Owning wrapper of a ``cleora_graph*`` (destroyed on close / garbage collection)."""
+def _torch_stream(device) -> int:
+    """cudaStream_t of torch's current stream on `device` (an index or torch.device).  torch's default
+    stream is the legacy NULL stream; it is passed as cudaStreamLegacy (0x1), because a NULL
+    cleora_opts.stream means "a library-owned non-blocking stream", which would not be ordered."""
+    import torch
+    return int(torch.cuda.current_stream(device).cuda_stream) or 1
 
-    def __init__(self, handle: int):
+
+def _order_after_torch(tensors, lib_stream):
+    """CUDA tensors handed to a call that runs on another stream than torch's current one: wait for
+    torch's pending work on them first (a tensor just written by a torch kernel, or a block the
+    caching allocator recycled while older kernels may still use it).  No-op for host arrays."""
+    for t in tensors:
+        if t is not None and getattr(t, "is_cuda", False):
+            import torch
+            cur = torch.cuda.current_stream(t.device)
+            if lib_stream is None or (int(cur.cuda_stream) or 1) != int(lib_stream):
+                cur.synchronize()
+            return
+
+
+class Graph:
+    """Owning wrapper of a ``cleora_graph*`` (destroyed on close / garbage collection).  ``stream``
+    is the cudaStream_t the handle enqueues on (None: a library-owned stream)."""
+
+    def __init__(self, handle: int, stream: int | None = None):
         self._h = handle
+        self.stream = stream
 
     @property
     def handle(self) -> int:
@@ -187,6 +211,10 @@ def cleora_build(src, dst, weight, n_nodes: int, directed: bool = False, *, devi
         raise CleoraError(EUSAGE, "src/dst/weight must be all on the host or all on the device")
     if on_dev and device < 0:
         device = int(ks.device.index or 0)
+    if stream is None and on_dev:
+        # device inputs: enqueue on torch's current stream, so the build is ordered after the
+        # kernels that produced them (and torch's later work after the build)
+        stream = _torch_stream(ks.device)
     o = _Opts()
     o.device = device
     o.input_on_device = 1 if on_dev else 0
@@ -202,7 +230,7 @@ def cleora_build(src, dst, weight, n_nodes: int, directed: bool = False, *, devi
     o.n_chunks, o.chunk, o.chunk_seed = int(n_chunks), int(chunk), int(chunk_seed) & 0xFFFFFFFFFFFFFFFF
     h = ctypes.c_void_p()
     _check(_lib.cleora_build(ps, pd, pw, n, int(n_nodes), 1 if directed else 0, ctypes.byref(o), ctypes.byref(h)))
-    return Graph(h.value)
+    return Graph(h.value, o.stream)
 
 
 EXPAND_CLIQUE, EXPAND_STAR = 0, 1
@@ -219,6 +247,8 @@ def cleora_expand(he_ptr, he_nodes, n_nodes: int, mode: int, he_weight=None, *, 
     if on_dev and not (dp_ and dn and (kw is None or dw)):
         raise CleoraError(EUSAGE, "inputs must be all on the host or all on the device")
     n_he = int(kp.shape[0]) - 1
+    if stream is None and on_dev:
+        stream = _torch_stream(kp.device)        # ordered after the kernels that produced the inputs
     st = 0 if stream is None else (stream if isinstance(stream, int) else int(getattr(stream, "cuda_stream", stream)))
     if on_dev and device < 0:
         device = int(kp.device.index or 0)
@@ -263,6 +293,8 @@ def cleora_build_batch(src, dst, weight, edge_ptr, node_count, directed: bool = 
         raise CleoraError(EUSAGE, "src/dst/weight must be all on the host or all on the device")
     if on_dev and device < 0:
         device = int(ks.device.index or 0)
+    if stream is None and on_dev:
+        stream = _torch_stream(ks.device)
     o = _Opts()
     o.device = device
     o.input_on_device = 1 if on_dev else 0
@@ -273,7 +305,7 @@ def cleora_build_batch(src, dst, weight, edge_ptr, node_count, directed: bool = 
     h = ctypes.c_void_p()
     _check(_lib.cleora_build_batch(ps, pd, pw, ep.ctypes.data, nc.ctypes.data, int(nc.shape[0]), 1 if directed else 0,
                                    ctypes.byref(o), ctypes.byref(h)))
-    return Graph(h.value)
+    return Graph(h.value, o.stream)
 
 
 def cleora_init(g: Graph, d: int, seed: int = 0):
@@ -296,6 +328,7 @@ def cleora_fetch(g: Graph, row_begin: int = 0, row_end: int | None = None, out=N
     p, on_dev, keep = _ptr(out, np.float32)
     if keep is not out:
         raise CleoraError(EUSAGE, "out must be a contiguous fp32 array")
+    _order_after_torch([out], g.stream)
     _check(_lib.cleora_fetch(g.handle, int(row_begin), int(row_end), p, 1 if on_dev else 0))
     return out
 
@@ -307,6 +340,7 @@ def cleora_fetch_async(g: Graph, row_begin: int, row_end: int, out):
     p, on_dev, keep = _ptr(out, np.float32)
     if keep is not out:
         raise CleoraError(EUSAGE, "out must be a contiguous fp32 array")
+    _order_after_torch([out], None)
     _check(_lib.cleora_fetch_async(g.handle, int(row_begin), int(row_end), p, 1 if on_dev else 0))
     return out
 
@@ -366,6 +400,7 @@ def cleora_merge_chunks(chunks, out=None):
     p, on_dev, keep = _ptr(out, np.float32)
     if keep is not out:
         raise CleoraError(EUSAGE, "out must be a contiguous fp32 array")
+    _order_after_torch([out], chunks[0].stream)
     arr = (ctypes.c_void_p * len(chunks))(*[c.handle for c in chunks])
     _check(_lib.cleora_merge_chunks(ctypes.cast(arr, ctypes.c_void_p), len(chunks), p, 1 if on_dev else 0))
     return out
@@ -391,6 +426,7 @@ def cleora_reconstruct(g: Graph, new_idx, known_idx, weight, n_new: int, out=Non
     po, od, ko = _ptr(out, np.float32)
     if ko is not out:
         raise CleoraError(EUSAGE, "out must be a contiguous fp32 array")
+    _order_after_torch([kn, kk, kw, out], g.stream)
     _check(_lib.cleora_reconstruct(g.handle, pn, pk, pw, n_e, int(n_new), 1 if on_dev else 0, po, 1 if od else 0))
     return out
 
@@ -426,3 +462,10 @@ def cleora_kernel_launches() -> int:
 def cleora_release_cached_memory():
     """Return the library's cached device blocks (freed T replicas, CSR, sort buffers) to the driver."""
     _check(_lib.cleora_release_cached_memory())
+
+
+def cleora_probe_gather(row_bytes: int, table_bytes: int = 64 << 20, n_gathers: int = 1 << 22, device: int = -1) -> float:
+    """Random-row gather rate (GB/s) from an L2-resident table (diagnostic; see include/cleora.h)."""
+    r = ctypes.c_double()
+    _check(_lib.cleora_probe_gather(int(device), int(row_bytes), int(table_bytes), int(n_gathers), ctypes.byref(r)))
+    return float(r.value)

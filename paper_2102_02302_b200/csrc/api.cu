@@ -857,6 +857,7 @@ int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, in
         if (!opts->nccl_id && !(opts->flags & CLEORA_F_LOOPBACK))
             return usage("cleora_build: world > 1 needs nccl_id");
         if (opts->rank < 0 || opts->rank >= opts->world) return usage("cleora_build: rank outside [0, world)");
+        if (opts->world > 511) return usage("cleora_build: world > 511 (shard cuts are read back in one 4 KB read)");
     }
     if (opts && opts->n_chunks != 0) {
         if (opts->n_chunks < 0 || opts->chunk < 0 || opts->chunk >= opts->n_chunks)
@@ -902,6 +903,7 @@ int cleora_expand(const int64_t* he_ptr, const int32_t* he_nodes, const float* h
         cudaError_t e = cudaMemcpyAsync(&n_members, he_ptr + n_hyperedges, sizeof n_members, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_expand: ") + cudaGetErrorString(e)));
+        if (n_members < 0) return usage("cleora_expand: he_ptr must start at 0 and be non-decreasing");
     } else {
         n_members = he_ptr[n_hyperedges];
         if (he_ptr[0] != 0) return usage("cleora_expand: he_ptr[0] must be 0");
@@ -1515,7 +1517,10 @@ int cleora_trim(cleora_graph* g) {
     if (!g->T[0]) return usage("cleora_trim: call cleora_init first");
     if (g->trimmed) return CLEORA_OK;
     DeviceGuard guard(g->device);
-    order_after_side(g);   // an asynchronous fetch of T[cur] keeps running; the frees below follow it
+    // no order_after_side here: an asynchronous fetch of T[cur] keeps running on the copy stream and
+    // reads nothing freed below (T[cur] stays); copy_pending stays set, so later fetches, merges and
+    // destroy still order after it.  (Waiting here made the handle's stream -- often shared with the
+    // next graph's build -- queue behind the D2H copy: ADVICE r1.)
     close_peers(g);
     for (size_t p = 0; p < g->rep.size(); p++)
         if ((int)p != g->rank)
@@ -1584,6 +1589,26 @@ void cleora_destroy(cleora_graph* g) {
     // g->comm belongs to the process-wide cache (comm_get)
     if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
     delete g;
+}
+
+int cleora_probe_gather(int32_t device, int32_t row_bytes, int64_t table_bytes, int64_t n_gathers, double* gbs) {
+    NvtxRange _nvtx("cleora_probe_gather");
+    if (!gbs) return usage("cleora_probe_gather: gbs is NULL");
+    if (table_bytes < row_bytes || n_gathers < 1 || n_gathers > INT32_MAX)
+        return usage("cleora_probe_gather: table_bytes >= row_bytes and 1 <= n_gathers < 2^31 required");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(Status::make(4, "cleora_probe_gather: no CUDA device visible"));
+    }
+    DeviceGuard guard(device);
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(Status::make(4, "cleora_probe_gather: stream"));
+    Status st = probe_gather(row_bytes, table_bytes, n_gathers, s, gbs);
+    cudaStreamDestroy(s);
+    if (!st.good()) return fail(st);
+    return CLEORA_OK;
 }
 
 int cleora_nccl_id_size(void) { return NCCL_UNIQUE_ID_BYTES; }

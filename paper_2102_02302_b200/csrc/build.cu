@@ -712,7 +712,7 @@ Status batch_global_ids(const int32_t* d_src, const int32_t* d_dst, int64_t E, c
 Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts) {
     DevBuf<int64_t> cuts;
     CL_TRY(cuts.alloc(world + 1, s, "shard cuts"));
-    k_cuts<<<1, 128, 0, s>>>(d_row_ptr, N, world, cuts.p);
+    k_cuts<<<(world + 128) / 128, 128, 0, s>>>(d_row_ptr, N, world, cuts.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     CL_TRY(read_small(h_cuts, cuts.p, (world + 1) * sizeof(int64_t), s));

@@ -189,6 +189,8 @@ Status batch_global_ids(const int32_t* d_src, const int32_t* d_dst, int64_t E, c
 Status launch_spmm_norm(const SpmmArgs& a, cudaStream_t s);
 enum { kGatherLdg = 0, kGatherBulk = 1, kGatherAsync = 2 };
 int gather_mode(int dp);          // which gather engine serves rows of dp floats
+// probe.cu: random-row gather rate (GB/s) from an L2-resident table of table_bytes (diagnostic)
+Status probe_gather(int row_bytes, int64_t table_bytes, int64_t n_gathers, cudaStream_t s, double* gbs);
 bool tma_path_supported(int dp);  // gather_mode(dp) uses the shared-memory ring kernel
 Status launch_spmm_tma(const SpmmArgs& a, cudaStream_t s);
 

@@ -20,14 +20,19 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__global__ void k_expand_check(const int32_t* __restrict__ nodes, int64_t n, int32_t n_nodes,
-                               const float* __restrict__ w, int64_t n_he, unsigned long long* __restrict__ bad) {
+// bad[0]: first member id out of range; bad[1]: first bad weight; bad[2]: first hyperedge e whose
+// offsets are not ptr[0] = 0, ptr[e] <= ptr[e+1] (a malformed ptr would make the expansion kernels
+// write outside the output, so it is rejected before they run, as on the host path)
+__global__ void k_expand_check(const int64_t* __restrict__ ptr, const int32_t* __restrict__ nodes, int64_t n,
+                               int32_t n_nodes, const float* __restrict__ w, int64_t n_he,
+                               unsigned long long* __restrict__ bad) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         if (nodes[i] < 0 || nodes[i] >= n_nodes) atomicMin(bad, (unsigned long long)i);
-    if (w)
-        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_he; e += stride)
-            if (!(isfinite(w[e]) && w[e] > 0.0f)) atomicMin(bad + 1, (unsigned long long)e);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_he; e += stride) {
+        if (w && !(isfinite(w[e]) && w[e] > 0.0f)) atomicMin(bad + 1, (unsigned long long)e);
+        if ((e == 0 && ptr[0] != 0) || ptr[e + 1] < ptr[e]) atomicMin(bad + 2, (unsigned long long)e);
+    }
 }
 
 // count (out == nullptr) or write the clique pairs of each hyperedge
@@ -93,16 +98,20 @@ Status expand_hypergraph(const int64_t* d_ptr, const int32_t* d_nodes, const flo
     // validation
     {
         unsigned long long* bad = nullptr;
-        CL_TRY(dalloc((void**)&bad, 2 * sizeof(unsigned long long), s, "expand check"));
-        cudaMemsetAsync(bad, 0xFF, 2 * sizeof(unsigned long long), s);
+        CL_TRY(dalloc((void**)&bad, 3 * sizeof(unsigned long long), s, "expand check"));
+        cudaMemsetAsync(bad, 0xFF, 3 * sizeof(unsigned long long), s);
         const int64_t n = n_members > n_he ? n_members : n_he;
-        k_expand_check<<<warp_grid((n + 31) / 32), kThreads, 0, s>>>(d_nodes, n_members, n_nodes, d_w, n_he, bad);
+        k_expand_check<<<warp_grid((n + 31) / 32), kThreads, 0, s>>>(d_ptr, d_nodes, n_members, n_nodes, d_w, n_he, bad);
         count_launches(1);
-        unsigned long long h[2];
+        unsigned long long h[3];
         Status rs = read_small(h, bad, sizeof h, s);
         dfree(bad, s);
         CL_TRY(rs);
         char buf[160];
+        if (h[2] != ~0ull) {
+            snprintf(buf, sizeof buf, "cleora_expand: he_ptr must start at 0 and be non-decreasing (hyperedge %llu)", h[2]);
+            return Status::make(2, buf);
+        }
         if (h[0] != ~0ull) {
             snprintf(buf, sizeof buf, "cleora_expand: member %llu: node id outside [0, n_nodes)", h[0]);
             return Status::make(3, buf);

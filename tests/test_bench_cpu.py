@@ -50,3 +50,38 @@ def test_e2e_schedule_by_memory():
     assert bench.e2e_schedule(14 * 10**9, 4.65 * 10**9, hbm) == "full"
     assert bench.e2e_schedule(110 * 10**9, 42.7 * 10**9, hbm) == "trim"
     assert bench.e2e_schedule(150 * 10**9, 42.7 * 10**9, hbm) is None
+
+
+def test_gpus_flag_launches_that_many_ranks():
+    """``bench.py --gpus 2`` without torchrun re-launches itself with 2 ranks (torch.distributed.run);
+    --dry-launch makes every rank print its rank / world and exit before any GPU work."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-launch"],
+                         capture_output=True, text=True, cwd=ROOT, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == [0, 1]
+    assert all(d["world"] == 2 and d["dry_launch"] for d in lines)
+
+
+def test_gpus_flag_must_match_world_size():
+    """Under a launcher, --gpus must equal WORLD_SIZE (a mismatch would mis-report n_gpus)."""
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-launch"],
+                         capture_output=True, text=True, cwd=ROOT, env=env, timeout=120)
+    assert out.returncode == 2 and "WORLD_SIZE=3" in out.stderr
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--dry-launch"],
+                         capture_output=True, text=True, cwd=ROOT, env=env, timeout=120)
+    assert out.returncode == 0 and json.loads(out.stdout.strip().splitlines()[-1])["world"] == 1
+
+
+def test_config_l2_statement_depends_on_size():
+    sys.path.insert(0, ROOT)
+    import bench
+    import gen
+    c1 = bench.config_dict(gen.config("c1"), 1)
+    assert "flushed" in c1["l2"] and "larger than L2" not in c1["l2"]
+    import numpy as np
+    g4 = gen.EdgeList("c4", 4847571, np.zeros(1, np.int32), np.zeros(1, np.int32), None, True, d=1024, iters=4)
+    assert "larger than L2" in bench.config_dict(g4, 1)["l2"]
