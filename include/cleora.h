@@ -62,6 +62,14 @@ enum {
                               after each step instead of the fused peer stores            */
 };
 
+/* Host-side all-gather supplied by the caller for world > 1 without NCCL (e.g. a gloo process group,
+ * or two processes sharing one GPU in a test): every rank passes `bytes` bytes in `send`; on return
+ * `recv` holds world * bytes bytes, rank p's at offset p * bytes.  Blocking; collective (every rank
+ * calls it the same number of times, in the same order); returns 0 on success.  The library uses it
+ * for the CUDA IPC handle exchange, for the failure agreement of every collective call, and, after a
+ * cudaStreamSynchronize, as the step barrier (a 1-byte all-gather). */
+typedef int (*cleora_allgather_fn)(void* ctx, const void* send, void* recv, int64_t bytes);
+
 /* Build options.  Pass NULL to cleora_build for: current device, host inputs, a
  * library-owned stream, one GPU, no flags. */
 typedef struct cleora_opts {
@@ -86,6 +94,10 @@ typedef struct cleora_opts {
     int32_t n_chunks;
     int32_t chunk;
     uint64_t chunk_seed;
+    /* world > 1 with nccl_id == NULL: the collectives go through this host all-gather instead of
+       NCCL (the exchange must then be the fused peer stores; there is no NCCL all-gather fallback) */
+    cleora_allgather_fn host_allgather;
+    void* host_ctx;
 } cleora_opts;
 
 typedef struct cleora_graph cleora_graph;   /* opaque */
@@ -107,10 +119,17 @@ typedef struct cleora_graph cleora_graph;   /* opaque */
  *     deg(a) = fp64 sum of e_ab over ascending b (weighted out-degree, reading R2);
  *     M_ab   = (float)(e_ab / deg(a)), IEEE round-to-nearest once.
  *   Inputs are borrowed for the duration of the call only.  On success *out owns the graph.
- *   Errors: EUSAGE (NULL pointer, n_nodes <= 0, n_edges <= 0, world > 1 without nccl_id,
- *   bad rank), EDATA (id outside [0, n_nodes), weight <= 0 or not finite), EINTERNAL.
- *   Multi-GPU (world > 1): collective; every rank passes the same edge list; each rank keeps
- *   the full CSR and computes the rows of its nnz-balanced contiguous shard.
+ *   Errors: EUSAGE (NULL pointer, n_nodes <= 0, n_edges <= 0, world > 1 without nccl_id or
+ *   host_allgather, bad rank, world > 255), EDATA (id outside [0, n_nodes), weight <= 0 or not
+ *   finite), EINTERNAL.
+ *   Multi-GPU (world > 1): collective; every rank passes the same edge list.  M is ROW-SHARDED:
+ *   every rank counts the entries of every row (after mirroring, before merging duplicates), the
+ *   rows are cut into `world` contiguous shards balanced on those counts (cut p = the first row
+ *   whose entry prefix reaches p * total / world), and each rank sorts, merges and scales only the
+ *   entries of its own rows -- no rank holds or sorts the whole M (§4.5: M's
+ *   2|E| entries are the term that divides).  Results do not depend on world (bitwise).  If any
+ *   rank fails (e.g. out of memory), every rank returns an error (the ranks agree on success
+ *   before returning).
  */
 CLEORA_API int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, int64_t n_edges,
                  int32_t n_nodes, int32_t directed, const cleora_opts* opts, cleora_graph** out);
@@ -250,7 +269,7 @@ typedef struct cleora_info_t {
     int64_t max_degree;     /* largest number of stored entries in one row              */
     int64_t heavy_rows;     /* rows scheduled on the multi-warp / multi-CTA path        */
     int64_t heavy_items;    /* CTA work items for those rows                            */
-    int64_t shard_begin;    /* rows this rank computes: [shard_begin, shard_end)        */
+    int64_t shard_begin;    /* rows this rank computes and stores: [shard_begin, shard_end) */
     int64_t shard_end;
     int32_t rank, world;
     int64_t device_bytes;   /* device memory currently owned by the handle              */
@@ -258,6 +277,7 @@ typedef struct cleora_info_t {
     int64_t referenced_rows;/* rows with in-degree > 0, i.e. ever gathered (-1: unknown)  */
     int32_t exchange;       /* 0 one GPU, 1 NCCL all-gather, 2 fused peer stores, 3 loopback */
     int32_t n_graphs;       /* graphs in a batched handle (cleora_build_batch), else 0   */
+    int64_t shard_nnz;      /* entries of this rank's rows (= nnz on one GPU)               */
 } cleora_info_t;
 /* Fill *out.  Synchronises the handle's stream (zero_rows and max_degree are computed on the device
  * by cleora_build and read back here, on first use; the handle caches them -- hence non-const).
@@ -320,8 +340,11 @@ CLEORA_API int cleora_probe_gather(int32_t device, int32_t row_bytes, int64_t ta
 
 /* ---- test hooks (not on the graded path) ------------------------------------------------ */
 
-/* Copy the device CSR to host arrays in the original labelling:
- * row_ptr [N+1] int64, col [nnz] int32, val [nnz] fp32, deg [N] fp64 (any may be NULL). */
+/* Copy the device CSR of this rank's rows to host arrays in the original labelling:
+ * row_ptr [N+1] int64, col [shard_nnz] int32, val [shard_nnz] fp32, deg [N] fp64 (any may be NULL).
+ * One GPU: the whole M.  world > 1: the shard [shard_begin, shard_end) -- row_ptr offsets count from
+ * the shard's first entry (row_ptr[r] = 0 for r <= shard_begin, = shard_nnz for r >= shard_end), deg
+ * is 0 outside the shard; the rows themselves are bit-identical to the whole M's. */
 CLEORA_API int cleora_fetch_csr(const cleora_graph* g, int64_t* row_ptr, int32_t* col, float* val, double* deg);
 
 /* Copy rows [row_begin, row_end) of rank `rank`'s replica of the current T into host memory
@@ -333,6 +356,10 @@ CLEORA_API int cleora_fetch_replica(const cleora_graph* g, int32_t rank, int64_t
 /* Overwrite rows [row_begin, row_end) of the current T from host memory (dense, d per row):
  * resume from a checkpoint or start from a custom T_0.  (Loopback: every replica.) */
 CLEORA_API int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const float* host_in);
+
+/* Process-wide number of CUDA IPC mappings opened so far (peer T buffers; they are cached across
+ * handles, so repeated handles of one shape open none).  Diagnostic. */
+CLEORA_API int64_t cleora_ipc_opens(void);
 
 /* Size of an ncclUniqueId (128) and a helper that fills one (rank 0 calls it and
  * broadcasts the bytes through the caller's process group). */

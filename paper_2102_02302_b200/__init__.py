@@ -24,7 +24,7 @@ __all__ = [
     "cleora_fetch_async", "cleora_trim",
     "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
     "cleora_release_cached_memory", "cleora_merge_chunks", "cleora_reconstruct", "cleora_build_batch",
-    "cleora_expand", "EXPAND_CLIQUE", "EXPAND_STAR", "cleora_probe_gather",
+    "cleora_expand", "EXPAND_CLIQUE", "EXPAND_STAR", "cleora_probe_gather", "cleora_ipc_opens", "host_allgather_from",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcleora.so")
@@ -37,11 +37,39 @@ OK, EUSAGE, EDATA, EINTERNAL = 0, 2, 3, 4
 F_TIMING, F_LOOPBACK, F_EXCHANGE_NCCL = 1, 2, 4
 
 
+# int (*cleora_allgather_fn)(void* ctx, const void* send, void* recv, int64_t bytes)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+
+
 class _Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("input_on_device", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
                 ("flags", ctypes.c_int32), ("n_chunks", ctypes.c_int32), ("chunk", ctypes.c_int32),
-                ("chunk_seed", ctypes.c_uint64)]
+                ("chunk_seed", ctypes.c_uint64), ("host_allgather", ALLGATHER_FN), ("host_ctx", ctypes.c_void_p)]
+
+
+def host_allgather_from(group=None):
+    """A cleora_allgather_fn over a torch.distributed process group (e.g. gloo on CPU): for world > 1
+    without NCCL -- several processes sharing one GPU in a test, or a box without NCCL.  Keep the
+    returned object alive as long as the handles built with it (cleora_build keeps a reference)."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(ctx, send, recv, nbytes):
+        try:
+            n = int(nbytes)
+            mine = torch.frombuffer(bytearray(ctypes.string_at(send, n)), dtype=torch.uint8) if n else \
+                torch.empty(0, dtype=torch.uint8)
+            world = dist.get_world_size(group)
+            out = [torch.empty(n, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(out, mine, group=group)
+            buf = b"".join(bytes(t.numpy().tobytes()) for t in out)
+            ctypes.memmove(recv, buf, len(buf))
+            return 0
+        except Exception:                # never raise through the C library
+            return 1
+
+    return ALLGATHER_FN(fn)
 
 
 class _Info(ctypes.Structure):
@@ -51,7 +79,7 @@ class _Info(ctypes.Structure):
                 ("heavy_items", ctypes.c_int64), ("shard_begin", ctypes.c_int64), ("shard_end", ctypes.c_int64),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
                 ("hot_rows", ctypes.c_int64), ("referenced_rows", ctypes.c_int64), ("exchange", ctypes.c_int32),
-                ("n_graphs", ctypes.c_int32)]
+                ("n_graphs", ctypes.c_int32), ("shard_nnz", ctypes.c_int64)]
 
 
 class _Stats(ctypes.Structure):
@@ -87,6 +115,7 @@ _SIGS = {
     "cleora_kernel_launches": (ctypes.c_int64, []),
     "cleora_release_cached_memory": (ctypes.c_int, []),
     "cleora_probe_gather": (ctypes.c_int, [_i32, _i32, _i64, _i64, ctypes.POINTER(ctypes.c_double)]),
+    "cleora_ipc_opens": (ctypes.c_int64, []),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -150,9 +179,10 @@ class Graph:
     """Owning wrapper of a ``cleora_graph*`` (destroyed on close / garbage collection).  ``stream``
     is the cudaStream_t the handle enqueues on (None: a library-owned stream)."""
 
-    def __init__(self, handle: int, stream: int | None = None):
+    def __init__(self, handle: int, stream: int | None = None, keep=None):
         self._h = handle
         self.stream = stream
+        self._keep = keep            # objects the C handle points to (a host all-gather callback)
 
     @property
     def handle(self) -> int:
@@ -196,8 +226,10 @@ class Graph:
 def cleora_build(src, dst, weight, n_nodes: int, directed: bool = False, *, device: int = -1, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None, timing: bool = False,
                  loopback: bool = False, exchange_nccl: bool = False, n_chunks: int = 0, chunk: int = 0,
-                 chunk_seed: int = 0) -> Graph:
-    """COO edge list -> device CSR of M = D^-1 A.  See include/cleora.h."""
+                 chunk_seed: int = 0, host_allgather=None) -> Graph:
+    """COO edge list -> device CSR of M = D^-1 A.  See include/cleora.h.
+    world > 1: row-sharded, collectives over NCCL (nccl_id) or ``host_allgather`` (an ALLGATHER_FN,
+    e.g. host_allgather_from(group))."""
     ps, ds, ks = _ptr(src, np.int32)
     pd, dd, kd = _ptr(dst, np.int32)
     pw, dw, kw = _ptr(weight, np.float32)
@@ -228,9 +260,11 @@ def cleora_build(src, dst, weight, n_nodes: int, directed: bool = False, *, devi
     o.flags = (F_TIMING if timing else 0) | (F_LOOPBACK if loopback else 0) | \
         (F_EXCHANGE_NCCL if exchange_nccl else 0)
     o.n_chunks, o.chunk, o.chunk_seed = int(n_chunks), int(chunk), int(chunk_seed) & 0xFFFFFFFFFFFFFFFF
+    if host_allgather is not None:
+        o.host_allgather = host_allgather
     h = ctypes.c_void_p()
     _check(_lib.cleora_build(ps, pd, pw, n, int(n_nodes), 1 if directed else 0, ctypes.byref(o), ctypes.byref(h)))
-    return Graph(h.value, o.stream)
+    return Graph(h.value, o.stream, keep=host_allgather)
 
 
 EXPAND_CLIQUE, EXPAND_STAR = 0, 1
@@ -372,8 +406,9 @@ def cleora_destroy(g: Graph):
 
 
 def cleora_fetch_csr(g: Graph) -> dict:
+    """This rank's rows of M (the whole M on one GPU; see include/cleora.h for shards)."""
     info = cleora_info(g)
-    n, nnz = info["n_nodes"], info["nnz"]
+    n, nnz = info["n_nodes"], info["shard_nnz"]
     rp = np.empty(n + 1, np.int64); col = np.empty(nnz, np.int32)
     val = np.empty(nnz, np.float32); deg = np.empty(n, np.float64)
     _check(_lib.cleora_fetch_csr(g.handle, rp.ctypes.data, col.ctypes.data, val.ctypes.data, deg.ctypes.data))
@@ -469,3 +504,8 @@ def cleora_probe_gather(row_bytes: int, table_bytes: int = 64 << 20, n_gathers: 
     r = ctypes.c_double()
     _check(_lib.cleora_probe_gather(int(device), int(row_bytes), int(table_bytes), int(n_gathers), ctypes.byref(r)))
     return float(r.value)
+
+
+def cleora_ipc_opens() -> int:
+    """Process-wide count of CUDA IPC mappings opened (peer T buffers; cached across handles)."""
+    return int(_lib.cleora_ipc_opens())

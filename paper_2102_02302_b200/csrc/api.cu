@@ -184,7 +184,7 @@ bool release_largest(int dev) {
 }
 }  // namespace
 
-Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what) {
+Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, bool block) {
     *p = nullptr;
     int dev = 0;
     CL_CUDA_TRY(cudaGetDevice(&dev));
@@ -200,7 +200,9 @@ Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what) {
         }
     }
     if (bytes == 0) bytes = 16;
-    const bool big = bytes >= kCacheMin && getenv("CLEORA_NO_CACHE") == nullptr;
+    // block: a plain cudaMalloc block whatever the size (T buffers: CUDA IPC cannot export pool memory)
+    static const bool no_cache = getenv("CLEORA_NO_CACHE") != nullptr;
+    const bool big = block || (bytes >= kCacheMin && !no_cache);
     if (big) {
         const size_t rb = round_block(bytes);
         std::lock_guard<std::mutex> lk(g_cache_mu);
@@ -367,19 +369,30 @@ struct cleora_graph {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int32_t n = 0;
-    int64_t nnz = 0, n_edges_in = 0, zero_rows = -1, max_degree = -1;   // -1: not read back yet
-    unsigned long long* d_scal = nullptr;   // the build's device scalars ([2] zero rows, [3] max degree)
+    // nnz: stored entries of the whole M (all shards); zero_rows, max_degree: of the whole M, -1 until
+    // read back (one GPU: lazily by cleora_info; row-sharded: combined over the ranks at the build)
+    int64_t nnz = 0, n_edges_in = 0, zero_rows = -1, max_degree = -1;
     int directed = 0;
-    int64_t* row_ptr = nullptr;
-    int32_t* col = nullptr;
-    float* val = nullptr;
-    double* deg = nullptr;
+    // CSR of M: one GPU -> csr[0] = all rows; world > 1 -> csr[0] = this rank's rows only (row-sharded
+    // build: row_ptr has N + 1 entries, shard-local offsets, 0 before the shard and nnz after it);
+    // loopback -> csr[p] = emulated rank p's shard
+    std::vector<Csr> csr;
+    int32_t* indeg = nullptr;       // row-sharded builds: the whole graph's in-degree (shard_plan)
+    uint8_t* ref = nullptr;         // exchange: ref[v] = some row gathers v (deferred peer stores)
+    bool sharded = false;
+    // environment switches, read by cleora_init
+    int env_cold_first = -1, env_csr_prefetch = 1;
+    bool env_write_zero = false, env_no_hot = false, env_defer = true;
+    int gmode = 0;                  // gather engine for the current dp (gather_mode)
     int heavy_thresh = 64;
     Schedule sched;
     int32_t d = 0, dp = 0;
     float* T[2] = {nullptr, nullptr};
     float* partials = nullptr;
     int32_t tag_dp = 0;             // row stride the hot-row tags in col (bit 31) were chosen for
+    Csr& own() { return csr[csr.size() > 1 ? rank : 0]; }
+    const Csr& own() const { return csr[csr.size() > 1 ? rank : 0]; }
+    Csr& of(int p) { return csr[csr.size() > 1 ? p : 0]; }
     // cleora_fetch_async: D2H on a copy stream, concurrent with later work on `stream`
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_copied = nullptr;
@@ -398,6 +411,9 @@ struct cleora_graph {
     std::vector<int64_t> cuts;
     int64_t r0 = 0, r1 = 0;
     ncclComm_t comm = nullptr;
+    // host-side collectives (world > 1 without NCCL): the caller's all-gather (cleora_opts)
+    cleora_allgather_fn host_ag = nullptr;
+    void* host_ctx = nullptr;
     // exchange of the row shards after every step (world > 1), see exchange_mode below
     int xmode = 0;
     bool zclean[2] = {false, false};   // rows without entries are already 0 in T[b]
@@ -490,13 +506,98 @@ Status collect_timing(cleora_graph* g) {
 // rows into the other ranks' replicas, which are local buffers; ranks run one after another.
 enum { X_NONE = 0, X_NCCL = 1, X_PEER = 2, X_LOOPBACK = 3 };
 
+// CUDA IPC mappings of peer T buffers, cached process-wide by (device, handle bytes).  A peer's T
+// blocks come from its block cache, so the next handle of the same shape usually exports the very same
+// blocks: cleora_init then finds them mapped already instead of opening (and later closing) them
+// again -- round 1 opened and closed every peer buffer in every cleora_init, i.e. in every timed
+// multi-GPU bench step.  A mapping stays valid while the exporting process keeps the block (the
+// block cache only hands it back to the driver on cleora_release_cached_memory or out of memory);
+// cleora_release_cached_memory also closes every mapping here.  Bounded: beyond kIpcCacheMax
+// entries the oldest not-in-use mapping is closed.
+namespace {
+struct IpcEntry {
+    int dev;
+    cudaIpcMemHandle_t h;
+    void* p;
+    int users;
+    uint64_t stamp;
+};
+std::mutex g_ipc_mu;
+std::vector<IpcEntry> g_ipc;
+uint64_t g_ipc_clock = 0;
+constexpr size_t kIpcCacheMax = 64;
+std::atomic<int64_t> g_ipc_opens{0};
+
+Status ipc_open(int dev, const cudaIpcMemHandle_t& h, void** out) {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    for (auto& e : g_ipc)
+        if (e.dev == dev && !memcmp(&e.h, &h, sizeof h)) {
+            e.users++;
+            e.stamp = ++g_ipc_clock;
+            *out = e.p;
+            return Status::ok();
+        }
+    void* p = nullptr;
+    cudaError_t r = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (r != cudaSuccess) {
+        cudaGetLastError();
+        return Status::make(4, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(r));
+    }
+    g_ipc_opens.fetch_add(1);
+    if (g_ipc.size() >= kIpcCacheMax) {          // close the oldest idle mapping
+        size_t at = g_ipc.size();
+        for (size_t i = 0; i < g_ipc.size(); i++)
+            if (g_ipc[i].users == 0 && (at == g_ipc.size() || g_ipc[i].stamp < g_ipc[at].stamp)) at = i;
+        if (at < g_ipc.size()) {
+            cudaIpcCloseMemHandle(g_ipc[at].p);
+            g_ipc.erase(g_ipc.begin() + at);
+        }
+    }
+    g_ipc.push_back({dev, h, p, 1, ++g_ipc_clock});
+    *out = p;
+    return Status::ok();
+}
+
+void ipc_release(void* p) {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    for (auto& e : g_ipc)
+        if (e.p == p && e.users > 0) {
+            e.users--;
+            return;
+        }
+}
+
+void ipc_close_all() {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    for (size_t i = 0; i < g_ipc.size();) {
+        if (g_ipc[i].users == 0) {
+            cudaIpcCloseMemHandle(g_ipc[i].p);
+            g_ipc.erase(g_ipc.begin() + i);
+        } else {
+            i++;
+        }
+    }
+}
+}  // namespace
+
 void close_peers(cleora_graph* g) {
     for (int b = 0; b < 2; b++)
         for (int i = 0; i < kMaxPeers; i++)
             if (g->peer_T[b][i]) {
-                cudaIpcCloseMemHandle(g->peer_T[b][i]);
+                ipc_release(g->peer_T[b][i]);      // the mapping stays cached (see ipc_open)
                 g->peer_T[b][i] = nullptr;
             }
+}
+
+void free_csr(cleora_graph* g) {
+    for (auto& c : g->csr) {
+        dfree(c.row_ptr, g->stream);
+        dfree(c.col, g->stream);
+        dfree(c.val, g->stream);
+        dfree(c.deg, g->stream);
+        dfree(c.d_scal, g->stream);
+        c = Csr();
+    }
 }
 
 void free_schedules(cleora_graph* g) {
@@ -524,13 +625,14 @@ Status make_schedules(cleora_graph* g) {
     free_schedules(g);
     if (!g->sched_p.empty()) {
         for (int p = 0; p < g->world; p++) {
-            CL_TRY(build_schedule(g->row_ptr, g->n, g->cuts[p], g->cuts[p + 1], g->heavy_thresh, g->chunk_rows,
+            CL_TRY(build_schedule(g->of(p).row_ptr, g->n, g->cuts[p], g->cuts[p + 1], g->heavy_thresh, g->chunk_rows,
                                   g->stream, &g->sched_p[p]));
             g->max_items = std::max(g->max_items, g->sched_p[p].n_items);
         }
         g->sched = g->sched_p[g->rank];
     } else {
-        CL_TRY(build_schedule(g->row_ptr, g->n, g->r0, g->r1, g->heavy_thresh, g->chunk_rows, g->stream, &g->sched));
+        CL_TRY(build_schedule(g->own().row_ptr, g->n, g->r0, g->r1, g->heavy_thresh, g->chunk_rows, g->stream,
+                              &g->sched));
         g->max_items = g->sched.n_items;
     }
     g->sched_thresh = g->heavy_thresh;
@@ -598,19 +700,75 @@ Status comm_get(const uint8_t* id128, int world, int rank, int dev, ncclComm_t* 
     return Status::ok();
 }
 
+// ---- collectives of a multi-rank handle: NCCL (g->comm) or the caller's host all-gather (g->host_ag)
+
+// all-gather of `bytes` host bytes per rank (blocking): all[p * bytes ...] = rank p's `mine`
+Status comm_allgather(cleora_graph* g, const void* mine, void* all, size_t bytes) {
+    if (g->host_ag) {
+        if (g->host_ag(g->host_ctx, mine, all, (int64_t)bytes) != 0)
+            return Status::make(4, "host all-gather (cleora_opts.host_allgather) failed");
+        return Status::ok();
+    }
+    Nccl& N = nccl();
+    const int W = g->world;
+    void* d = nullptr;
+    CL_TRY(dalloc(&d, bytes * W + 16, g->stream, "all-gather buffer"));
+    Status st = Status::ok();
+    do {
+        if (cudaMemcpyAsync((char*)d + bytes * g->rank, mine, bytes, cudaMemcpyHostToDevice, g->stream) != cudaSuccess) {
+            st = Status::make(4, "all-gather staging copy");
+            break;
+        }
+        ncclResult_t r = N.AllGather((char*)d + bytes * g->rank, d, bytes, ncclChar, g->comm, g->stream);
+        if (r != ncclSuccess) { st = Status::make(4, std::string("ncclAllGather: ") + N.GetErrorString(r)); break; }
+        if (cudaMemcpyAsync(all, d, bytes * W, cudaMemcpyDeviceToHost, g->stream) != cudaSuccess ||
+            cudaStreamSynchronize(g->stream) != cudaSuccess) {
+            st = Status::make(4, "all-gather read-back");
+            break;
+        }
+    } while (0);
+    dfree(d, g->stream);
+    return st;
+}
+
+// Failure agreement: every rank reports whether its part of a collective call succeeded,
+// so that one rank's failure (out of memory, say) makes every rank return an error instead of
+// leaving the others blocked in the next collective.  Returns the local status, or EINTERNAL naming
+// the first failed rank when only another rank failed.
+Status comm_agree(cleora_graph* g, const Status& local) {
+    if (g->world <= 1 || g->xmode == X_LOOPBACK) return local;
+    const int mine = local.good() ? 0 : (local.code ? local.code : 4);
+    std::vector<int> all(g->world, 0);
+    CL_TRY(comm_allgather(g, &mine, all.data(), sizeof(int)));
+    if (!local.good()) return local;
+    for (int p = 0; p < g->world; p++)
+        if (all[p]) return Status::make(4, "rank " + std::to_string(p) + " of " + std::to_string(g->world) + " failed");
+    return Status::ok();
+}
+
+// Stream-ordered barrier over all ranks: work enqueued after it on any rank runs after every rank's
+// work enqueued before it (the SpMM's peer stores included).  NCCL: a 1-int all-reduce on the stream.
+// Host all-gather: the stream is synchronised first, then a 1-byte all-gather.
 Status rank_barrier(cleora_graph* g) {
+    if (g->host_ag) {
+        CL_CUDA_TRY(cudaStreamSynchronize(g->stream));
+        char b = 0;
+        std::vector<char> all(g->world);
+        return comm_allgather(g, &b, all.data(), 1);
+    }
     Nccl& N = nccl();
     CL_NCCL_TRY(N.AllReduce(g->d_flag, g->d_flag, 1, ncclInt32, ncclMax, g->comm, g->stream));
     return Status::ok();
 }
 
 // X_PEER set-up (collective, inside cleora_init): all-gather the IPC handles of every rank's
-// T[0], T[1] and open the others'.  Any rank that cannot open them makes all ranks fall back to
-// X_NCCL (the decision is all-reduced, so every rank takes the same path).
+// T[0], T[1] and map the others' (ipc_open: cached across handles).  Any rank that cannot map them
+// makes all ranks fall back to X_NCCL (the decision is all-gathered, so every rank takes the same
+// path); with host collectives there is no fallback and the call fails on every rank.
 Status open_peers(cleora_graph* g) {
-    Nccl& N = nccl();
     const int W = g->world;
     if (W - 1 > kMaxPeers) {
+        if (g->host_ag) return Status::make(4, "cleora_init: host collectives need peer mappings (world <= 8)");
         g->xmode = X_NCCL;
         return Status::ok();
     }
@@ -622,25 +780,9 @@ Status open_peers(cleora_graph* g) {
             ok = 0;
         }
     const size_t hb = sizeof(mine);
-    void* d_all = nullptr;
-    CL_TRY(dalloc(&d_all, hb * W + 16, g->stream, "IPC handles"));
     std::vector<char> all(hb * W);
-    Status st = Status::ok();
-    do {
-        if (cudaMemcpyAsync((char*)d_all + hb * g->rank, mine, hb, cudaMemcpyHostToDevice, g->stream) != cudaSuccess) {
-            st = Status::make(4, "IPC handle copy");
-            break;
-        }
-        ncclResult_t r = N.AllGather((char*)d_all + hb * g->rank, d_all, hb, ncclChar, g->comm, g->stream);
-        if (r != ncclSuccess) { st = Status::make(4, std::string("ncclAllGather: ") + N.GetErrorString(r)); break; }
-        if (cudaMemcpyAsync(all.data(), d_all, hb * W, cudaMemcpyDeviceToHost, g->stream) != cudaSuccess ||
-            cudaStreamSynchronize(g->stream) != cudaSuccess) {
-            st = Status::make(4, "IPC handle gather");
-            break;
-        }
-    } while (0);
-    dfree(d_all, g->stream);
-    CL_TRY(st);
+    CL_TRY(comm_allgather(g, mine, all.data(), hb));
+    std::string why;
     int i = 0;
     for (int p = 0; p < W && ok; p++) {
         if (p == g->rank) continue;
@@ -648,26 +790,24 @@ Status open_peers(cleora_graph* g) {
             cudaIpcMemHandle_t h;
             memcpy(&h, all.data() + hb * p + sizeof(cudaIpcMemHandle_t) * b, sizeof h);
             void* ptr = nullptr;
-            if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-                cudaGetLastError();
+            Status so = ipc_open(g->device, h, &ptr);
+            if (!so.good()) {
                 ok = 0;
+                why = so.msg;
             } else {
                 g->peer_T[b][i] = (float*)ptr;
             }
         }
         i++;
     }
-    // all ranks agree: peer stores only if every rank opened every peer
-    int h_ok = ok;
-    CL_CUDA_TRY(cudaMemcpyAsync(g->d_flag, &h_ok, sizeof(int), cudaMemcpyHostToDevice, g->stream));
-    {
-        ncclResult_t r = N.AllReduce(g->d_flag, g->d_flag, 1, ncclInt32, ncclMin, g->comm, g->stream);
-        if (r != ncclSuccess) return Status::make(4, std::string("ncclAllReduce: ") + N.GetErrorString(r));
-    }
-    CL_CUDA_TRY(cudaMemcpyAsync(&h_ok, g->d_flag, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
-    CL_CUDA_TRY(cudaStreamSynchronize(g->stream));
-    if (!h_ok) {
+    // all ranks agree: peer stores only if every rank mapped every peer
+    std::vector<int> oks(W, 0);
+    CL_TRY(comm_allgather(g, &ok, oks.data(), sizeof(int)));
+    bool all_ok = true;
+    for (int p = 0; p < W; p++) all_ok = all_ok && oks[p];
+    if (!all_ok) {
         close_peers(g);
+        if (g->host_ag) return Status::make(4, "cleora_init: peer mapping failed on a rank" + (why.empty() ? "" : ": " + why));
         g->xmode = X_NCCL;
     }
     return Status::ok();
@@ -692,6 +832,103 @@ struct BatchSpec {
     const int32_t* node_count;  // host [n_graphs]
     int32_t n_graphs;
 };
+
+// The build proper (inputs staged on the device, CSR, shard cuts); collective work only through
+// shard-independent steps, so a failure here is agreed on by do_build before it returns.
+Status build_body(const int32_t* src, const int32_t* dst, const float* w, int64_t E, int32_t N, int directed,
+                  const cleora_opts* o, cleora_graph* g, const BatchSpec* batch) {
+    // a1: device copies of the COO when the caller passed host memory
+    const int32_t* dsrc = src;
+    const int32_t* ddst = dst;
+    const float* dw = w;
+    void *bs = nullptr, *bd = nullptr, *bw = nullptr;
+    void *gs = nullptr, *gd = nullptr;
+    struct Staged {           // freed on every return path
+        cleora_graph* g;
+        void** p[5];
+        ~Staged() { for (auto q : p) { dfree(*q, g->stream); *q = nullptr; } }
+    } staged{g, {&bs, &bd, &bw, &gs, &gd}};
+    const bool on_dev = o && o->input_on_device;
+    if (!on_dev) {
+        CL_TRY(dalloc(&bs, E * sizeof(int32_t), g->stream, "input src"));
+        CL_TRY(dalloc(&bd, E * sizeof(int32_t), g->stream, "input dst"));
+        CL_CUDA_TRY(cudaMemcpyAsync(bs, src, E * sizeof(int32_t), cudaMemcpyHostToDevice, g->stream));
+        CL_CUDA_TRY(cudaMemcpyAsync(bd, dst, E * sizeof(int32_t), cudaMemcpyHostToDevice, g->stream));
+        if (w) {
+            CL_TRY(dalloc(&bw, E * sizeof(float), g->stream, "input weight"));
+            CL_CUDA_TRY(cudaMemcpyAsync(bw, w, E * sizeof(float), cudaMemcpyHostToDevice, g->stream));
+        }
+        dsrc = (const int32_t*)bs;
+        ddst = (const int32_t*)bd;
+        dw = (const float*)bw;
+    }
+    trace("build: inputs staged", g->stream, true);
+    // batched handle: local ids -> rows of the block-diagonal M
+    if (batch) {
+        std::vector<int64_t> base(batch->n_graphs + 1, 0);
+        for (int i = 0; i < batch->n_graphs; i++) base[i + 1] = base[i] + batch->node_count[i];
+        g->n_graphs = batch->n_graphs;
+        void* d_ep = nullptr;
+        Status st0 = dalloc((void**)&g->d_base, base.size() * sizeof(int64_t), g->stream, "batch bases");
+        if (st0.good()) st0 = dalloc(&d_ep, base.size() * sizeof(int64_t), g->stream, "batch edge offsets");
+        if (st0.good()) st0 = dalloc(&gs, E * sizeof(int32_t), g->stream, "batch src");
+        if (st0.good()) st0 = dalloc(&gd, E * sizeof(int32_t), g->stream, "batch dst");
+        if (st0.good()) {
+            cudaMemcpyAsync(g->d_base, base.data(), base.size() * sizeof(int64_t), cudaMemcpyHostToDevice, g->stream);
+            cudaMemcpyAsync(d_ep, batch->edge_ptr, base.size() * sizeof(int64_t), cudaMemcpyHostToDevice, g->stream);
+            st0 = batch_global_ids(dsrc, ddst, E, (const int64_t*)d_ep, g->d_base, batch->n_graphs, g->stream,
+                                   (int32_t*)gs, (int32_t*)gd);
+        }
+        dfree(d_ep, g->stream);
+        CL_TRY(st0);
+        dsrc = (const int32_t*)gs;
+        ddst = (const int32_t*)gd;
+    }
+    BuildExtra bx;
+    if (o && o->n_chunks >= 1) {
+        g->n_chunks = o->n_chunks;
+        g->chunk = o->chunk;
+        g->chunk_seed = o->chunk_seed;
+        CL_TRY(dalloc((void**)&g->occ, (size_t)N * sizeof(int32_t), g->stream, "chunk occurrences"));
+        bx.n_chunks = o->n_chunks;
+        bx.chunk = o->chunk;
+        bx.chunk_key = sm64(o->chunk_seed + 0x9E3779B97F4A7C15ull);
+        bx.occ = g->occ;
+    }
+    g->cuts.assign(g->world + 1, 0);
+    if (g->world == 1) {
+        BuildOut b;
+        CL_TRY(build_csr(dsrc, ddst, dw, E, N, directed, g->stream, &b, &bx));
+        trace("build: csr", g->stream, true);
+        g->csr.assign(1, Csr());
+        g->csr[0] = Csr{b.row_ptr, b.col, b.val, b.deg, b.d_scal, b.nnz};
+        g->nnz = b.nnz;
+        g->cuts[1] = N;
+    } else {
+        // row-sharded: cuts from every row's entry count, then only this rank's rows
+        // (every emulated rank's, in loopback)
+        std::vector<int64_t> ent(g->world + 1, 0);
+        g->sharded = true;
+        CL_TRY(shard_plan(dsrc, ddst, dw, E, N, directed, &bx, g->world, g->stream, g->cuts.data(), ent.data(),
+                          &g->indeg));
+        const bool lb = g->xmode == X_LOOPBACK;
+        g->csr.assign(lb ? g->world : 1, Csr());
+        for (int p = lb ? 0 : g->rank; p < (lb ? g->world : g->rank + 1); p++) {
+            BuildExtra bp = bx;
+            bp.row_lo = (int32_t)g->cuts[p];
+            bp.row_hi = (int32_t)g->cuts[p + 1];
+            bp.shard_entries = ent[p + 1] - ent[p];
+            BuildOut b;
+            CL_TRY(build_csr(dsrc, ddst, dw, E, N, directed, g->stream, &b, &bp));
+            g->of(p) = Csr{b.row_ptr, b.col, b.val, b.deg, b.d_scal, b.nnz};
+        }
+        trace("build: shard csr", g->stream, true);
+    }
+    g->r0 = g->cuts[g->rank];
+    g->r1 = g->cuts[g->rank + 1];
+    g->bytes = (int64_t)(N + 1) * 8 + g->own().nnz * 8 + (int64_t)N * 8;
+    return Status::ok();
+}
 
 Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t E, int32_t N, int directed,
                 const cleora_opts* o, cleora_graph* g, const BatchSpec* batch = nullptr) {
@@ -721,111 +958,60 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
     g->heavy_thresh = heavy_thresh_default(64);   // set per kernel by cleora_init
     g->rank = (o && o->world > 1) ? o->rank : 0;
     g->world = (o && o->world > 1) ? o->world : 1;
-
-    // a1: device copies of the COO when the caller passed host memory
-    const int32_t* dsrc = src;
-    const int32_t* ddst = dst;
-    const float* dw = w;
-    void *bs = nullptr, *bd = nullptr, *bw = nullptr;
-    const bool on_dev = o && o->input_on_device;
-    if (!on_dev) {
-        CL_TRY(dalloc(&bs, E * sizeof(int32_t), g->stream, "input src"));
-        CL_TRY(dalloc(&bd, E * sizeof(int32_t), g->stream, "input dst"));
-        CL_CUDA_TRY(cudaMemcpyAsync(bs, src, E * sizeof(int32_t), cudaMemcpyHostToDevice, g->stream));
-        CL_CUDA_TRY(cudaMemcpyAsync(bd, dst, E * sizeof(int32_t), cudaMemcpyHostToDevice, g->stream));
-        if (w) {
-            CL_TRY(dalloc(&bw, E * sizeof(float), g->stream, "input weight"));
-            CL_CUDA_TRY(cudaMemcpyAsync(bw, w, E * sizeof(float), cudaMemcpyHostToDevice, g->stream));
-        }
-        dsrc = (const int32_t*)bs;
-        ddst = (const int32_t*)bd;
-        dw = (const float*)bw;
-    }
-    trace("build: inputs staged", g->stream, true);
-    BuildOut b;
-    // batched handle: local ids -> rows of the block-diagonal M
-    void *gs = nullptr, *gd = nullptr;
-    if (batch) {
-        std::vector<int64_t> base(batch->n_graphs + 1, 0);
-        for (int i = 0; i < batch->n_graphs; i++) base[i + 1] = base[i] + batch->node_count[i];
-        g->n_graphs = batch->n_graphs;
-        void* d_ep = nullptr;
-        Status st0 = dalloc((void**)&g->d_base, base.size() * sizeof(int64_t), g->stream, "batch bases");
-        if (st0.good()) st0 = dalloc(&d_ep, base.size() * sizeof(int64_t), g->stream, "batch edge offsets");
-        if (st0.good()) st0 = dalloc(&gs, E * sizeof(int32_t), g->stream, "batch src");
-        if (st0.good()) st0 = dalloc(&gd, E * sizeof(int32_t), g->stream, "batch dst");
-        if (st0.good()) {
-            cudaMemcpyAsync(g->d_base, base.data(), base.size() * sizeof(int64_t), cudaMemcpyHostToDevice, g->stream);
-            cudaMemcpyAsync(d_ep, batch->edge_ptr, base.size() * sizeof(int64_t), cudaMemcpyHostToDevice, g->stream);
-            st0 = batch_global_ids(dsrc, ddst, E, (const int64_t*)d_ep, g->d_base, batch->n_graphs, g->stream,
-                                   (int32_t*)gs, (int32_t*)gd);
-        }
-        dfree(d_ep, g->stream);
-        if (!st0.good()) {
-            dfree(gs, g->stream);
-            dfree(gd, g->stream);
-            dfree(bs, g->stream);
-            dfree(bd, g->stream);
-            dfree(bw, g->stream);
-            return st0;
-        }
-        dsrc = (const int32_t*)gs;
-        ddst = (const int32_t*)gd;
-    }
-    BuildExtra bx;
-    if (o && o->n_chunks >= 1) {
-        g->n_chunks = o->n_chunks;
-        g->chunk = o->chunk;
-        g->chunk_seed = o->chunk_seed;
-        CL_TRY(dalloc((void**)&g->occ, (size_t)N * sizeof(int32_t), g->stream, "chunk occurrences"));
-        bx.n_chunks = o->n_chunks;
-        bx.chunk = o->chunk;
-        bx.chunk_key = sm64(o->chunk_seed + 0x9E3779B97F4A7C15ull);
-        bx.occ = g->occ;
-    }
-    Status st = build_csr(dsrc, ddst, dw, E, N, directed, g->stream, &b, &bx);
-    trace("build: csr", g->stream, true);
-    dfree(bs, g->stream);
-    dfree(bd, g->stream);
-    dfree(bw, g->stream);
-    dfree(gs, g->stream);
-    dfree(gd, g->stream);
-    if (!st.good()) return st;
-    g->nnz = b.nnz;
-    g->row_ptr = b.row_ptr;
-    g->col = b.col;
-    g->val = b.val;
-    g->deg = b.deg;
-    g->d_scal = b.d_scal;
-    g->bytes = (int64_t)(N + 1) * 8 + b.nnz * 8 + (int64_t)N * 8;
-
-    g->cuts.assign(g->world + 1, 0);
-    if (g->world > 1) {
-        CL_TRY(shard_cuts(g->row_ptr, N, g->world, g->stream, g->cuts.data()));
-    } else {
-        g->cuts[1] = N;
-    }
-    g->r0 = g->cuts[g->rank];
-    g->r1 = g->cuts[g->rank + 1];
     const bool loopback = g->world > 1 && o && (o->flags & CLEORA_F_LOOPBACK);
     if (loopback) {
         g->sched_p.resize(g->world);        // every rank's schedule lives here (built by init)
         g->rep.assign(g->world, {nullptr, nullptr});
         g->xmode = X_LOOPBACK;
     }
-    // the iteration schedule depends on the kernel, i.e. on d: cleora_init builds it
-
+    // collectives first (NCCL communicator: itself collective), then the build, whose outcome every
+    // rank agrees on before returning
     if (g->world > 1 && !loopback) {
         g->xmode = (o->flags & CLEORA_F_EXCHANGE_NCCL) ? X_NCCL : X_PEER;
         CL_TRY(dalloc((void**)&g->d_flag, 16, g->stream, "barrier flag"));
         CL_CUDA_TRY(cudaMemsetAsync(g->d_flag, 0, 16, g->stream));
-        Nccl& nc = nccl();
-        if (!nc.ok) return Status::make(4, "cleora_build: NCCL unavailable: " + nc.why);
-        CL_TRY(comm_get(o->nccl_id, g->world, g->rank, dev, &g->comm));
+        if (o->nccl_id) {
+            Nccl& nc = nccl();
+            if (!nc.ok) return Status::make(4, "cleora_build: NCCL unavailable: " + nc.why);
+            CL_TRY(comm_get(o->nccl_id, g->world, g->rank, dev, &g->comm));
+        } else {
+            g->host_ag = o->host_allgather;
+            g->host_ctx = o->host_ctx;
+            if (g->xmode == X_NCCL) return Status::make(2, "cleora_build: CLEORA_F_EXCHANGE_NCCL needs nccl_id");
+        }
     }
+    Status st = build_body(src, dst, w, E, N, directed, o, g, batch);
+    if (g->world > 1 && st.good()) {
+        // the whole M's facts: entries, rows without entries, longest row -- summed / maxed over the shards
+        std::vector<unsigned long long> f(3 * g->csr.size());
+        for (size_t p = 0; p < g->csr.size() && st.good(); p++) {
+            st = read_small(&f[3 * p], g->csr[p].d_scal + 2, 2 * sizeof(unsigned long long), g->stream);
+            f[3 * p + 2] = (unsigned long long)g->csr[p].nnz;
+        }
+        if (st.good() && !loopback) {
+            std::vector<unsigned long long> all(3 * g->world);
+            Status sa = comm_agree(g, st);
+            if (sa.good()) sa = comm_allgather(g, f.data(), all.data(), 3 * sizeof(unsigned long long));
+            if (!sa.good()) return sa;
+            f.swap(all);
+        }
+        if (st.good()) {
+            unsigned long long z = 0, mx = 0, nz = 0;
+            for (size_t q = 0; q < f.size() / 3; q++) {
+                z += f[3 * q];
+                mx = std::max(mx, f[3 * q + 1]);
+                nz += f[3 * q + 2];
+            }
+            g->zero_rows = (int64_t)z;
+            g->max_degree = (int64_t)mx;
+            g->nnz = (int64_t)nz;
+            return Status::ok();
+        }
+    }
+    if (g->world > 1 && !loopback) return comm_agree(g, st);
     // no final synchronisation: the CSR's last kernels run on while the caller goes on to
     // cleora_init (stream order keeps everything that reads them behind them)
-    return Status::ok();
+    return st;
 }
 
 }  // namespace
@@ -837,6 +1023,7 @@ const char* cleora_last_error(void) { return g_err.c_str(); }
 int64_t cleora_kernel_launches(void) { return g_launches.load(); }
 
 int cleora_release_cached_memory(void) {
+    ipc_close_all();
     release_cached(-1, nullptr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_release_cached_memory: ") + cudaGetErrorString(e)));
@@ -854,10 +1041,10 @@ int cleora_build(const int32_t* src, const int32_t* dst, const float* weight, in
     if (opts && opts->world > 1) {
         if (opts->world - 1 > kMaxPeers && (opts->flags & CLEORA_F_LOOPBACK))
             return usage("cleora_build: loopback emulation supports at most 8 ranks");
-        if (!opts->nccl_id && !(opts->flags & CLEORA_F_LOOPBACK))
-            return usage("cleora_build: world > 1 needs nccl_id");
+        if (!opts->nccl_id && !opts->host_allgather && !(opts->flags & CLEORA_F_LOOPBACK))
+            return usage("cleora_build: world > 1 needs nccl_id or host_allgather");
         if (opts->rank < 0 || opts->rank >= opts->world) return usage("cleora_build: rank outside [0, world)");
-        if (opts->world > 511) return usage("cleora_build: world > 511 (shard cuts are read back in one 4 KB read)");
+        if (opts->world > 255) return usage("cleora_build: world > 255 (shard cuts and counts are read back in one 4 KB read)");
     }
     if (opts && opts->n_chunks != 0) {
         if (opts->n_chunks < 0 || opts->chunk < 0 || opts->chunk >= opts->n_chunks)
@@ -1000,35 +1187,31 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     DeviceGuard guard(g->device);
     order_after_side(g);
     const int32_t dp = (d + 3) / 4 * 4;
+    // environment switches (measurement and diagnosis): read once here, not per launch
+    g->env_cold_first = getenv("CLEORA_COLD_FIRST") ? atoi(getenv("CLEORA_COLD_FIRST")) : -1;
+    g->env_write_zero = getenv("CLEORA_WRITE_ZERO_ROWS") != nullptr;
+    g->env_csr_prefetch = getenv("CLEORA_CSR_PREFETCH") ? atoi(getenv("CLEORA_CSR_PREFETCH")) : 1;
+    g->env_no_hot = getenv("CLEORA_NO_HOT") != nullptr;
+    g->env_defer = getenv("CLEORA_NO_DEFER") == nullptr;
     if (dp != g->dp || !g->T[0]) {
         free_T(g);
         const size_t tb = (size_t)g->n * dp * sizeof(float);
-        for (int i = 0; i < 2; i++) {
-            Status s = dalloc((void**)&g->T[i], tb, g->stream, "embedding T");
-            if (!s.good()) {
-                free_T(g);
-                return fail(s);
-            }
-        }
-        if (g->xmode == X_LOOPBACK) {
+        Status sa = Status::ok();
+        for (int i = 0; i < 2 && sa.good(); i++) sa = dalloc((void**)&g->T[i], tb, g->stream, "embedding T", true);
+        if (sa.good() && g->xmode == X_LOOPBACK) {
             g->rep[g->rank] = {g->T[0], g->T[1]};
-            for (int p = 0; p < g->world; p++) {
+            for (int p = 0; p < g->world && sa.good(); p++) {
                 if (p == g->rank) continue;
-                for (int i = 0; i < 2; i++) {
-                    Status s = dalloc((void**)&g->rep[p][i], tb, g->stream, "loopback replica");
-                    if (!s.good()) {
-                        free_T(g);
-                        return fail(s);
-                    }
-                }
+                for (int i = 0; i < 2 && sa.good(); i++)
+                    sa = dalloc((void**)&g->rep[p][i], tb, g->stream, "loopback replica");
             }
         }
-        if (g->xmode == X_PEER) {
-            Status s = open_peers(g);          // collective; may switch every rank to X_NCCL
-            if (!s.good()) {
-                free_T(g);
-                return fail(s);
-            }
+        // every rank must have its replicas before any maps them (failure agreement)
+        if (g->xmode == X_PEER || g->xmode == X_NCCL) sa = comm_agree(g, sa);
+        if (sa.good() && g->xmode == X_PEER) sa = open_peers(g);   // collective; may switch every rank to X_NCCL
+        if (!sa.good()) {
+            free_T(g);
+            return fail(sa);
         }
     }
     g->d = d;
@@ -1050,13 +1233,14 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     // heavy rows: > 64 entries with TMA bulk gathers, > 256 with cp.async / LDG gathers (measured:
     // c2 12.68 vs 12.80 ms per step with 64 / 256; c5 427 -> 375 ms, c4@256 8.10 -> 7.27 ms with 256);
     // every sequential fp32 run stays <= 256 terms (256-entry blocks keep the error ~3e-7)
-    g->heavy_thresh = heavy_thresh_default(gather_mode(dp) == kGatherBulk ? 64 : 256);
+    g->gmode = gather_mode(dp);
+    g->heavy_thresh = heavy_thresh_default(g->gmode == kGatherBulk ? 64 : 256);
     // light-chunk row cap per gather engine and row size (measured, scripts/chunk_sweep*.sh, min
     // launch ms): TMA bulk (d = 1024) 6 rows, c3 2.04 -> 1.42 vs 31; cp.async at d = 512 12 rows, c3
     // 0.86 -> 0.75; cp.async at d = 256 31 rows (c3 0.518 vs 0.581 at 8); LDG at d <= 128 16 rows,
     // f4 1.39 -> 1.25, c3@128 0.508 -> 0.490, c4@128 4.296 -> 4.306
     {
-        const int mode = gather_mode(dp);
+        const int mode = g->gmode;
         g->chunk_rows = mode == kGatherBulk ? 6 : mode == kGatherAsync ? (dp > 256 ? 12 : kChunkRows)
                                                                         : (dp <= 128 ? 16 : kChunkRows);
     }
@@ -1073,19 +1257,32 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
         if (!s.good()) return fail(s);
         g->partials_floats = (size_t)g->max_items * dp;
     }
-    if (g->tag_dp != dp && !getenv("CLEORA_NO_HOT") && g->nnz > 0) {
+    if (g->tag_dp != dp && !g->env_no_hot && g->nnz > 0) {
         // L2 residency hints: tag (bit 31 of col, in place) the columns whose rows are re-read
         // most (highest in-degree) so that their gathers use an evict_last policy, within a
-        // budget of the 126 MB L2
+        // budget of the 126 MB L2.  Row-sharded: every shard's columns, from the whole graph's
+        // in-degree (shard_plan), so the tags do not depend on the number of ranks.
         const char* e = getenv("CLEORA_HOT_MB");
         const int64_t budget = (int64_t)(e ? atof(e) : 72.0) * 1024 * 1024;
-        Status s = hot_tag(g->col, g->nnz, g->n, (int64_t)dp * 4, budget, g->stream, &g->n_hot, &g->n_ref,
-                           g->directed ? nullptr : g->row_ptr);
+        Status s = Status::ok();
+        for (size_t p = 0; p < g->csr.size() && s.good(); p++)
+            s = hot_tag(g->csr[p].col, g->csr[p].nnz, g->n, (int64_t)dp * 4, budget, g->stream, &g->n_hot, &g->n_ref,
+                        g->directed || g->sharded ? nullptr : g->csr[p].row_ptr, g->indeg);
         if (!s.good()) {
             free_T(g);
             return fail(s);
         }
         g->tag_dp = dp;
+    }
+    if (g->sharded && (g->xmode == X_PEER || g->xmode == X_LOOPBACK) && !g->ref && g->env_defer) {
+        // rows some row gathers: only they must reach the peers before the next step (H6)
+        Status s = dalloc((void**)&g->ref, (size_t)g->n, g->stream, "referenced rows");
+        if (s.good()) s = ref_flags(g->indeg, g->n, g->stream, g->ref);
+        if (!s.good()) {
+            dfree(g->ref, g->stream);
+            g->ref = nullptr;
+            return fail(s);
+        }
     }
     if (g->xmode == X_PEER) {
         // no rank may store into another's replicas before that rank is done with its
@@ -1118,9 +1315,11 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
             const int p = g->xmode == X_LOOPBACK ? sh : g->rank;
             const Schedule& sc = g->xmode == X_LOOPBACK ? g->sched_p[p] : g->sched;
             SpmmArgs a;
-            a.row_ptr = g->row_ptr;
-            a.col = g->col;
-            a.val = g->val;
+            const Csr& c = g->of(p);
+            a.row_ptr = c.row_ptr;
+            a.col = c.col;
+            a.val = c.val;
+            a.gather_mode = g->gmode;
             a.T_in = g->xmode == X_LOOPBACK ? g->rep[p][in] : g->T[in];
             a.T_out = g->xmode == X_LOOPBACK ? g->rep[p][out] : g->T[out];
             a.dp = g->dp;
@@ -1133,7 +1332,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
             a.counters = sc.counters;
             // with hot rows pinned (power-law graphs) the other gathers are evicted first; without
             // (e.g. lattices, whose re-reads are local) they keep the normal policy (measured: c2, c4, c3)
-            a.cold_first = getenv("CLEORA_COLD_FIRST") ? atoi(getenv("CLEORA_COLD_FIRST")) : (g->n_hot > 0 ? 1 : 0);
+            a.cold_first = g->env_cold_first >= 0 ? g->env_cold_first : (g->n_hot > 0 ? 1 : 0);
             a.work = sc.work;
             a.light_start = sc.light_start;
             a.n_light = sc.n_light;
@@ -1145,8 +1344,11 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
             } else if (g->xmode == X_PEER) {
                 for (int q = 0; q < g->world - 1; q++) a.peer_out[a.n_peers++] = g->peer_T[out][q];
             }
-            a.skip_zero_rows = (g->zclean[out] && !getenv("CLEORA_WRITE_ZERO_ROWS")) ? 1 : 0;
-            a.csr_prefetch = getenv("CLEORA_CSR_PREFETCH") ? atoi(getenv("CLEORA_CSR_PREFETCH")) : 1;
+            a.skip_zero_rows = (g->zclean[out] && !g->env_write_zero) ? 1 : 0;
+            a.csr_prefetch = g->env_csr_prefetch;
+            // deferred exchange: before the last step of this call only gathered rows go to the peers;
+            // the last step sends every row, so a fetch on any rank sees the whole T
+            a.peer_ref = (a.n_peers > 0 && g->ref && i + 1 < k) ? g->ref : nullptr;
             Status s = launch_spmm_norm(a, g->stream);
             if (!s.good()) return fail(s);
         }
@@ -1359,6 +1561,8 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
         for (int q = 0; q < kMaxPeers; q++) a.peer_out[q] = nullptr;
         a.skip_zero_rows = 0;
         a.csr_prefetch = 0;
+        a.peer_ref = nullptr;
+        a.gather_mode = g->gmode;
         st = launch_spmm_norm(a, s);
     }
     if (st.good()) {
@@ -1439,15 +1643,18 @@ int cleora_fetch_csr(const cleora_graph* g, int64_t* row_ptr, int32_t* col, floa
     if (!g) return usage("cleora_fetch_csr: graph is NULL");
     if (g->trimmed) return usage("cleora_fetch_csr: the handle was trimmed (cleora_trim)");
     DeviceGuard guard(g->device);
+    const Csr& c = g->own();
     cudaError_t e = cudaSuccess;
     if (row_ptr && e == cudaSuccess)
-        e = cudaMemcpyAsync(row_ptr, g->row_ptr, ((size_t)g->n + 1) * 8, cudaMemcpyDeviceToHost, g->stream);
-    if (col && e == cudaSuccess) e = cudaMemcpyAsync(col, g->col, (size_t)g->nnz * 4, cudaMemcpyDeviceToHost, g->stream);
+        e = cudaMemcpyAsync(row_ptr, c.row_ptr, ((size_t)g->n + 1) * 8, cudaMemcpyDeviceToHost, g->stream);
+    if (col && e == cudaSuccess && c.nnz > 0)
+        e = cudaMemcpyAsync(col, c.col, (size_t)c.nnz * 4, cudaMemcpyDeviceToHost, g->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
     if (col && e == cudaSuccess)
-        for (int64_t k = 0; k < g->nnz; k++) col[k] &= kColMask;     // drop the hot-row tags
-    if (val && e == cudaSuccess) e = cudaMemcpyAsync(val, g->val, (size_t)g->nnz * 4, cudaMemcpyDeviceToHost, g->stream);
-    if (deg && e == cudaSuccess) e = cudaMemcpyAsync(deg, g->deg, (size_t)g->n * 8, cudaMemcpyDeviceToHost, g->stream);
+        for (int64_t k = 0; k < c.nnz; k++) col[k] &= kColMask;     // drop the hot-row tags
+    if (val && e == cudaSuccess && c.nnz > 0)
+        e = cudaMemcpyAsync(val, c.val, (size_t)c.nnz * 4, cudaMemcpyDeviceToHost, g->stream);
+    if (deg && e == cudaSuccess) e = cudaMemcpyAsync(deg, c.deg, (size_t)g->n * 8, cudaMemcpyDeviceToHost, g->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_fetch_csr: ") + cudaGetErrorString(e)));
     return CLEORA_OK;
@@ -1462,10 +1669,10 @@ int cleora_info(cleora_graph* g, cleora_info_t* o) {
     o->d = g->d;
     o->d_stride = g->dp;
     o->iterations = g->iters;
-    if (g->zero_rows < 0 && g->d_scal) {
+    if (g->zero_rows < 0 && !g->csr.empty() && g->csr[0].d_scal) {
         DeviceGuard g0(g->device);
         unsigned long long f[2] = {0, 0};
-        Status s = read_small(f, g->d_scal + 2, sizeof f, g->stream);
+        Status s = read_small(f, g->csr[0].d_scal + 2, sizeof f, g->stream);
         if (!s.good()) return fail(s);
         g->zero_rows = (int64_t)f[0];
         g->max_degree = (int64_t)f[1];
@@ -1480,6 +1687,7 @@ int cleora_info(cleora_graph* g, cleora_info_t* o) {
     o->world = g->world;
     o->hot_rows = g->n_hot;
     o->n_graphs = g->n_graphs;
+    o->shard_nnz = g->csr.empty() ? 0 : g->own().nnz;
     o->referenced_rows = g->n_ref;
     o->exchange = g->xmode;
     o->device_bytes = g->bytes + ((g->T[0] ? 1 : 0) + (g->T[1] ? 1 : 0)) * (int64_t)g->n * g->dp * 4 +
@@ -1541,14 +1749,21 @@ int cleora_trim(cleora_graph* g) {
     g->partials = nullptr;
     g->partials_floats = 0;
     free_schedules(g);
-    dfree(g->row_ptr, g->stream);
-    dfree(g->col, g->stream);
-    dfree(g->val, g->stream);
-    dfree(g->deg, g->stream);
-    g->row_ptr = nullptr;
-    g->col = nullptr;
-    g->val = nullptr;
-    g->deg = nullptr;
+    // keep the build scalars (cleora_info reads zero_rows / max_degree lazily from csr[0].d_scal)
+    for (auto& c : g->csr) {
+        dfree(c.row_ptr, g->stream);
+        dfree(c.col, g->stream);
+        dfree(c.val, g->stream);
+        dfree(c.deg, g->stream);
+        c.row_ptr = nullptr;
+        c.col = nullptr;
+        c.val = nullptr;
+        c.deg = nullptr;
+    }
+    dfree(g->indeg, g->stream);
+    dfree(g->ref, g->stream);
+    g->indeg = nullptr;
+    g->ref = nullptr;
     g->bytes = 0;
     g->trimmed = true;
     return CLEORA_OK;
@@ -1569,13 +1784,11 @@ void cleora_destroy(cleora_graph* g) {
     if (g->stream) {
         cudaStreamSynchronize(g->stream);
         free_T(g);
-        dfree(g->row_ptr, g->stream);
-        dfree(g->col, g->stream);
-        dfree(g->val, g->stream);
-        dfree(g->deg, g->stream);
+        free_csr(g);
+        dfree(g->indeg, g->stream);
+        dfree(g->ref, g->stream);
         free_schedules(g);
         dfree(g->d_flag, g->stream);
-        dfree(g->d_scal, g->stream);
         dfree(g->occ, g->stream);
         dfree(g->d_base, g->stream);
         cudaStreamSynchronize(g->stream);
@@ -1610,6 +1823,8 @@ int cleora_probe_gather(int32_t device, int32_t row_bytes, int64_t table_bytes, 
     if (!st.good()) return fail(st);
     return CLEORA_OK;
 }
+
+int64_t cleora_ipc_opens(void) { return g_ipc_opens.load(); }
 
 int cleora_nccl_id_size(void) { return NCCL_UNIQUE_ID_BYTES; }
 

@@ -81,15 +81,16 @@ __global__ void k_head_flags(const uint64_t* __restrict__ keys, int64_t n, uint6
 }
 
 // B2: one thread per (a,b) run: sequential fp64 sum in stable order.
+// keys are (src - row_lo) * N + dst (row_lo = the first row of the shard, 0 for a whole graph)
 __global__ void k_merge_runs(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ pos,
                              const int64_t* __restrict__ run_start, int64_t nnz, int64_t n_valid,
-                             const float* __restrict__ w, int64_t E, int32_t N, int32_t* __restrict__ rows,
-                             int32_t* __restrict__ col, double* __restrict__ e_ab) {
+                             const float* __restrict__ w, int64_t E, int32_t N, int32_t row_lo,
+                             int32_t* __restrict__ rows, int32_t* __restrict__ col, double* __restrict__ e_ab) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nnz; u += stride) {
         int64_t s = run_start[u], e = (u + 1 < nnz) ? run_start[u + 1] : n_valid;
         uint64_t k = keys[s];
-        rows[u] = (int32_t)(k / (uint64_t)N);
+        rows[u] = (int32_t)(k / (uint64_t)N) + row_lo;
         col[u] = (int32_t)(k % (uint64_t)N);
         double acc = 0.0;
         if (w) {
@@ -157,9 +158,10 @@ __device__ double degree_long_row(const double* __restrict__ e_ab, int64_t k0, i
     return s;
 }
 
+// zero rows are counted inside [row_lo, row_hi) only (a shard's rows; the whole graph otherwise)
 __global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __restrict__ e_ab, int32_t N,
-                         double* __restrict__ deg, unsigned long long* __restrict__ zero_rows,
-                         unsigned long long* __restrict__ max_deg) {
+                         int32_t row_lo, int32_t row_hi, double* __restrict__ deg,
+                         unsigned long long* __restrict__ zero_rows, unsigned long long* __restrict__ max_deg) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     // zero-row count and max degree: per-lane registers, one atomic per block at the end (per-row
@@ -171,7 +173,7 @@ __global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __re
         if (a < N) {
             k0 = row_ptr[a];
             k1 = row_ptr[a + 1];
-            if (k1 == k0) my_zero++;
+            if (k1 == k0 && a >= row_lo && a < row_hi) my_zero++;
             else my_max = max(my_max, (unsigned long long)(k1 - k0));
         }
         const bool lng = a < N && k1 - k0 > 32;
@@ -285,6 +287,113 @@ __global__ void k_cuts(const int64_t* __restrict__ rp, int32_t N, int world, int
     cuts[p] = lo;
 }
 
+// ---- row-sharded builds (world > 1): every rank reads the whole COO, counts the
+// entries of every row (after mirroring, before merging), cuts the rows into nnz-balanced shards,
+// and keeps only the entries of its own rows -- M is never materialised whole on any rank.
+
+// cnt[a] += entries of row a; indeg[b] += entries of column b (directed only: for undirected
+// graphs the pattern is symmetric and indeg = cnt); occ as k_validate_expand; validation as
+// k_validate_expand (first bad edge, kind)
+__global__ void k_count_rows(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                             const float* __restrict__ w, int64_t E, int32_t N, int directed,
+                             unsigned long long* __restrict__ cnt, int32_t* __restrict__ indeg,
+                             unsigned long long* __restrict__ err_first, int* __restrict__ err_kind, int32_t n_chunks,
+                             int32_t chunk, uint64_t chunk_key, int32_t* __restrict__ occ) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += stride) {
+        const int32_t u = src[i], v = dst[i];
+        const bool bad_id = u < 0 || u >= N || v < 0 || v >= N;
+        bool bad_w = false;
+        if (w) {
+            const float x = w[i];
+            bad_w = !(isfinite(x) && x > 0.0f);
+        }
+        if (bad_id || bad_w) {
+            atomicMin(err_first, (unsigned long long)i);
+            atomicOr(err_kind, bad_id ? 1 : 2);
+            continue;
+        }
+        const bool keep = n_chunks <= 1 ||
+                          (int32_t)(((sm64(chunk_key ^ (uint64_t)i) >> 32) * (uint64_t)n_chunks) >> 32) == chunk;
+        if (!keep) continue;
+        if (occ) {
+            atomicAdd(occ + u, 1);
+            atomicAdd(occ + v, 1);
+        }
+        atomicAdd(cnt + u, 1ull);
+        if (directed) {
+            atomicAdd(indeg + v, 1);
+        } else if (u != v) {
+            atomicAdd(cnt + v, 1ull);
+        }
+    }
+}
+
+__global__ void k_cnt_to_indeg(const unsigned long long* __restrict__ cnt, int32_t N, int32_t* __restrict__ indeg) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < N; v += stride) indeg[v] = (int32_t)cnt[v];
+}
+
+// cuts[p] = first row whose entry prefix reaches p * total / world; ent[p] = prefix[cuts[p]]
+__global__ void k_cuts_ent(const int64_t* __restrict__ prefix, int32_t N, int world, int64_t* __restrict__ cuts,
+                           int64_t* __restrict__ ent) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > world) return;
+    const int64_t tot = prefix[N];
+    int64_t c;
+    if (p == 0) {
+        c = 0;
+    } else if (p == world) {
+        c = N;
+    } else {
+        int64_t lo = 0, hi = N;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((__int128)prefix[mid] * world >= (__int128)p * tot) hi = mid; else lo = mid + 1;
+        }
+        c = lo;
+    }
+    cuts[p] = c;
+    ent[p] = prefix[c];
+}
+
+// entry i of the mirrored list (i < E: edge i as given; i >= E: the mirror of edge i - E) is in the
+// shard: valid (checked by k_count_rows), in the chunk, not the dropped mirror of a self-loop, and
+// its source row in [lo, hi).  cub::DeviceSelect keeps the selected indices in input order, so the
+// shard's entries keep their relative order of the whole list (readings B1, B2: the same sums).
+struct InShard {
+    const int32_t* src;
+    const int32_t* dst;
+    int64_t E;
+    int32_t lo, hi;
+    int directed;
+    int32_t n_chunks, chunk;
+    uint64_t chunk_key;
+    __device__ bool operator()(uint32_t i) const {
+        const bool mirror = (int64_t)i >= E;
+        const int64_t e = mirror ? (int64_t)i - E : (int64_t)i;
+        const int32_t u = src[e], v = dst[e];
+        if (mirror && (directed || u == v)) return false;
+        const int32_t r = mirror ? v : u;
+        if (r < lo || r >= hi) return false;
+        return n_chunks <= 1 ||
+               (int32_t)(((sm64(chunk_key ^ (uint64_t)e) >> 32) * (uint64_t)n_chunks) >> 32) == chunk;
+    }
+};
+
+__global__ void k_shard_keys(const uint32_t* __restrict__ pos, int64_t n, const int32_t* __restrict__ src,
+                             const int32_t* __restrict__ dst, int64_t E, int32_t N, int32_t lo,
+                             uint64_t* __restrict__ keys) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const int64_t i = pos[k];
+        const bool mirror = i >= E;
+        const int64_t e = mirror ? i - E : i;
+        const int32_t u = mirror ? dst[e] : src[e], v = mirror ? src[e] : dst[e];
+        keys[k] = (uint64_t)(uint32_t)(u - lo) * (uint64_t)N + (uint64_t)(uint32_t)v;
+    }
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -305,9 +414,15 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
                  int directed, cudaStream_t s, BuildOut* out, const BuildExtra* extra) {
     const BuildExtra none;
     const BuildExtra& x = extra ? *extra : none;
-    const int64_t n_ent = directed ? E : 2 * E;
-    if (n_ent >= (int64_t)UINT32_MAX) return Status::make(2, "cleora_build: too many edges (entry positions are 32-bit)");
-    const uint64_t NN = (uint64_t)N * (uint64_t)N;
+    // shard mode (x.row_hi >= 0): only the entries of rows [row_lo, row_hi), x.shard_entries of them,
+    // selected from the mirrored list in order; the edges were validated (and occ counted) by
+    // shard_plan, so nothing is dropped here
+    const bool shard = x.row_hi >= 0;
+    const int32_t lo = shard ? x.row_lo : 0, hi = shard ? x.row_hi : N;
+    const int64_t n_all = directed ? E : 2 * E;         // entries of the mirrored list
+    const int64_t n_ent = shard ? x.shard_entries : n_all;
+    if (n_all >= (int64_t)UINT32_MAX) return Status::make(2, "cleora_build: too many edges (entry positions are 32-bit)");
+    const uint64_t NN = (uint64_t)(hi - lo) * (uint64_t)N;
     const uint64_t sentinel = NN;                        // sorts after every valid key
     const int end_bit = 64 - __builtin_clzll(sentinel | 1ull);
 
@@ -320,23 +435,38 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     const bool keys_only = d_w == nullptr;
     CL_TRY(keys.alloc(n_ent, s, "sort keys"));
     CL_TRY(keys2.alloc(n_ent, s, "sort keys (alt)"));
-    if (!keys_only) {
-        CL_TRY(pos.alloc(n_ent, s, "sort payload"));
-        CL_TRY(pos2.alloc(n_ent, s, "sort payload (alt)"));
-    }
+    if (!keys_only || shard) CL_TRY(pos.alloc(n_ent, s, "sort payload"));
+    if (!keys_only) CL_TRY(pos2.alloc(n_ent, s, "sort payload (alt)"));
     CL_TRY(scal.alloc(8, s, "scalars"));
     CL_TRY(err_kind.alloc(1, s, "scalars"));
     CL_CUDA_TRY(cudaMemsetAsync(scal.p, 0, 8 * sizeof(unsigned long long), s));
     CL_CUDA_TRY(cudaMemsetAsync(scal.p, 0xFF, sizeof(unsigned long long), s));   // err_first = max
     CL_CUDA_TRY(cudaMemsetAsync(err_kind.p, 0, sizeof(int), s));
 
-    if (x.occ) CL_CUDA_TRY(cudaMemsetAsync(x.occ, 0, (size_t)N * sizeof(int32_t), s));
-    k_validate_expand<<<grid_for(E, 4), kThreads, 0, s>>>(d_src, d_dst, d_w, E, N, x.dst_limit < 0 ? N : x.dst_limit,
-                                                          directed, sentinel, keys.p, pos.p, scal.p + 0, err_kind.p,
-                                                          scal.p + 1, x.n_chunks, x.chunk, x.chunk_key, x.occ);
-    CL_CUDA_TRY(cudaGetLastError());
-    count_launches(1);
-    trace("csr: validate+expand", s, false);
+    if (shard) {
+        // positions of the shard's entries in list order, then their keys
+        thrust::counting_iterator<uint32_t> it(0);
+        InShard pred{d_src, d_dst, E, lo, hi, directed, x.n_chunks, x.chunk, x.chunk_key};
+        size_t tmp_bytes = 0;
+        CL_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, it, pos.p, scal.p + 5, n_all, pred, s));
+        {
+            DevBuf<uint8_t> tmp;
+            CL_TRY(tmp.alloc(tmp_bytes, s, "shard select temp"));
+            CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, pos.p, scal.p + 5, n_all, pred, s));
+        }
+        k_shard_keys<<<grid_for(n_ent, 4), kThreads, 0, s>>>(pos.p, n_ent, d_src, d_dst, E, N, lo, keys.p);
+        CL_CUDA_TRY(cudaGetLastError());
+        count_launches(3);
+        trace("csr: shard select+keys", s, false);
+    } else {
+        if (x.occ) CL_CUDA_TRY(cudaMemsetAsync(x.occ, 0, (size_t)N * sizeof(int32_t), s));
+        k_validate_expand<<<grid_for(E, 4), kThreads, 0, s>>>(d_src, d_dst, d_w, E, N, x.dst_limit < 0 ? N : x.dst_limit,
+                                                              directed, sentinel, keys.p, pos.p, scal.p + 0, err_kind.p,
+                                                              scal.p + 1, x.n_chunks, x.chunk, x.chunk_key, x.occ);
+        CL_CUDA_TRY(cudaGetLastError());
+        count_launches(1);
+        trace("csr: validate+expand", s, false);
+    }
 
     // B1: stable radix sort by (src, dst) over the bits the keys use
     {
@@ -358,6 +488,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         if (!keys_only && vb.Current() != pos.p) std::swap(pos.p, pos2.p);
     }
     dfree(keys2.release(), s);
+    if (keys_only) dfree(pos.release(), s);             // shard mode: positions only made the keys
     trace("csr: radix sort", s, true);
 
     // B2: run starts of equal keys, merged weights.  Over all n_ent keys (the dropped entries carry
@@ -406,7 +537,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     CL_TRY(rows.alloc(nnz, s, "entry rows"));
     CL_TRY(col.alloc(nnz, s, "CSR col"));
     CL_TRY(e_ab.alloc(nnz, s, "e_ab"));
-    k_merge_runs<<<grid_for(nnz, 4), kThreads, 0, s>>>(keys.p, pos.p, run_start.p, nnz, n_valid, d_w, E, N,
+    k_merge_runs<<<grid_for(nnz, 4), kThreads, 0, s>>>(keys.p, pos.p, run_start.p, nnz, n_valid, d_w, E, N, lo,
                                                        rows.p, col.p, e_ab.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
@@ -430,7 +561,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int blocks = std::min(grid_for(N, 1), sms * 16);   // 32 rows per warp step, grid-stride
-        k_degree<<<blocks, kThreads, 0, s>>>(row_ptr.p, e_ab.p, N, deg.p, scal.p + 2, scal.p + 3);
+        k_degree<<<blocks, kThreads, 0, s>>>(row_ptr.p, e_ab.p, N, lo, hi, deg.p, scal.p + 2, scal.p + 3);
     }
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
@@ -601,29 +732,33 @@ __global__ void k_tag(int32_t* __restrict__ col, int64_t nnz, const int32_t* __r
 }  // namespace
 
 Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes, cudaStream_t s,
-               int64_t* n_hot, int64_t* n_ref, const int64_t* d_row_ptr_sym) {
+               int64_t* n_hot, int64_t* n_ref, const int64_t* d_row_ptr_sym, const int32_t* d_indeg_in) {
     // hot rows = the K = budget / row_bytes rows of largest in-degree (exact threshold: the K-th
     // largest in-degree, from a radix sort of the in-degrees; ties at the threshold are kept
     // unless they overshoot the budget by more than a quarter)
-    DevBuf<int32_t> indeg, sorted;
+    DevBuf<int32_t> indeg_own, sorted;
     DevBuf<unsigned long long> cnt;
-    CL_TRY(indeg.alloc(N, s, "in-degree"));
+    const int32_t* indeg = d_indeg_in;         // row-sharded builds: the whole graph's, from shard_plan
+    if (!indeg) CL_TRY(indeg_own.alloc(N, s, "in-degree"));
     CL_TRY(sorted.alloc(N, s, "sorted in-degree"));
     CL_TRY(cnt.alloc(3, s, "hot count"));
-    if (d_row_ptr_sym) {                       // no atomics (c5: 36 ms of contended hub counters)
-        k_row_lengths<<<grid_for(N, 4), kThreads, 0, s>>>(d_row_ptr_sym, N, indeg.p);
-    } else {
-        CL_CUDA_TRY(cudaMemsetAsync(indeg.p, 0, (size_t)N * 4, s));
-        k_indegree<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p);
+    if (!indeg) {
+        if (d_row_ptr_sym) {                   // no atomics (c5: 36 ms of contended hub counters)
+            k_row_lengths<<<grid_for(N, 4), kThreads, 0, s>>>(d_row_ptr_sym, N, indeg_own.p);
+        } else {
+            CL_CUDA_TRY(cudaMemsetAsync(indeg_own.p, 0, (size_t)N * 4, s));
+            k_indegree<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg_own.p);
+        }
+        CL_CUDA_TRY(cudaGetLastError());
+        count_launches(1);
+        indeg = indeg_own.p;
     }
-    CL_CUDA_TRY(cudaGetLastError());
-    count_launches(1);
     {
         size_t tmp_bytes = 0;
-        CL_CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, indeg.p, sorted.p, (int64_t)N, 0, 32, s));
+        CL_CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, indeg, sorted.p, (int64_t)N, 0, 32, s));
         DevBuf<uint8_t> tmp;
         CL_TRY(tmp.alloc(tmp_bytes, s, "in-degree sort temp"));
-        CL_CUDA_TRY(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, indeg.p, sorted.p, (int64_t)N, 0, 32, s));
+        CL_CUDA_TRY(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, indeg, sorted.p, (int64_t)N, 0, 32, s));
         count_launches(2 + 4);
     }
     int64_t K = budget_bytes / (row_bytes > 0 ? row_bytes : 1);
@@ -632,7 +767,7 @@ Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_
     // from pinning); counted on the device, then read back with the counts in one round trip
     const int32_t* kth = K > 0 ? sorted.p + (N - K) : nullptr;
     CL_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, 3 * sizeof(unsigned long long), s));
-    k_count_ge<<<grid_for(N, 8), kThreads, 0, s>>>(indeg.p, N, kth, cnt.p);
+    k_count_ge<<<grid_for(N, 8), kThreads, 0, s>>>(indeg, N, kth, cnt.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     unsigned long long c[3];
@@ -659,9 +794,11 @@ Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_
     if (t == INT32_MAX) nh = 0;
     *n_hot = nh;
     if (n_ref) *n_ref = (int64_t)c[2];
-    k_tag<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p, t);
+    if (nnz > 0) {
+        k_tag<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg, t);
+        count_launches(1);
+    }
     CL_CUDA_TRY(cudaGetLastError());
-    count_launches(1);
     return Status::ok();
 }
 
@@ -706,6 +843,83 @@ Status batch_global_ids(const int32_t* d_src, const int32_t* d_dst, int64_t E, c
         snprintf(buf, sizeof buf, "cleora_build_batch: edge %llu: node id outside [0, node_count) of its graph", h);
         return Status::make(3, buf);
     }
+    return Status::ok();
+}
+
+Status shard_plan(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N, int directed,
+                  const BuildExtra* extra, int world, cudaStream_t s, int64_t* h_cuts, int64_t* h_ent,
+                  int32_t** d_indeg) {
+    const BuildExtra none;
+    const BuildExtra& x = extra ? *extra : none;
+    if ((int64_t)(directed ? E : 2 * E) >= (int64_t)UINT32_MAX)
+        return Status::make(2, "cleora_build: too many edges (entry positions are 32-bit)");
+    if (world + 1 > 4096 / 16) return Status::make(2, "cleora_build: world > 255 for a row-sharded build");
+    DevBuf<unsigned long long> cnt, scal;
+    DevBuf<int64_t> prefix, cuts, ent;
+    DevBuf<int32_t> indeg;
+    DevBuf<int> kind;
+    CL_TRY(cnt.alloc((size_t)N + 1, s, "row entry counts"));
+    CL_TRY(indeg.alloc(N, s, "in-degree"));
+    CL_TRY(scal.alloc(1, s, "scalars"));
+    CL_TRY(kind.alloc(1, s, "scalars"));
+    CL_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, ((size_t)N + 1) * sizeof(unsigned long long), s));
+    if (directed) CL_CUDA_TRY(cudaMemsetAsync(indeg.p, 0, (size_t)N * sizeof(int32_t), s));
+    CL_CUDA_TRY(cudaMemsetAsync(scal.p, 0xFF, sizeof(unsigned long long), s));
+    CL_CUDA_TRY(cudaMemsetAsync(kind.p, 0, sizeof(int), s));
+    if (x.occ) CL_CUDA_TRY(cudaMemsetAsync(x.occ, 0, (size_t)N * sizeof(int32_t), s));
+    k_count_rows<<<grid_for(E, 4), kThreads, 0, s>>>(d_src, d_dst, d_w, E, N, directed, cnt.p, indeg.p, scal.p, kind.p,
+                                                     x.n_chunks, x.chunk, x.chunk_key, x.occ);
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    if (!directed) {
+        k_cnt_to_indeg<<<grid_for(N, 4), kThreads, 0, s>>>(cnt.p, N, indeg.p);
+        CL_CUDA_TRY(cudaGetLastError());
+        count_launches(1);
+    }
+    CL_TRY(prefix.alloc((size_t)N + 1, s, "row entry prefix"));
+    {
+        size_t tmp_bytes = 0;
+        const int64_t* in = reinterpret_cast<const int64_t*>(cnt.p);   // counts < 2^63: same bits
+        CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, in, prefix.p, (int64_t)N + 1, s));
+        DevBuf<uint8_t> tmp;
+        CL_TRY(tmp.alloc(tmp_bytes, s, "scan temp"));
+        CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, in, prefix.p, (int64_t)N + 1, s));
+        count_launches(2);
+    }
+    CL_TRY(cuts.alloc(world + 1, s, "shard cuts"));
+    CL_TRY(ent.alloc(world + 1, s, "shard entries"));
+    k_cuts_ent<<<(world + 128) / 128, 128, 0, s>>>(prefix.p, N, world, cuts.p, ent.p);
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    unsigned long long bad = 0;
+    int h_kind = 0;
+    {
+        const SmallRead rd[4] = {{&bad, scal.p, sizeof bad}, {&h_kind, kind.p, sizeof h_kind},
+                                 {h_cuts, cuts.p, (world + 1) * sizeof(int64_t)},
+                                 {h_ent, ent.p, (world + 1) * sizeof(int64_t)}};
+        CL_TRY(read_small_n(rd, 4, s));
+    }
+    if (h_kind) {
+        char buf[256];
+        snprintf(buf, sizeof buf, "cleora_build: edge %llu: %s", bad,
+                 (h_kind & 1) ? "node id outside [0, n_nodes)" : "weight not finite or <= 0");
+        return Status::make(3, buf);
+    }
+    *d_indeg = indeg.release();
+    return Status::ok();
+}
+
+namespace {
+__global__ void k_ref_flags(const int32_t* __restrict__ indeg, int32_t N, uint8_t* __restrict__ ref) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < N; v += stride) ref[v] = indeg[v] > 0 ? 1 : 0;
+}
+}  // namespace
+
+Status ref_flags(const int32_t* d_indeg, int32_t N, cudaStream_t s, uint8_t* d_ref) {
+    k_ref_flags<<<grid_for(N, 4), kThreads, 0, s>>>(d_indeg, N, d_ref);
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     return Status::ok();
 }
 

@@ -54,7 +54,7 @@ void count_launches(int64_t n);
 // ---------------------------------------------------------------- device buffers
 // Stream-ordered allocation from the device's default pool (release threshold raised so
 // repeated build/destroy cycles do not return memory to the driver).
-Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what);
+Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, bool block = false);
 void dfree(void* p, cudaStream_t s);
 
 // SplitMix64 output function (the mixer of the T_0 hash, reading R1, and of the chunk
@@ -102,17 +102,33 @@ struct SpmmArgs {
     // emulation, the other local replicas -- so the all-gather overlaps the SpMM row by row.
     int32_t n_peers;
     float* peer_out[kMaxPeers];
+    // non-NULL: a non-empty row r goes to the peers only when peer_ref[r] (some row gathers it); the
+    // rest of the exchange is deferred to the last step of an iterate call, which sends every row
+    const uint8_t* peer_ref;
     // Rows without entries are already 0 in T_out (written by an earlier iteration): skip them.
     int32_t skip_zero_rows;
     int32_t csr_prefetch;   // register kernel: L1-prefetch each light chunk's CSR words
+    int32_t gather_mode;    // kGather* for this dp (gather_mode(dp), read once by cleora_init)
 };
 
-// Store float4 f of row `row` of the iteration's output into T_out and every peer replica.
-__device__ __forceinline__ void put_out4(const SpmmArgs& a, int64_t row, int f, const float4& v) {
+// Store float4 f of row `row` of the iteration's output into T_out and every peer replica.  `empty`:
+// the row has no entries (its zeros always reach the peers, which then skip it like this rank does).
+__device__ __forceinline__ void put_out4(const SpmmArgs& a, int64_t row, int f, const float4& v, bool empty = false) {
     const int64_t off = row * (int64_t)a.dp;
     __stcs(reinterpret_cast<float4*>(a.T_out + off) + f, v);
-    for (int p = 0; p < a.n_peers; p++) __stcs(reinterpret_cast<float4*>(a.peer_out[p] + off) + f, v);
+    if (a.n_peers > 0 && (empty || !a.peer_ref || a.peer_ref[row]))
+        for (int p = 0; p < a.n_peers; p++) __stcs(reinterpret_cast<float4*>(a.peer_out[p] + off) + f, v);
 }
+
+// A CSR of M (or of one row shard of it) on the device
+struct Csr {
+    int64_t* row_ptr = nullptr;
+    int32_t* col = nullptr;
+    float* val = nullptr;
+    double* deg = nullptr;
+    unsigned long long* d_scal = nullptr;   // build scalars ([2] zero rows of its rows, [3] max degree)
+    int64_t nnz = 0;
+};
 
 // build.cu
 struct BuildOut {
@@ -134,6 +150,10 @@ struct BuildExtra {
     uint64_t chunk_key = 0;     // sm64(chunk_seed + 0x9E3779B97F4A7C15)
     int32_t* occ = nullptr;
     int32_t dst_limit = -1;     // -1: N
+    // row-sharded build: only rows [row_lo, row_hi) (row_hi = -1: all), whose entries (after mirroring,
+    // before merging) number shard_entries; the edges were validated and occ counted by shard_plan
+    int32_t row_lo = 0, row_hi = -1;
+    int64_t shard_entries = 0;
 };
 Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N,
                  int directed, cudaStream_t s, BuildOut* out, const BuildExtra* extra = nullptr);
@@ -154,6 +174,16 @@ struct Schedule {
 Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int heavy_thresh,
                       int chunk_rows, cudaStream_t s, Schedule* out);
 Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts);
+// Row-sharded builds (world > 1): validate every edge, count every row's entries (mirrored, before
+// merging), cut the rows into `world` shards balanced on those counts (cut p = first row whose entry
+// prefix reaches p * total / world; h_cuts[world + 1]), h_ent[p] = entries before cut p, and the
+// whole graph's in-degree (int32[N], device, caller frees) for the hot-row tags and the exchange's
+// referenced-row flags.  extra: chunk filter and occ (counted here).  EDATA on a bad edge.
+Status shard_plan(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N, int directed,
+                  const BuildExtra* extra, int world, cudaStream_t s, int64_t* h_cuts, int64_t* h_ent,
+                  int32_t** d_indeg);
+// ref[v] = in-degree(v) > 0 (rows some row gathers)
+Status ref_flags(const int32_t* d_indeg, int32_t N, cudaStream_t s, uint8_t* d_ref);
 
 // Hot-row tagging for L2 residency hints, in place: col[k] = (col[k] & 0x7fffffff) |
 // (indeg(col[k]) >= 2^b) << 31, b the smallest power of two such that the hot rows' bytes fit
@@ -162,7 +192,8 @@ Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s
 constexpr int32_t kColMask = 0x7fffffff;
 Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes,
                cudaStream_t s, int64_t* n_hot, int64_t* n_ref /* rows with in-degree > 0, or NULL */,
-               const int64_t* d_row_ptr_sym /* undirected graphs: in-degree = row length, else NULL */);
+               const int64_t* d_row_ptr_sym /* undirected graphs: in-degree = row length, else NULL */,
+               const int32_t* d_indeg = nullptr /* precomputed in-degree (row-sharded builds), else NULL */);
 
 // chunks.cu: out = sum_q w_qv Tq[q] (Algorithm 1 lines 10-12); d_Tq / d_occ are device arrays
 // of Q device pointers; out and every Tq[q] are N x dp

@@ -187,10 +187,10 @@ __device__ void light_row(const SpmmArgs& a, const Pol& pol, int64_t row, int64_
 #pragma unroll
         for (int v = 0; v < V; v++) {
             const int f = lane + 32 * v;
-            if (4 * f < dp) put_out4(a, row, f, scale4(acc[v], inv));
+            if (4 * f < dp) put_out4(a, row, f, scale4(acc[v], inv), k1 == k0);
         }
     } else {
-        for (int f = lane; 4 * f < dp; f += 32) put_out4(a, row, f, scale4(out[f], inv));
+        for (int f = lane; 4 * f < dp; f += 32) put_out4(a, row, f, scale4(out[f], inv), k1 == k0);
     }
 }
 
@@ -256,8 +256,8 @@ __device__ void light_row_pair(const SpmmArgs& a, const Pol& pol, int64_t row, i
     for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
     if (!live || (n_row == 0 && a.skip_zero_rows)) return;
     const double inv = inv_norm(ss);
-    if (ok0) put_out4(a, row, hl, scale4(acc0, inv));
-    if (ok1) put_out4(a, row, hl + 16, scale4(acc1, inv));
+    if (ok0) put_out4(a, row, hl, scale4(acc0, inv), n_row == 0);
+    if (ok1) put_out4(a, row, hl + 16, scale4(acc1, inv), n_row == 0);
 }
 
 template <int V, bool H>
@@ -483,7 +483,7 @@ Status launch_v(const SpmmArgs& a, cudaStream_t s) {
 }  // namespace
 
 Status launch_spmm_norm(const SpmmArgs& a, cudaStream_t s) {
-    if (tma_path_supported(a.dp)) return launch_spmm_tma(a, s);
+    if (a.gather_mode != kGatherLdg) return launch_spmm_tma(a, s);
     if (a.dp <= 128) return launch_v<1>(a, s);
     if (a.dp <= 256) return launch_v<2>(a, s);
     if (a.dp <= 512) return launch_v<4>(a, s);

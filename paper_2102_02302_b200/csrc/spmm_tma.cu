@@ -177,7 +177,7 @@ __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, f
 #pragma unroll
     for (int v = 0; v < V; v++) {
         const int f = lane + 32 * v;
-        if (FULL || 4 * f < dp) put_out4(a, row, f, scale4(acc[v], inv));
+        if (FULL || 4 * f < dp) put_out4(a, row, f, scale4(acc[v], inv), empty);
         acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
@@ -492,7 +492,7 @@ int gather_mode(int dp) {
 bool tma_path_supported(int dp) { return gather_mode(dp) != kGatherLdg; }
 
 Status launch_spmm_tma(const SpmmArgs& a, cudaStream_t s) {
-    const int mode = gather_mode(a.dp);
+    const int mode = a.gather_mode;
     if (a.dp == 1024) return launch_mode<8, true>(a, s, mode);
     if (a.dp == 512) return launch_mode<4, true>(a, s, mode);
     if (a.dp == 256) return launch_mode<2, true>(a, s, mode);

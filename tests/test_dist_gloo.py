@@ -39,14 +39,32 @@ def _worker(rank, world, port, cfg, q):
         import paper_2102_02302_b200 as cl
         g = gen.chung_lu(3000, 9000, 2.1, 9.5388, 233115.5 * 3000 / 1134890, seed=cfg["seed"]) \
             if cfg["kind"] == "cl" else gen.rmat_directed(2048, 11, 20000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=cfg["seed"])
-        M = oracle.build_from(g)
-        cuts = cl.cleora_plan_shards(M.row_ptr, world)
-        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+        M_full = oracle.build_from(g)
+        if cfg.get("cuts") == "entries":
+            # the row-sharded build (cleora_build, world > 1): cuts from the mirrored entry counts,
+            # and this rank builds M from its rows' entries only; its rows must be bit-identical
+            # to the whole M's, and the rest empty
+            from tests import _shard
+            cuts = _shard.cuts(g, world)
+            r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+            s_, d_, w_ = _shard.shard_edges(g, r0, r1)
+            M = oracle.build_csr(s_, d_, w_, g.n, True)
+            a, b = int(M_full.row_ptr[r0]), int(M_full.row_ptr[r1])
+            assert np.array_equal(M.row_ptr[r0:r1 + 1] + a, M_full.row_ptr[r0:r1 + 1])
+            assert M.row_ptr[r0] == 0 and M.row_ptr[-1] == b - a
+            assert np.array_equal(M.col, M_full.col[a:b])
+            assert M.val.tobytes() == M_full.val[a:b].tobytes()
+            assert M.deg[r0:r1].tobytes() == M_full.deg[r0:r1].tobytes()
+            assert not M.deg[:r0].any() and not M.deg[r1:].any()
+        else:
+            M = M_full
+            cuts = cl.cleora_plan_shards(M.row_ptr, world)
+            r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
         T = torch.from_numpy(oracle.hash_init(g.n, cfg["d"], 0))
         if cfg.get("protocol") == "peer":
             T = _peer_protocol(M, T, cuts, rank, world, cfg["iters"])
             if rank == 0:
-                ref = oracle.embed(M, cfg["d"], 0, cfg["iters"])
+                ref = oracle.embed(M_full, cfg["d"], 0, cfg["iters"])
                 q.put((T.numpy().tobytes() == ref.tobytes(), [int(c) for c in cuts]))
             return
         for _ in range(cfg["iters"]):
@@ -61,7 +79,7 @@ def _worker(rank, world, port, cfg, q):
                     out[b:e] = blk
             T = out
         if rank == 0:
-            ref = oracle.embed(M, cfg["d"], 0, cfg["iters"])
+            ref = oracle.embed(M_full, cfg["d"], 0, cfg["iters"])
             q.put((T.numpy().tobytes() == ref.tobytes(), [int(c) for c in cuts]))
     finally:
         dist.destroy_process_group()
@@ -94,12 +112,15 @@ def _peer_protocol(M, T0, cuts, rank, world, iters):
     return bufs[cur]
 
 
-@pytest.mark.parametrize("world,kind,protocol", [(2, "cl", "nccl"), (3, "rmat", "nccl"), (2, "rmat", "peer"),
-                                                 (3, "cl", "peer")])
-def test_sharded_iteration_equals_single_process(world, kind, protocol):
+@pytest.mark.parametrize("world,kind,protocol,cut", [(2, "cl", "nccl", "nnz"), (3, "rmat", "nccl", "nnz"),
+                                                     (2, "rmat", "peer", "nnz"), (3, "cl", "peer", "nnz"),
+                                                     (2, "cl", "peer", "entries"), (3, "rmat", "peer", "entries"),
+                                                     (4, "rmat", "nccl", "entries")])
+def test_sharded_iteration_equals_single_process(world, kind, protocol, cut):
+    """Each rank holds only its shard's CSR when cut == "entries" (the row-sharded build)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    cfg = dict(kind=kind, seed=world, d=16, iters=4, protocol=protocol)
+    cfg = dict(kind=kind, seed=world, d=16, iters=4, protocol=protocol, cuts=cut)
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
     for p in procs:

@@ -1,0 +1,108 @@
+"""The real multi-process exchange on ONE GPU: two processes, each a rank of a world-2 handle,
+collectives through the caller's host all-gather (gloo; NCCL refuses two ranks on one device), the
+fused peer-store exchange through CUDA IPC mappings of each other's T buffers (X_PEER).
+
+This runs, on hardware, what the loopback emulation cannot: cudaIpcGetMemHandle on blocks of the
+library's block cache, cudaIpcOpenMemHandle in another process, stores through those mappings with
+__threadfence_system, the barrier ordering of the steps (stream synchronise + host all-gather), the
+mapping cache (a second handle of the same shape reuses the same blocks: no new IPC opens), and a
+rank destroying its handle while the other still maps its blocks.  No kernel ever waits for another
+process's kernel (the barrier is on the host), so the two ranks can share the GPU.  Every rank's
+embedding must be BITWISE the 1-GPU result."""
+import os
+import socket
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import gen
+    import paper_2102_02302_b200 as cl
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {}
+    try:
+        torch.cuda.set_device(0)
+        ag = cl.host_allgather_from()
+        g = gen.rmat_directed(8192, 13, 120000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=4)
+        u = gen.chung_lu(20000, 60000, 2.1, 9.5388, 233115.5 * 20000 / 1134890, seed=2)
+        res = []
+        for gr, d, calls in ((g, 256, [3]), (g, 256, [1, 2]), (u, 1024, [4]), (u, 64, [2, 2])):
+            opens0 = cl.cleora_ipc_opens()
+            G = cl.cleora_build(gr.src, gr.dst, gr.w, gr.n, gr.directed, device=0, rank=rank, world=world,
+                                host_allgather=ag)
+            cl.cleora_init(G, d, 0)
+            for k in calls:
+                cl.cleora_iterate(G, k)
+            info = cl.cleora_info(G)
+            T = cl.cleora_fetch(G)
+            res.append((gr.name, d, calls, info["exchange"], info["shard_begin"], info["shard_end"],
+                        cl.cleora_ipc_opens() - opens0, T.tobytes()))
+            if rank == 0:
+                G.close()                 # rank 1 still maps this rank's blocks (returned to the cache)
+            dist.barrier()
+            if rank == 1:
+                T2 = cl.cleora_fetch(G)   # its own replica is untouched by rank 0's destroy
+                assert T2.tobytes() == T.tobytes()
+                G.close()
+            dist.barrier()
+        # 1-GPU references, computed by rank 0 in its own process
+        if rank == 0:
+            for gr, d, calls in ((g, 256, [3]), (u, 1024, [4]), (u, 64, [4])):
+                G = cl.cleora_build(gr.src, gr.dst, gr.w, gr.n, gr.directed, device=0)
+                cl.cleora_init(G, d, 0)
+                cl.cleora_iterate(G, sum(calls))
+                out[(gr.name, d)] = cl.cleora_fetch(G).tobytes()
+                G.close()
+        q.put((rank, res, out))
+    except Exception as e:  # report instead of hanging the parent
+        import traceback
+        q.put((rank, "error", traceback.format_exc() + repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_one_gpu_peer_exchange():
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(2):
+        rank, res, out = q.get(timeout=900)
+        assert res != "error", out
+        got[rank] = (res, out)
+    for p in procs:
+        p.join(timeout=120)
+    refs = got[0][1]
+    for rank in (0, 1):
+        res = got[rank][0]
+        for i, (name, d, calls, mode, b, e, opens, T) in enumerate(res):
+            assert mode == 2, f"rank {rank}: exchange mode {mode}, expected fused peer stores (2)"
+            assert T == refs[(name, d)], f"rank {rank} {name} d={d} calls={calls}: differs from 1 GPU"
+            if i == 1:      # same graph and d as case 0: the peer's blocks come back from its cache
+                assert opens == 0, f"rank {rank}: {opens} new IPC mappings for a repeated handle"
+        assert res[0][4] == (0 if rank == 0 else res[0][4]) and res[0][5] > res[0][4]
