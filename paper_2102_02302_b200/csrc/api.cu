@@ -424,7 +424,7 @@ struct cleora_graph {
     // (rep[rank] aliases T), sched_p[p] = rank p's schedule
     std::vector<std::array<float*, 2>> rep;
     std::vector<Schedule> sched_p;
-    int64_t max_items = 0;
+    int64_t max_items = 0;          // partial-vector slots the schedule(s) may use (upper bound)
     int sched_thresh = -1;          // heavy_thresh the current schedule(s) were built with
     int chunk_rows = kChunkRows;    // light-chunk row cap for the current gather engine
     int sched_rows = -1;            // chunk_rows the current schedule(s) were built with
@@ -606,6 +606,7 @@ void free_schedules(cleora_graph* g) {
         dfree(sc.counters, g->stream);
         dfree(sc.work, g->stream);
         dfree(sc.light_start, g->stream);
+        dfree(sc.counts, g->stream);
         sc = Schedule();
     };
     if (g->sched_p.empty()) {
@@ -625,15 +626,15 @@ Status make_schedules(cleora_graph* g) {
     free_schedules(g);
     if (!g->sched_p.empty()) {
         for (int p = 0; p < g->world; p++) {
-            CL_TRY(build_schedule(g->of(p).row_ptr, g->n, g->cuts[p], g->cuts[p + 1], g->heavy_thresh, g->chunk_rows,
-                                  g->stream, &g->sched_p[p]));
-            g->max_items = std::max(g->max_items, g->sched_p[p].n_items);
+            CL_TRY(build_schedule(g->of(p).row_ptr, g->n, g->cuts[p], g->cuts[p + 1], g->of(p).nnz,
+                                  g->of(p).max_degree, g->heavy_thresh, g->chunk_rows, g->stream, &g->sched_p[p]));
+            g->max_items = std::max(g->max_items, g->sched_p[p].n_slots_max);
         }
         g->sched = g->sched_p[g->rank];
     } else {
-        CL_TRY(build_schedule(g->own().row_ptr, g->n, g->r0, g->r1, g->heavy_thresh, g->chunk_rows, g->stream,
-                              &g->sched));
-        g->max_items = g->sched.n_items;
+        CL_TRY(build_schedule(g->own().row_ptr, g->n, g->r0, g->r1, g->own().nnz, g->own().max_degree, g->heavy_thresh,
+                              g->chunk_rows, g->stream, &g->sched));
+        g->max_items = g->sched.n_slots_max;
     }
     g->sched_thresh = g->heavy_thresh;
     g->sched_rows = g->chunk_rows;
@@ -901,8 +902,10 @@ Status build_body(const int32_t* src, const int32_t* dst, const float* w, int64_
         CL_TRY(build_csr(dsrc, ddst, dw, E, N, directed, g->stream, &b, &bx));
         trace("build: csr", g->stream, true);
         g->csr.assign(1, Csr());
-        g->csr[0] = Csr{b.row_ptr, b.col, b.val, b.deg, b.d_scal, b.nnz};
+        g->csr[0] = Csr{b.row_ptr, b.col, b.val, b.deg, b.d_scal, b.nnz, b.zero_rows, b.max_degree};
         g->nnz = b.nnz;
+        g->zero_rows = b.zero_rows;
+        g->max_degree = b.max_degree;
         g->cuts[1] = N;
     } else {
         // row-sharded: cuts from every row's entry count, then only this rank's rows
@@ -920,7 +923,7 @@ Status build_body(const int32_t* src, const int32_t* dst, const float* w, int64_
             bp.shard_entries = ent[p + 1] - ent[p];
             BuildOut b;
             CL_TRY(build_csr(dsrc, ddst, dw, E, N, directed, g->stream, &b, &bp));
-            g->of(p) = Csr{b.row_ptr, b.col, b.val, b.deg, b.d_scal, b.nnz};
+            g->of(p) = Csr{b.row_ptr, b.col, b.val, b.deg, b.d_scal, b.nnz, b.zero_rows, b.max_degree};
         }
         trace("build: shard csr", g->stream, true);
     }
@@ -984,8 +987,9 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
     if (g->world > 1 && st.good()) {
         // the whole M's facts: entries, rows without entries, longest row -- summed / maxed over the shards
         std::vector<unsigned long long> f(3 * g->csr.size());
-        for (size_t p = 0; p < g->csr.size() && st.good(); p++) {
-            st = read_small(&f[3 * p], g->csr[p].d_scal + 2, 2 * sizeof(unsigned long long), g->stream);
+        for (size_t p = 0; p < g->csr.size(); p++) {
+            f[3 * p] = (unsigned long long)g->csr[p].zero_rows;
+            f[3 * p + 1] = (unsigned long long)g->csr[p].max_degree;
             f[3 * p + 2] = (unsigned long long)g->csr[p].nnz;
         }
         if (st.good() && !loopback) {
@@ -1235,7 +1239,7 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     // every sequential fp32 run stays <= 256 terms (256-entry blocks keep the error ~3e-7)
     g->gmode = gather_mode(dp);
     g->heavy_thresh = heavy_thresh_default(g->gmode == kGatherBulk ? 64 : 256);
-    // light-chunk row cap per gather engine and row size (measured, scripts/chunk_sweep*.sh, min
+    // light-chunk row cap per gather engine and row size (measured, scripts/r01/chunk_sweep*.sh, min
     // launch ms): TMA bulk (d = 1024) 6 rows, c3 2.04 -> 1.42 vs 31; cp.async at d = 512 12 rows, c3
     // 0.86 -> 0.75; cp.async at d = 256 31 rows (c3 0.518 vs 0.581 at 8); LDG at d <= 128 16 rows,
     // f4 1.39 -> 1.25, c3@128 0.508 -> 0.490, c4@128 4.296 -> 4.306
@@ -1265,7 +1269,9 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
         const char* e = getenv("CLEORA_HOT_MB");
         const int64_t budget = (int64_t)(e ? atof(e) : 72.0) * 1024 * 1024;
         Status s = Status::ok();
-        for (size_t p = 0; p < g->csr.size() && s.good(); p++)
+        // T within the budget: everything fits in L2 anyway, nothing to pin (and no host round trip)
+        if ((int64_t)g->n * dp * 4 <= budget) g->n_hot = 0;
+        for (size_t p = 0; p < g->csr.size() && s.good() && (int64_t)g->n * dp * 4 > budget; p++)
             s = hot_tag(g->csr[p].col, g->csr[p].nnz, g->n, (int64_t)dp * 4, budget, g->stream, &g->n_hot, &g->n_ref,
                         g->directed || g->sharded ? nullptr : g->csr[p].row_ptr, g->indeg);
         if (!s.good()) {
@@ -1327,7 +1333,8 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
             a.r1 = g->cuts[p + 1];
             a.heavy_thresh = g->heavy_thresh;
             a.items = sc.items;
-            a.n_items = sc.n_items;
+            a.counts = sc.counts;
+            a.n_items_max = sc.n_items_max;
             a.partials = g->partials;
             a.counters = sc.counters;
             // with hot rows pinned (power-law graphs) the other gathers are evicted first; without
@@ -1335,7 +1342,6 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
             a.cold_first = g->env_cold_first >= 0 ? g->env_cold_first : (g->n_hot > 0 ? 1 : 0);
             a.work = sc.work;
             a.light_start = sc.light_start;
-            a.n_light = sc.n_light;
             a.n_peers = 0;
             for (int q = 0; q < kMaxPeers; q++) a.peer_out[q] = nullptr;
             if (g->xmode == X_LOOPBACK) {
@@ -1534,10 +1540,10 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
         if (st.good()) st = read_small(&tail[1], b.row_ptr + N2, sizeof(int64_t), s);
         if (st.good() && tail[1] != tail[0]) st = Status::make(3, "cleora_reconstruct: new_idx outside [0, n_new)");
     }
-    if (st.good()) st = build_schedule(b.row_ptr, N2, 0, n_new, g->heavy_thresh, g->chunk_rows, s, &sc);
+    if (st.good()) st = build_schedule(b.row_ptr, N2, 0, n_new, b.nnz, b.max_degree, g->heavy_thresh, g->chunk_rows, s, &sc);
     if (st.good()) st = dalloc((void**)&Tnew, (size_t)n_new * g->dp * sizeof(float), s, "reconstructed rows");
-    if (st.good() && sc.n_items > 0)
-        st = dalloc((void**)&parts, (size_t)sc.n_items * g->dp * sizeof(float), s, "reconstruct partials");
+    if (st.good() && sc.n_slots_max > 0)
+        st = dalloc((void**)&parts, (size_t)sc.n_slots_max * g->dp * sizeof(float), s, "reconstruct partials");
     if (st.good()) {
         SpmmArgs a;
         a.row_ptr = b.row_ptr;
@@ -1550,12 +1556,12 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
         a.r1 = n_new;
         a.heavy_thresh = g->heavy_thresh;
         a.items = sc.items;
-        a.n_items = sc.n_items;
+        a.counts = sc.counts;
+        a.n_items_max = sc.n_items_max;
         a.partials = parts;
         a.counters = sc.counters;
         a.work = sc.work;
         a.light_start = sc.light_start;
-        a.n_light = sc.n_light;
         a.cold_first = 0;
         a.n_peers = 0;
         for (int q = 0; q < kMaxPeers; q++) a.peer_out[q] = nullptr;
@@ -1579,6 +1585,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
     dfree(sc.counters, s);
     dfree(sc.work, s);
     dfree(sc.light_start, s);
+    dfree(sc.counts, s);
     dfree(b.row_ptr, s);
     dfree(b.col, s);
     dfree(b.val, s);
@@ -1669,18 +1676,19 @@ int cleora_info(cleora_graph* g, cleora_info_t* o) {
     o->d = g->d;
     o->d_stride = g->dp;
     o->iterations = g->iters;
-    if (g->zero_rows < 0 && !g->csr.empty() && g->csr[0].d_scal) {
-        DeviceGuard g0(g->device);
-        unsigned long long f[2] = {0, 0};
-        Status s = read_small(f, g->csr[0].d_scal + 2, sizeof f, g->stream);
-        if (!s.good()) return fail(s);
-        g->zero_rows = (int64_t)f[0];
-        g->max_degree = (int64_t)f[1];
-    }
     o->zero_rows = g->zero_rows;
     o->max_degree = g->max_degree;
-    o->heavy_rows = g->sched.n_heavy_rows;
-    o->heavy_items = g->sched.n_items;
+    if (g->sched.counts && g->sched.n_items < 0) {      // schedule counts: on the device until asked for
+        DeviceGuard g0(g->device);
+        int64_t c[4] = {0, 0, 0, 0};
+        Status s = read_small(c, g->sched.counts, sizeof c, g->stream);
+        if (!s.good()) return fail(s);
+        g->sched.n_light = c[0];
+        g->sched.n_items = c[1];
+        g->sched.n_heavy_rows = c[2];
+    }
+    o->heavy_rows = std::max<int64_t>(0, g->sched.n_heavy_rows);
+    o->heavy_items = std::max<int64_t>(0, g->sched.n_items);
     o->shard_begin = g->r0;
     o->shard_end = g->r1;
     o->rank = g->rank;
@@ -1692,8 +1700,8 @@ int cleora_info(cleora_graph* g, cleora_info_t* o) {
     o->exchange = g->xmode;
     o->device_bytes = g->bytes + ((g->T[0] ? 1 : 0) + (g->T[1] ? 1 : 0)) * (int64_t)g->n * g->dp * 4 +
                       (int64_t)g->partials_floats * 4 +
-                      g->sched.n_items * (int64_t)sizeof(HeavyItem) + g->sched.n_heavy_rows * 4 +
-                      (g->sched.light_start ? (g->sched.n_light + 1) * 8 : 0);
+                      g->sched.n_items_max * (int64_t)sizeof(HeavyItem) + g->sched.n_slots_max * 4 +
+                      (g->sched.light_start ? (g->r1 - g->r0 + 1) * 8 : 0);
     DeviceGuard guard(g->device);
     cudaError_t e = cudaStreamSynchronize(g->stream);
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_info: ") + cudaGetErrorString(e)));

@@ -9,6 +9,8 @@
 //   B3 deg(a) = fp64 sum of e_ab over ascending b     -> one warp per row, sequential fold
 //   B4 val    = fp32_rn(e_ab / deg(a))                -> IEEE double divide, one rounding
 // This translation unit must not be compiled with --use_fast_math.
+#include <algorithm>
+
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -82,11 +84,15 @@ __global__ void k_head_flags(const uint64_t* __restrict__ keys, int64_t n, uint6
 
 // B2: one thread per (a,b) run: sequential fp64 sum in stable order.
 // keys are (src - row_lo) * N + dst (row_lo = the first row of the shard, 0 for a whole graph)
+// nnz (runs) and the dropped-entry count are read on the device: the build reads nothing back before
+// its last kernel (grids are sized for every entry)
 __global__ void k_merge_runs(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ pos,
-                             const int64_t* __restrict__ run_start, int64_t nnz, int64_t n_valid,
+                             const int64_t* __restrict__ run_start, const unsigned long long* __restrict__ d_nnz,
+                             const unsigned long long* __restrict__ d_ndrop, int64_t n_ent,
                              const float* __restrict__ w, int64_t E, int32_t N, int32_t row_lo,
                              int32_t* __restrict__ rows, int32_t* __restrict__ col, double* __restrict__ e_ab) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t nnz = (int64_t)*d_nnz, n_valid = n_ent - (int64_t)*d_ndrop;
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nnz; u += stride) {
         int64_t s = run_start[u], e = (u + 1 < nnz) ? run_start[u + 1] : n_valid;
         uint64_t k = keys[s];
@@ -106,8 +112,12 @@ __global__ void k_merge_runs(const uint64_t* __restrict__ keys, const uint32_t* 
 }
 
 // row_ptr from the row of each (sorted) unique entry; deterministic, no atomics.
-__global__ void k_row_ptr(const int32_t* __restrict__ rows, int64_t nnz, int32_t N, int64_t* __restrict__ row_ptr) {
+__global__ void k_row_ptr(const int32_t* __restrict__ rows, const unsigned long long* __restrict__ d_nnz, int32_t N,
+                          int64_t* __restrict__ row_ptr) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t nnz = (int64_t)*d_nnz;
+    if (nnz == 0)                                  // no entries at all (an empty chunk or shard)
+        for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= N; r += stride) row_ptr[r] = 0;
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nnz; u += stride) {
         int32_t r = rows[u];
         int32_t prev = (u == 0) ? -1 : rows[u - 1];
@@ -214,8 +224,10 @@ __global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __re
 
 // B4: val = fp32_rn(e_ab / deg(a)).
 __global__ void k_values(const int32_t* __restrict__ rows, const double* __restrict__ e_ab,
-                         const double* __restrict__ deg, int64_t nnz, float* __restrict__ val) {
+                         const double* __restrict__ deg, const unsigned long long* __restrict__ d_nnz,
+                         float* __restrict__ val) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t nnz = (int64_t)*d_nnz;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride)
         val[k] = __double2float_rn(e_ab[k] / deg[rows[k]]);
 }
@@ -241,31 +253,46 @@ __global__ void k_put_end(int64_t* __restrict__ starts, const int64_t* __restric
     starts[*n] = end;
 }
 
-__global__ void k_items_per_row(const int64_t* __restrict__ rp, const int64_t* __restrict__ hrows, int64_t nh,
-                                int64_t per_item, int64_t* __restrict__ nit) {
+// h < *nh (heavy rows found): items of the row, and its partial-vector slots (multi-part rows only);
+// h in [*nh, nh_max]: 0, so the scans' last entries are the totals
+__global__ void k_items_per_row(const int64_t* __restrict__ rp, const int64_t* __restrict__ hrows,
+                                const int64_t* __restrict__ nh, int64_t nh_max, int64_t per_item,
+                                int64_t* __restrict__ nit, int64_t* __restrict__ nsl) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride) {
-        int64_t r = hrows[h];
-        int64_t c = rp[r + 1] - rp[r];
-        nit[h] = (c + per_item - 1) / per_item;
+    const int64_t n = *nh;
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h <= nh_max; h += stride) {
+        int64_t c = 0;
+        if (h < n) {
+            const int64_t r = hrows[h];
+            c = (rp[r + 1] - rp[r] + per_item - 1) / per_item;
+        }
+        nit[h] = c;
+        nsl[h] = c > 1 ? c : 0;
     }
 }
 
-__global__ void k_fill_items(const int64_t* __restrict__ rp, const int64_t* __restrict__ hrows, int64_t nh,
-                             const int64_t* __restrict__ first, int64_t per_item, HeavyItem* __restrict__ items) {
+__global__ void k_fill_items(const int64_t* __restrict__ rp, const int64_t* __restrict__ hrows,
+                             const int64_t* __restrict__ nh, int64_t nh_max, const int64_t* __restrict__ first,
+                             const int64_t* __restrict__ sfirst, int64_t per_item, HeavyItem* __restrict__ items,
+                             int64_t* __restrict__ counts) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride) {
-        int64_t r = hrows[h];
-        int64_t k0 = rp[r], k1 = rp[r + 1];
-        int64_t n = (k1 - k0 + per_item - 1) / per_item;
-        for (int64_t p = 0; p < n; p++) {
+    const int64_t n = *nh;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        counts[1] = first[nh_max];                // totals (inputs past *nh are 0)
+        counts[3] = sfirst[nh_max];
+    }
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < n; h += stride) {
+        const int64_t r = hrows[h];
+        const int64_t k0 = rp[r], k1 = rp[r + 1];
+        const int64_t np = (k1 - k0 + per_item - 1) / per_item;
+        for (int64_t p = 0; p < np; p++) {
             HeavyItem it;
             it.k0 = k0 + p * per_item;
             it.k1 = min(k1, it.k0 + per_item);
             it.row = (int32_t)r;
             it.part = (int32_t)p;
-            it.nparts = (int32_t)n;
-            it.hrow = (int32_t)h;
+            it.nparts = (int32_t)np;
+            it.slot = np > 1 ? (int32_t)(sfirst[h] + p) : -1;
             items[first[h] + p] = it;
         }
     }
@@ -511,34 +538,19 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         count_launches(2);
     }
     dfree(flags.release(), s);
-    // one host round trip: validation verdict (first bad edge, dropped entries, kind) and run count
-    unsigned long long h_scal[2], h_nnz = 0;
-    int h_kind = 0;
-    {
-        const SmallRead rd[3] = {{h_scal, scal.p, 2 * sizeof(unsigned long long)}, {&h_kind, err_kind.p, sizeof(int)},
-                                 {&h_nnz, scal.p + 4, sizeof h_nnz}};
-        CL_TRY(read_small_n(rd, 3, s));
-    }
-    if (h_kind) {
-        char buf[256];
-        snprintf(buf, sizeof buf, "cleora_build: edge %llu: %s", (unsigned long long)h_scal[0],
-                 (h_kind & 1) ? (x.dst_limit >= 0 ? "node id outside its range" : "node id outside [0, n_nodes)")
-                              : "weight not finite or <= 0");
-        return Status::make(3, buf);
-    }
-    const int64_t n_valid = n_ent - (int64_t)h_scal[1];
-    const int64_t nnz = (int64_t)h_nnz;
     trace("csr: run select", s, false);
 
+    // the merged entries are at most the sorted ones: everything below is sized for n_ent and reads the
+    // real count (scal[4]) on the device, so the build's only host round trip comes after its last kernel
     DevBuf<int32_t> rows, col;
     DevBuf<double> e_ab, deg;
     DevBuf<int64_t> row_ptr;
     DevBuf<float> val;
-    CL_TRY(rows.alloc(nnz, s, "entry rows"));
-    CL_TRY(col.alloc(nnz, s, "CSR col"));
-    CL_TRY(e_ab.alloc(nnz, s, "e_ab"));
-    k_merge_runs<<<grid_for(nnz, 4), kThreads, 0, s>>>(keys.p, pos.p, run_start.p, nnz, n_valid, d_w, E, N, lo,
-                                                       rows.p, col.p, e_ab.p);
+    CL_TRY(rows.alloc(n_ent, s, "entry rows"));
+    CL_TRY(col.alloc(n_ent, s, "CSR col"));
+    CL_TRY(e_ab.alloc(n_ent, s, "e_ab"));
+    k_merge_runs<<<grid_for(n_ent, 4), kThreads, 0, s>>>(keys.p, pos.p, run_start.p, scal.p + 4, scal.p + 1, n_ent, d_w,
+                                                         E, N, lo, rows.p, col.p, e_ab.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     trace("csr: merge runs", s, true);
@@ -548,9 +560,8 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     dfree(pos2.release(), s);
 
     CL_TRY(row_ptr.alloc((size_t)N + 1, s, "CSR row_ptr"));
-    // k_row_ptr fills row_ptr[1..N] from the entries; with no entries at all (an empty chunk) it is all 0
-    CL_CUDA_TRY(cudaMemsetAsync(row_ptr.p, 0, nnz == 0 ? ((size_t)N + 1) * sizeof(int64_t) : sizeof(int64_t), s));
-    k_row_ptr<<<grid_for(nnz, 4), kThreads, 0, s>>>(rows.p, nnz, N, row_ptr.p);
+    CL_CUDA_TRY(cudaMemsetAsync(row_ptr.p, 0, sizeof(int64_t), s));
+    k_row_ptr<<<grid_for(n_ent, 4), kThreads, 0, s>>>(rows.p, scal.p + 4, N, row_ptr.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
 
@@ -566,11 +577,29 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     trace("csr: degree", s, true);
-    CL_TRY(val.alloc(nnz, s, "CSR val"));
-    k_values<<<grid_for(nnz, 4), kThreads, 0, s>>>(rows.p, e_ab.p, deg.p, nnz, val.p);
+    CL_TRY(val.alloc(n_ent, s, "CSR val"));
+    k_values<<<grid_for(n_ent, 4), kThreads, 0, s>>>(rows.p, e_ab.p, deg.p, scal.p + 4, val.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
-    out->nnz = nnz;
+    // one host round trip: validation verdict (first bad edge, kind) and the graph's facts (entries,
+    // rows without entries, longest row).  On invalid input the work above ran on placeholder ids
+    // (0) and is simply discarded.
+    unsigned long long h_scal[5] = {0, 0, 0, 0, 0};
+    int h_kind = 0;
+    {
+        const SmallRead rd[2] = {{h_scal, scal.p, 5 * sizeof(unsigned long long)}, {&h_kind, err_kind.p, sizeof(int)}};
+        CL_TRY(read_small_n(rd, 2, s));
+    }
+    if (h_kind) {
+        char buf[256];
+        snprintf(buf, sizeof buf, "cleora_build: edge %llu: %s", (unsigned long long)h_scal[0],
+                 (h_kind & 1) ? (x.dst_limit >= 0 ? "node id outside its range" : "node id outside [0, n_nodes)")
+                              : "weight not finite or <= 0");
+        return Status::make(3, buf);
+    }
+    out->nnz = (int64_t)h_scal[4];
+    out->zero_rows = (int64_t)h_scal[2];
+    out->max_degree = (int64_t)h_scal[3];
     out->d_scal = scal.release();
     out->row_ptr = row_ptr.release();
     out->col = col.release();
@@ -579,22 +608,25 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     return Status::ok();
 }
 
-Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int heavy_thresh, int chunk_rows,
-                      cudaStream_t s, Schedule* out) {
+Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int64_t nnz, int64_t max_degree,
+                      int heavy_thresh, int chunk_rows, cudaStream_t s, Schedule* out) {
     (void)N;
     const int64_t nr = r1 - r0;
-    out->n_heavy_rows = 0;
-    out->n_items = 0;
-    out->items = nullptr;
-    out->counters = nullptr;
+    *out = Schedule();
     {
         DevBuf<unsigned> work;
+        DevBuf<int64_t> counts;
         CL_TRY(work.alloc(4, s, "work tickets"));
+        CL_TRY(counts.alloc(4, s, "schedule counts"));
         CL_CUDA_TRY(cudaMemsetAsync(work.p, 0, 4 * sizeof(unsigned), s));
+        CL_CUDA_TRY(cudaMemsetAsync(counts.p, 0, 4 * sizeof(int64_t), s));
         out->work = work.release();
+        out->counts = counts.release();
     }
-    if (nr <= 0) return Status::ok();
-    DevBuf<int64_t> cnt1;                 // number of light chunks
+    if (nr <= 0) {
+        out->n_heavy_rows = out->n_items = out->n_light = 0;
+        return Status::ok();
+    }
     {
         // light chunks (see Schedule); window from CLEORA_CHUNK_ENTRIES, default 1024 entries
         const char* e = getenv("CLEORA_CHUNK_ENTRIES");
@@ -602,7 +634,6 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         if (win < 1) win = 1;
         DevBuf<int64_t> starts;
         CL_TRY(starts.alloc(nr + 1, s, "light chunk starts"));
-        CL_TRY(cnt1.alloc(1, s, "scalars"));
         thrust::counting_iterator<int64_t> it(r0);
         // small graphs: fewer rows per chunk, so that every warp of the persistent grid gets work
         // (c1, 10k rows: 31-row chunks left most of the 2,368 warps idle and one warp walked 31
@@ -621,66 +652,66 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         if (rows > cap) rows = cap;
         IsChunkStart pred{d_row_ptr, r0, win, rows};
         size_t tmp_bytes = 0;
-        CL_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, it, starts.p, cnt1.p, nr, pred, s));
+        CL_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, it, starts.p, out->counts + 0, nr, pred, s));
         DevBuf<uint8_t> tmp;
         CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
-        CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, starts.p, cnt1.p, nr, pred, s));
-        k_put_end<<<1, 1, 0, s>>>(starts.p, cnt1.p, r1);       // starts[n_light] = r1
+        CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, starts.p, out->counts + 0, nr, pred, s));
+        k_put_end<<<1, 1, 0, s>>>(starts.p, out->counts + 0, r1);       // starts[n_light] = r1
         CL_CUDA_TRY(cudaGetLastError());
         count_launches(3);
         out->light_start = starts.release();
     }
-    DevBuf<int64_t> hrows, cnt;
+    // heavy rows: at most nnz / (heavy_thresh + 1) of them
+    const int64_t nh_max = max_degree <= heavy_thresh ? 0 : std::min(nr, nnz / ((int64_t)heavy_thresh + 1));
+    if (nh_max == 0) {
+        out->n_heavy_rows = out->n_items = 0;
+        return Status::ok();
+    }
+    const int64_t per_item = (int64_t)heavy_thresh * kWarpsPerCta;
+    DevBuf<int64_t> hrows;
     CL_TRY(hrows.alloc(nr, s, "heavy rows"));
-    CL_TRY(cnt.alloc(2, s, "scalars"));
     {
         thrust::counting_iterator<int64_t> it(r0);
         IsHeavy pred{d_row_ptr, heavy_thresh};
         size_t tmp_bytes = 0;
-        CL_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, it, hrows.p, cnt.p, nr, pred, s));
+        CL_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, it, hrows.p, out->counts + 2, nr, pred, s));
         DevBuf<uint8_t> tmp;
         CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
-        CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, hrows.p, cnt.p, nr, pred, s));
+        CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, hrows.p, out->counts + 2, nr, pred, s));
         count_launches(2);
     }
-    int64_t nl = 0, nh = 0;   // both counts in one host round trip
-    {
-        const SmallRead rd[2] = {{&nl, cnt1.p, sizeof nl}, {&nh, cnt.p, sizeof nh}};
-        CL_TRY(read_small_n(rd, 2, s));
-    }
-    out->n_light = nl;
-    out->n_heavy_rows = nh;
-    if (nh == 0) return Status::ok();
-    const int64_t per_item = (int64_t)heavy_thresh * kWarpsPerCta;
-    DevBuf<int64_t> nit, first;
-    CL_TRY(nit.alloc(nh, s, "items per heavy row"));
-    CL_TRY(first.alloc(nh, s, "first item"));
-    k_items_per_row<<<grid_for(nh), kThreads, 0, s>>>(d_row_ptr, hrows.p, nh, per_item, nit.p);
+    DevBuf<int64_t> nit, nsl, first, sfirst;
+    CL_TRY(nit.alloc(nh_max + 1, s, "items per heavy row"));
+    CL_TRY(nsl.alloc(nh_max + 1, s, "slots per heavy row"));
+    CL_TRY(first.alloc(nh_max + 1, s, "first item"));
+    CL_TRY(sfirst.alloc(nh_max + 1, s, "first slot"));
+    k_items_per_row<<<grid_for(nh_max + 1), kThreads, 0, s>>>(d_row_ptr, hrows.p, out->counts + 2, nh_max, per_item,
+                                                              nit.p, nsl.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     {
-        size_t tmp_bytes = 0;
-        CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, nit.p, first.p, nh, s));
+        size_t tb1 = 0, tb2 = 0;
+        CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb1, nit.p, first.p, nh_max + 1, s));
+        CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb2, nsl.p, sfirst.p, nh_max + 1, s));
         DevBuf<uint8_t> tmp;
-        CL_TRY(tmp.alloc(tmp_bytes, s, "scan temp"));
-        CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, nit.p, first.p, nh, s));
-        count_launches(2);
+        CL_TRY(tmp.alloc(std::max(tb1, tb2), s, "scan temp"));
+        CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tb1, nit.p, first.p, nh_max + 1, s));
+        CL_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, nsl.p, sfirst.p, nh_max + 1, s));
+        count_launches(4);
     }
-    int64_t last[2];
-    {
-        const SmallRead rd[2] = {{&last[0], first.p + nh - 1, sizeof(int64_t)}, {&last[1], nit.p + nh - 1, sizeof(int64_t)}};
-        CL_TRY(read_small_n(rd, 2, s));
-    }
-    const int64_t n_items = last[0] + last[1];
+    // upper bounds: every item but a row's last holds per_item entries; a row of several parts has
+    // more than per_item entries, so its parts are fewer than 2 * entries / per_item
+    out->n_items_max = nh_max + nnz / per_item + 1;
+    out->n_slots_max = 2 * (nnz / per_item) + 1;
     DevBuf<HeavyItem> items;
     DevBuf<unsigned> counters;
-    CL_TRY(items.alloc(n_items, s, "heavy items"));
-    CL_TRY(counters.alloc(nh, s, "heavy counters"));
-    CL_CUDA_TRY(cudaMemsetAsync(counters.p, 0, nh * sizeof(unsigned), s));
-    k_fill_items<<<grid_for(nh), kThreads, 0, s>>>(d_row_ptr, hrows.p, nh, first.p, per_item, items.p);
+    CL_TRY(items.alloc(out->n_items_max, s, "heavy items"));
+    CL_TRY(counters.alloc(out->n_slots_max, s, "heavy counters"));
+    CL_CUDA_TRY(cudaMemsetAsync(counters.p, 0, out->n_slots_max * sizeof(unsigned), s));
+    k_fill_items<<<grid_for(nh_max), kThreads, 0, s>>>(d_row_ptr, hrows.p, out->counts + 2, nh_max, first.p, sfirst.p,
+                                                       per_item, items.p, out->counts);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
-    out->n_items = n_items;
     out->items = items.release();
     out->counters = counters.release();
     return Status::ok();

@@ -67,11 +67,12 @@ __host__ __device__ __forceinline__ uint64_t sm64(uint64_t z) {
 
 // ---------------------------------------------------------------- schedule
 // A CTA work item of the heavy path: entries [k0, k1) of row `row`, which is part `part`
-// of `nparts` of that row; `hrow` indexes the row's completion counter; the partial vector
-// of item i lives at partials + i * dp.
+// of `nparts` of that row.  Rows of several parts: the item's partial vector lives at partials +
+// slot * dp (the row's parts have consecutive slots), the row's completion counter at
+// counters[slot - part]; single-part rows need neither (slot = -1).
 struct HeavyItem {
     int64_t k0, k1;
-    int32_t row, part, nparts, hrow;
+    int32_t row, part, nparts, slot;
 };
 static_assert(sizeof(HeavyItem) == 32, "HeavyItem layout");
 
@@ -90,12 +91,12 @@ struct SpmmArgs {
     int64_t r0, r1;         // rows this launch computes on the light path (shard)
     int32_t heavy_thresh;   // rows with more entries than this are on the heavy path
     const HeavyItem* items;
-    int64_t n_items;
-    float* partials;        // n_items * dp floats
-    unsigned* counters;     // one per heavy row, 0 between launches
+    const int64_t* counts;  // schedule counts on the device (Schedule::counts): [0] light chunks, [1] items
+    int64_t n_items_max;    // host upper bound of counts[1] (0: no heavy rows possible)
+    float* partials;        // partial-vector slots * dp floats
+    unsigned* counters;     // completion counters of multi-part rows, 0 between launches
     unsigned* work;         // 3 work tickets of the persistent kernel, 0 between launches
     const int64_t* light_start;   // light chunks (Schedule::light_start)
-    int64_t n_light;
     int32_t cold_first;     // TMA path: gathers of non-hot rows with evict_first (else evict_normal)
     // Fused exchange (multi-GPU): every finished row is also stored into the T_out replicas of
     // the other ranks -- NVLink peer pointers opened through CUDA IPC, or, in loopback
@@ -128,6 +129,7 @@ struct Csr {
     double* deg = nullptr;
     unsigned long long* d_scal = nullptr;   // build scalars ([2] zero rows of its rows, [3] max degree)
     int64_t nnz = 0;
+    int64_t zero_rows = 0, max_degree = 0;  // of its rows (read back with the build's verdict)
 };
 
 // build.cu
@@ -137,9 +139,10 @@ struct BuildOut {
     int32_t* col = nullptr;
     float* val = nullptr;
     double* deg = nullptr;
-    // device scalars of the build ([2] rows without entries, [3] largest row), left on the device so
-    // that the build needs no host round trip after its last kernel; the caller frees the buffer
+    // device scalars of the build ([2] rows without entries, [3] largest row, [4] nnz); the caller
+    // frees the buffer.  Their host copies come back with the build's one readback, after its last kernel.
     unsigned long long* d_scal = nullptr;
+    int64_t zero_rows = 0, max_degree = 0;
 };
 // Optional parts of a build: keep only the edges of chunk `chunk` of `n_chunks` (Algorithm 1
 // line 1, reading R13), count every node's endpoint occurrences among the kept edges (reading
@@ -163,16 +166,20 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
 // ticket's work is bounded in rows (row pointers fit one register per lane) and in entries
 // (no long tail behind a chunk of medium-degree rows).
 constexpr int kChunkRows = 31;
+// Built without a host round trip: the counts stay on the device (read by the SpMM kernels; read back
+// only by cleora_info), the arrays are sized by host upper bounds.
 struct Schedule {
-    int64_t n_heavy_rows = 0, n_items = 0;
+    int64_t n_items_max = 0, n_slots_max = 0;   // host upper bounds: items, partial-vector slots
+    int64_t n_heavy_rows = -1, n_items = -1, n_light = -1;   // host copies of counts, -1: not read yet
     HeavyItem* items = nullptr;
-    unsigned* counters = nullptr;
+    unsigned* counters = nullptr;   // [n_slots_max]
     unsigned* work = nullptr;   // [4] persistent-kernel tickets
-    int64_t* light_start = nullptr;   // [n_light + 1]
-    int64_t n_light = 0;
+    int64_t* light_start = nullptr;   // [n_light + 1] (allocated for r1 - r0 + 1)
+    int64_t* counts = nullptr;  // device: [0] light chunks, [1] items, [2] heavy rows, [3] partial slots
 };
-Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int heavy_thresh,
-                      int chunk_rows, cudaStream_t s, Schedule* out);
+// nnz: entries of rows [r0, r1), max_degree: their longest row (upper bounds are enough)
+Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int64_t nnz, int64_t max_degree,
+                      int heavy_thresh, int chunk_rows, cudaStream_t s, Schedule* out);
 Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts);
 // Row-sharded builds (world > 1): validate every edge, count every row's entries (mirrored, before
 // merging), cut the rows into `world` shards balanced on those counts (cut p = first row whose entry

@@ -272,7 +272,7 @@ __device__ void heavy_item(const SpmmArgs& a, const Pol& pol, int64_t idx, float
     const int64_t sub = (len + kWarpsPerCta - 1) / kWarpsPerCta;
     const int64_t wk0 = min(it.k0 + warp * sub, it.k1), wk1 = min(wk0 + sub, it.k1);
     const bool single = it.nparts == 1;
-    float4* dst = reinterpret_cast<float4*>(single ? a.T_out + (int64_t)it.row * dp : a.partials + idx * (int64_t)dp);
+    float4* dst = reinterpret_cast<float4*>(single ? a.T_out + (int64_t)it.row * dp : a.partials + (int64_t)it.slot * dp);
 
     float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
     double ss = 0.0;
@@ -315,13 +315,13 @@ __device__ void heavy_item(const SpmmArgs& a, const Pol& pol, int64_t idx, float
     __threadfence();
     __syncthreads();
     if (t == 0) {
-        const unsigned prev = atomicAdd(a.counters + it.hrow, 1u);
+        const unsigned prev = atomicAdd(a.counters + (it.slot - it.part), 1u);
         *flag = (prev == (unsigned)it.nparts - 1) ? 1 : 0;
     }
     __syncthreads();
     if (!*flag) return;
     __threadfence();
-    const int64_t first = idx - it.part;
+    const int64_t first = it.slot - it.part;
     const float4* parts = reinterpret_cast<const float4*>(a.partials + first * (int64_t)dp);
     const int64_t pstride = dp / 4;
     double zx = 0, zy = 0, zz = 0, zw = 0;
@@ -351,7 +351,7 @@ __device__ void heavy_item(const SpmmArgs& a, const Pol& pol, int64_t idx, float
                      make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
         }
     }
-    if (t == 0) a.counters[it.hrow] = 0u;         // ready for the next launch
+    if (t == 0) a.counters[first] = 0u;           // ready for the next launch
 }
 
 // Persistent kernel: one wave of CTAs (SM count x resident CTAs per SM).  Work is handed out
@@ -374,17 +374,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_n
     __shared__ unsigned s_item;
     const int lane = threadIdx.x & 31;
     const Pol pol = make_pol<H>(a);               // once per thread, not per row
-    if (a.n_items > 0) {
+    const int64_t n_items = a.n_items_max > 0 ? a.counts[1] : 0;   // schedule counts live on the device
+    if (n_items > 0) {
         for (;;) {
             if (threadIdx.x == 0) s_item = atomicAdd(a.work + 0, 1u);
             __syncthreads();
             const int64_t it = s_item;
             __syncthreads();
-            if (it >= a.n_items) break;
+            if (it >= n_items) break;
             heavy_item<V, H>(a, pol, it, red, scratch, &flag);
         }
     }
-    const int64_t nchunks = a.n_light;
+    const int64_t nchunks = a.counts[0];
     for (;;) {
         unsigned c = 0;
         if (lane == 0) c = atomicAdd(a.work + 1, 1u);
@@ -466,7 +467,7 @@ Status launch_vh(const SpmmArgs& a, cudaStream_t s) {
         blocks_per_sm = bps[dev];
         sms = nsm[dev];
     }
-    if (a.r1 <= a.r0 && a.n_items == 0) return Status::ok();
+    if (a.r1 <= a.r0 && a.n_items_max == 0) return Status::ok();
     const int grid = sms * blocks_per_sm;                // one persistent wave
     k_spmm_norm<V, H><<<grid, kWarpsPerCta * 32, smem, s>>>(a);
     CL_CUDA_TRY(cudaGetLastError());

@@ -297,18 +297,18 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
         const double inv = inv_norm(tot);
         if (t < nq) put_out4(a, it.row, t, scale4(y, inv));
     } else {
-        float4* part = reinterpret_cast<float4*>(a.partials + idx * (int64_t)dp);
+        float4* part = reinterpret_cast<float4*>(a.partials + (int64_t)it.slot * dp);
         if (t < nq) part[t] = y;
         __threadfence();
         __syncthreads();
         if (t == 0) {
-            const unsigned prev = atomicAdd(a.counters + it.hrow, 1u);
+            const unsigned prev = atomicAdd(a.counters + (it.slot - it.part), 1u);
             *flag = (prev == (unsigned)it.nparts - 1) ? 1 : 0;
         }
         __syncthreads();
         if (*flag) {
             __threadfence();
-            const float4* parts = reinterpret_cast<const float4*>(a.partials + (idx - it.part) * (int64_t)dp);
+            const float4* parts = reinterpret_cast<const float4*>(a.partials + (int64_t)(it.slot - it.part) * dp);
             double zx = 0, zy = 0, zz = 0, zw = 0;
             if (t < nq) {
                 for (int q = 0; q < it.nparts; q++) {     // part order: deterministic
@@ -321,7 +321,7 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
             if (t < nq)
                 put_out4(a, it.row, t,
                          make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
-            if (t == 0) a.counters[it.hrow] = 0u;
+            if (t == 0) a.counters[it.slot - it.part] = 0u;
         }
     }
     __syncthreads();              // red (ring slot 0) is refilled by TMA next: order the generic
@@ -357,17 +357,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
     }
     __syncthreads();
 
-    if (a.n_items > 0) {
+    const int64_t n_items = a.n_items_max > 0 ? a.counts[1] : 0;   // schedule counts live on the device
+    if (n_items > 0) {
         for (;;) {
             if (threadIdx.x == 0) s_item = atomicAdd(a.work + 0, 1u);
             __syncthreads();
             const int64_t it = s_item;
             __syncthreads();
-            if (it >= a.n_items) break;
+            if (it >= n_items) break;
             heavy_item_t<V, FULL, SA>(a, it, r, smem, ring_f4, scratch, &flag);
         }
     }
-    const int64_t nchunks = a.n_light;
+    const int64_t nchunks = a.counts[0];
     float4 acc[V];
 #pragma unroll
     for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -450,7 +451,7 @@ Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
         }
         c = cc;
     }
-    if (a.r1 <= a.r0 && a.n_items == 0) return Status::ok();
+    if (a.r1 <= a.r0 && a.n_items_max == 0) return Status::ok();
     k_spmm_tma<V, FULL, SA><<<c.sms * c.blocks_per_sm, kWarpsPerCta * 32, c.smem, s>>>(a, c.S);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);

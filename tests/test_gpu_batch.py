@@ -68,8 +68,13 @@ def test_batch_equals_separate_runs(cl, directed, weighted, d):
         G.close()
         assert T[rows].tobytes() == alone.tobytes(), f"graph {i} ({g.name}) differs from its own run"
         R = oracle.embed(oracle.build_from(g), d, 5, iters)
-        assert float(np.abs(T[rows].astype(np.float64) - R).max()) <= 1e-5, g.name
+        Tg = T[rows].astype(np.float64)
+        assert float(np.abs(Tg - R).max()) <= 1e-5, g.name
         assert np.array_equal(~T[rows].any(1), ~R.any(1)), g.name
+        nz = R.any(1)                       # BASELINE north star: cosine >= 0.99999 per non-zero row
+        if nz.any():
+            cos = (Tg[nz] * R[nz]).sum(1) / (np.linalg.norm(Tg[nz], axis=1) * np.linalg.norm(R[nz], axis=1))
+            assert float(cos.min()) >= 0.99999, f"{g.name}: min cosine {cos.min()}"
 
 
 def test_batch_id_errors(cl):
