@@ -5,7 +5,7 @@ mkdir -p $out
 export CLEORA_GEN_CACHE=/tmp/cleora_gen
 python -c "import __graft_entry__ as g; g.build()" > $out/build.log 2>&1 || { echo BUILD FAILED; tail -30 $out/build.log; exit 1; }
 if [ -n "$2" ]; then K="-k $2"; else K=""; fi
-CLEORA_SKIP_C5=${SKIP_C5:-1} timeout 2400 python -m pytest tests -m gpu -x -q $K > $out/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $out/pytest.log
+CLEORA_PARITY_LOG=$out/parity.jsonl CLEORA_SKIP_C5=${SKIP_C5:-1} timeout 2400 python -m pytest tests -m gpu -x -q $K > $out/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $out/pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 900 python bench.py > $out/bench.json 2> $out/bench.err; echo "bench rc=$?"
 python - <<'PY' $out/bench.json

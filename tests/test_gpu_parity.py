@@ -125,24 +125,34 @@ def test_schedule_threshold_does_not_change_results(cl, thresh, monkeypatch):
     run_case(cl, g, 256, iters=4)
 
 
+def _record(name, worst):
+    """Worst max|d| / min cosine of a full-config case, printed and (CLEORA_PARITY_LOG=file) logged."""
+    import json
+    line = json.dumps({"config": name, "max_abs": worst[0], "min_cos": worst[1]})
+    print(line)
+    if os.environ.get("CLEORA_PARITY_LOG"):
+        with open(os.environ["CLEORA_PARITY_LOG"], "a") as f:
+            f.write(line + "\n")
+
+
 def test_c1_full(cl):
     g = gen.config("c1")
-    run_case(cl, g, g.d, g.iters)
+    _record("c1", run_case(cl, g, g.d, g.iters))
 
 
 def test_c3_full(cl):
     g = gen.config("c3")
-    run_case(cl, g, g.d, g.iters, per_iter=False)
+    _record("c3", run_case(cl, g, g.d, g.iters, per_iter=False))
 
 
 def test_c2_full(cl):
     g = gen.config("c2")
-    run_case(cl, g, g.d, g.iters, per_iter=False)
+    _record("c2", run_case(cl, g, g.d, g.iters, per_iter=False))
 
 
 def test_c4_full(cl):
     g = gen.config("c4")
-    run_case(cl, g, g.d, g.iters, per_iter=False)
+    _record("c4", run_case(cl, g, g.d, g.iters, per_iter=False))
 
 
 def test_determinism_and_composability(cl):

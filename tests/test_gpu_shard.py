@@ -109,3 +109,34 @@ def test_chunked_sharded_equals_single(cl):
     G1.close()
     for T in _embed(cl, g, 64, [3], loopback=True, world=2, rank=0, n_chunks=3, chunk=1, chunk_seed=5):
         assert T.tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("name,world", [("c2", 4), ("c4", 2)])
+def test_full_size_sharded_bitwise(cl, name, world):
+    """The bench configs row-sharded in loopback (every replica of every emulated rank) against one
+    GPU, bitwise, on row blocks across the graph (host memory: a few GB per replica block)."""
+    import torch
+    g = gen.config(name)
+    dev = torch.device("cuda", 0)
+    src, dst = torch.from_numpy(g.src).to(dev), torch.from_numpy(g.dst).to(dev)
+    w = torch.from_numpy(g.w).to(dev) if g.w is not None else None
+    blocks = [(0, 60000), (g.n // 2, g.n // 2 + 60000), (g.n - 60000, g.n)]
+    G = cl.cleora_build(src, dst, w, g.n, g.directed, device=0)
+    cl.cleora_init(G, g.d, 0)
+    cl.cleora_iterate(G, g.iters)
+    ref = [cl.cleora_fetch(G, a, b) for a, b in blocks]
+    info1 = cl.cleora_info(G)
+    G.close()
+    cl.cleora_release_cached_memory()
+    G = cl.cleora_build(src, dst, w, g.n, g.directed, device=0, loopback=True, world=world, rank=world - 1)
+    try:
+        cl.cleora_init(G, g.d, 0)
+        cl.cleora_iterate(G, g.iters)
+        info = cl.cleora_info(G)
+        assert info["nnz"] == info1["nnz"] and info["zero_rows"] == info1["zero_rows"]
+        for p in range(world):
+            for (a, b), R in zip(blocks, ref):
+                assert cl.cleora_fetch_replica(G, p, a, b).tobytes() == R.tobytes(), f"{name} replica {p} rows [{a},{b})"
+    finally:
+        G.close()
+        cl.cleora_release_cached_memory()
