@@ -637,6 +637,7 @@ def main():
             barrier()
             return max_over_ranks(e0.elapsed_time(e1) / k), 1e3 * (time.perf_counter() - t0) / k
 
+        oom0 = cl.cleora_oom_fallbacks()
         e2e_serial(1)
         if pipelined:
             try:
@@ -660,6 +661,7 @@ def main():
             mode = "serial: build, iterations, blocking fetch, destroy (two handles do not fit in HBM)"
         h2d = g.n_edges * 8 + (g.n_edges * 4 if g.w is not None else 0)
         e2e = {"value": nnz * d * iters / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "oom_fallbacks": cl.cleora_oom_fallbacks() - oom0,
                "d2h_bytes_per_step": g.n * d * 4, "ms_per_step": ms_e2e, "steps": k2, "wall_ms_per_step": wall,
                "mode": mode, "serial_value": nnz * d * iters / (ms_serial / 1e3), "serial_ms_per_step": ms_serial}
         del outs, src_h, dst_h, w_h

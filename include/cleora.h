@@ -361,6 +361,10 @@ CLEORA_API int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_e
  * handles, so repeated handles of one shape open none).  Diagnostic. */
 CLEORA_API int64_t cleora_ipc_opens(void);
 
+/* Process-wide number of device allocations that found no room and first returned cached segments to
+ * the driver (each such cudaFree synchronises the device).  Diagnostic. */
+CLEORA_API int64_t cleora_oom_fallbacks(void);
+
 /* Size of an ncclUniqueId (128) and a helper that fills one (rank 0 calls it and
  * broadcasts the bytes through the caller's process group). */
 CLEORA_API int cleora_nccl_id_size(void);

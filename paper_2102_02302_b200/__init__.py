@@ -24,7 +24,7 @@ __all__ = [
     "cleora_fetch_async", "cleora_trim",
     "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
     "cleora_release_cached_memory", "cleora_merge_chunks", "cleora_reconstruct", "cleora_build_batch",
-    "cleora_expand", "EXPAND_CLIQUE", "EXPAND_STAR", "cleora_probe_gather", "cleora_ipc_opens", "host_allgather_from",
+    "cleora_expand", "EXPAND_CLIQUE", "EXPAND_STAR", "cleora_probe_gather", "cleora_ipc_opens", "cleora_oom_fallbacks", "host_allgather_from",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcleora.so")
@@ -116,6 +116,7 @@ _SIGS = {
     "cleora_release_cached_memory": (ctypes.c_int, []),
     "cleora_probe_gather": (ctypes.c_int, [_i32, _i32, _i64, _i64, ctypes.POINTER(ctypes.c_double)]),
     "cleora_ipc_opens": (ctypes.c_int64, []),
+    "cleora_oom_fallbacks": (ctypes.c_int64, []),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -509,3 +510,8 @@ def cleora_probe_gather(row_bytes: int, table_bytes: int = 64 << 20, n_gathers: 
 def cleora_ipc_opens() -> int:
     """Process-wide count of CUDA IPC mappings opened (peer T buffers; cached across handles)."""
     return int(_lib.cleora_ipc_opens())
+
+
+def cleora_oom_fallbacks() -> int:
+    """Process-wide count of allocations that had to return cached segments to the driver first."""
+    return int(_lib.cleora_oom_fallbacks())

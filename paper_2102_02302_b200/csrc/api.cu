@@ -11,6 +11,7 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -104,87 +105,161 @@ Status read_small_n(const SmallRead* r, int n, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- device memory
-// Small buffers come from the device's default stream-ordered pool.  Large ones (>= 1 MiB:
-// the T replicas, CSR arrays, sort buffers) go through a process-wide cache of freed blocks,
-// keyed by device and size rounded to 2 MiB: a graph built, embedded and destroyed over and
-// over (the bench step; a service embedding many graphs of one shape) reuses the same
-// physical blocks instead of growing the pool.  Measured on B200: without it, pool growth
-// in the middle of a run stalled single steps by 40-140 ms (scripts/step_jitter.py).
-// A cached block carries an event recorded on the stream that freed it; the stream that
-// reuses it waits on that event, so stream ordering is kept across streams.
-// cleora_release_cached_memory() returns every cached block to the driver; an allocation
-// that fails for lack of memory does the same on its device and retries once.
+// Small buffers come from the device's default stream-ordered pool.  Large ones (>= 1 MiB: the T
+// replicas, CSR arrays, sort buffers) come from a process-wide cache of cudaMalloc segments, handed
+// out whole and reused by exact (2 MiB-rounded) size: a graph built, embedded and destroyed over and
+// over (the bench step; a service embedding many graphs of one shape) reuses the same physical
+// blocks.  Measured on B200 before any cache: pool growth in the middle of a run stalled single steps
+// by 40-140 ms (scripts/step_jitter.py).
+// Stream order: a freed segment carries the events recorded on the streams that freed it; whoever
+// reuses it waits on them first.  Segments go back to the driver on cleora_release_cached_memory(),
+// beyond the cap (CLEORA_CACHE_MAX_FRAC of HBM, 0.8), or when a cudaMalloc fails (then largest
+// first, and the allocation is retried; cleora_oom_fallbacks counts these).
 static std::mutex g_pool_mu;
 static bool g_pool_cfg[64];
 
 namespace {
 constexpr size_t kCacheMin = (size_t)1 << 20;
 constexpr size_t kCacheGrain = (size_t)2 << 20;
-struct Block {
-    void* p;
+struct Range {                      // a piece of a segment, free or handed out
     size_t bytes;
     int dev;
-    cudaEvent_t ready;
+    char* seg;                      // base of its segment
+    size_t seg_bytes;
+    bool free;
+    std::vector<cudaEvent_t> ready; // free ranges: reuse waits on these
 };
 std::mutex g_cache_mu;
-std::vector<Block> g_cache;                 // freed, reusable
-std::vector<Block> g_live;                  // handed out (p -> size, device)
-size_t g_cached_bytes = 0;
+std::map<char*, Range> g_ranges;    // every range of every segment, by address
+size_t g_free_bytes = 0;            // bytes in free ranges
+std::vector<cudaEvent_t> g_ev_pool;
+std::atomic<int64_t> g_oom_fallbacks{0};
 
 size_t round_block(size_t b) { return (b + kCacheGrain - 1) / kCacheGrain * kCacheGrain; }
 
-void release_cached(int dev /* -1: all */, cudaStream_t s) {
-    std::vector<Block> drop;
-    {
-        std::lock_guard<std::mutex> lk(g_cache_mu);
-        for (size_t i = 0; i < g_cache.size();) {
-            if (dev < 0 || g_cache[i].dev == dev) {
-                drop.push_back(g_cache[i]);
-                g_cached_bytes -= g_cache[i].bytes;
-                g_cache[i] = g_cache.back();
-                g_cache.pop_back();
+cudaEvent_t ev_get() {              // caller holds g_cache_mu
+    if (!g_ev_pool.empty()) {
+        cudaEvent_t e = g_ev_pool.back();
+        g_ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return e;
+}
+
+// Take the free segments that are whole (one free range) out of the cache: all of `dev` (-1: every
+// device), or only the largest one.  Caller frees them with cudaFree after waiting for their events.
+struct Dropped {
+    char* p;
+    int dev;
+    std::vector<cudaEvent_t> ready;
+};
+std::vector<Dropped> take_whole_free(int dev, bool largest_only) {
+    std::vector<Dropped> out;
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    char* best = nullptr;
+    size_t best_b = 0;
+    for (auto it = g_ranges.begin(); it != g_ranges.end();) {
+        Range& r = it->second;
+        const bool whole = r.free && it->first == r.seg && r.bytes == r.seg_bytes;
+        if (whole && (dev < 0 || r.dev == dev)) {
+            if (largest_only) {
+                if (r.bytes > best_b) { best_b = r.bytes; best = it->first; }
             } else {
-                i++;
+                out.push_back({it->first, r.dev, std::move(r.ready)});
+                g_free_bytes -= r.bytes;
+                it = g_ranges.erase(it);
+                continue;
             }
         }
+        ++it;
     }
+    if (largest_only && best) {
+        auto it = g_ranges.find(best);
+        out.push_back({best, it->second.dev, std::move(it->second.ready)});
+        g_free_bytes -= it->second.bytes;
+        g_ranges.erase(it);
+    }
+    return out;
+}
+
+void free_dropped(std::vector<Dropped>& v) {
     int cur = -1;
     cudaGetDevice(&cur);
-    for (auto& b : drop) {
-        cudaSetDevice(b.dev);
-        cudaEventSynchronize(b.ready);
-        cudaEventDestroy(b.ready);
-        cudaFree(b.p);
+    for (auto& d : v) {
+        cudaSetDevice(d.dev);
+        for (auto e : d.ready) {
+            cudaEventSynchronize(e);
+            cudaEventDestroy(e);
+        }
+        cudaFree(d.p);
     }
     if (cur >= 0) cudaSetDevice(cur);
+    v.clear();
+}
+
+void release_cached(int dev /* -1: all */, cudaStream_t s) {
+    auto v = take_whole_free(dev, false);
+    free_dropped(v);
     (void)s;
 }
 
-// Return the largest cached block of `dev` to the driver; false when there is none.
 bool release_largest(int dev) {
-    Block b{};
-    {
-        std::lock_guard<std::mutex> lk(g_cache_mu);
-        size_t best = 0;
-        int at = -1;
-        for (size_t i = 0; i < g_cache.size(); i++)
-            if (g_cache[i].dev == dev && g_cache[i].bytes > best) {
-                best = g_cache[i].bytes;
-                at = (int)i;
-            }
-        if (at < 0) return false;
-        b = g_cache[at];
-        g_cached_bytes -= b.bytes;
-        g_cache.erase(g_cache.begin() + at);
-    }
-    cudaEventSynchronize(b.ready);
-    cudaEventDestroy(b.ready);
-    cudaFree(b.p);
+    auto v = take_whole_free(dev, true);
+    if (v.empty()) return false;
+    free_dropped(v);
     return true;
+}
+
+// Two size classes that never share a segment: a long-lived small buffer (a row pointer) carved out of
+// a 40 GB segment would keep the whole segment from ever going back to the driver.
+constexpr size_t kBigClass = (size_t)1 << 30;
+inline bool big_class(size_t b) { return b >= kBigClass; }
+
+// best-fit free range of `dev` for `rb` bytes (`base`: starting at a segment base; `tight`: at most
+// 1/8 larger than rb) in segments of rb's size class; split off the tail; the stream waits for the
+// range's events.  Caller holds g_cache_mu.
+void* take_range(int dev, size_t rb, bool base, bool tight, cudaStream_t s) {
+    auto best = g_ranges.end();
+    for (auto it = g_ranges.begin(); it != g_ranges.end(); ++it) {
+        const Range& r = it->second;
+        if (!r.free || r.dev != dev || r.bytes < rb || (base && it->first != r.seg)) continue;
+        // no splitting: a cached segment is handed out whole and of exactly the size asked for (rounded
+        // to 2 MiB).  Two alternatives were measured on c5's e2e pipeline, where one step's working
+        // set nearly fills the 180 GB, and dropped: splitting segments (best fit, merging freed
+        // neighbours) let pieces of long-lived buffers pin large segments, and lending transient
+        // buffers segments up to twice their size wasted the rest; either way a 22.7 GB sort buffer
+        // later found no room and nothing to give back -- a hard out-of-memory error where exact
+        // whole segments only cost cudaFree/cudaMalloc round trips (profiles/r02_bench_c5_oom.txt)
+        (void)tight;
+        if (r.bytes != rb) continue;
+        if (big_class(r.seg_bytes) != big_class(rb)) continue;
+        if (best == g_ranges.end() || r.bytes < best->second.bytes) best = it;
+    }
+    if (best == g_ranges.end()) return nullptr;
+    char* p = best->first;
+    Range& r = best->second;
+    for (auto e : r.ready) {
+        cudaStreamWaitEvent(s, e, 0);
+        g_ev_pool.push_back(e);
+    }
+    r.ready.clear();
+    r.free = false;
+    g_free_bytes -= r.bytes;
+    return p;
 }
 }  // namespace
 
-Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, bool block) {
+Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, int flags) {
+    const bool block = flags & kAllocBase;
+    // transient buffers (sort keys, run starts, staged inputs: freed before the call returns) may be
+    // carved out of any free range; long-lived ones (CSR, T, schedules) take a range that fits tightly
+    // or a new segment, so that they never pin a large segment they only use a corner of
+    const bool tight = !(flags & kAllocTransient);
     *p = nullptr;
     int dev = 0;
     CL_CUDA_TRY(cudaGetDevice(&dev));
@@ -200,57 +275,51 @@ Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, bool blo
         }
     }
     if (bytes == 0) bytes = 16;
-    // block: a plain cudaMalloc block whatever the size (T buffers: CUDA IPC cannot export pool memory)
+    // block: a range at the base of a cudaMalloc segment whatever the size (T buffers: CUDA IPC cannot
+    // export pool memory, and exports whole allocations)
     static const bool no_cache = getenv("CLEORA_NO_CACHE") != nullptr;
     const bool big = block || (bytes >= kCacheMin && !no_cache);
+    const size_t rb = round_block(bytes);
     if (big) {
-        const size_t rb = round_block(bytes);
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        for (size_t i = 0; i < g_cache.size(); i++) {
-            if (g_cache[i].dev == dev && g_cache[i].bytes == rb) {
-                Block b = g_cache[i];
-                g_cache[i] = g_cache.back();
-                g_cache.pop_back();
-                g_cached_bytes -= rb;
-                cudaStreamWaitEvent(s, b.ready, 0);
-                *p = b.p;
-                g_live.push_back(b);
-                return Status::ok();
-            }
+        if (void* q = take_range(dev, rb, block, tight, s)) {
+            *p = q;
+            return Status::ok();
         }
     }
     for (;;) {
         cudaError_t e;
         if (big) {
-            // cached blocks are plain device allocations (not pool memory): they outlive streams
-            e = cudaMalloc(p, round_block(bytes));
+            // cached segments are plain device allocations (not pool memory): they outlive streams
+            e = cudaMalloc(p, rb);
         } else {
             e = cudaMallocAsync(p, bytes, s);
         }
         if (e == cudaSuccess) break;
         cudaGetLastError();
         *p = nullptr;
-        // out of memory: give cached blocks back to the driver, largest first, until it fits (the
-        // rest stays cached for the next graph of the same shape)
+        // out of memory: give whole free segments back to the driver, largest first, until it fits
         if (e == cudaErrorMemoryAllocation && release_largest(dev)) {
+            g_oom_fallbacks.fetch_add(1);
             static const bool tr = getenv("CLEORA_TRACE") != nullptr;
-            if (tr) fprintf(stderr, "[cleora trace] out of memory for %s (%zu bytes): released a cached block\n", what, bytes);
+            if (tr) fprintf(stderr, "[cleora trace] out of memory for %s (%zu bytes): released a cached segment\n", what, bytes);
             continue;
+        }
+        if (e == cudaErrorMemoryAllocation && big && tight) {
+            // nothing left to give back: as a last resort carve a long-lived buffer out of any free range
+            std::lock_guard<std::mutex> lk(g_cache_mu);
+            if (void* q = take_range(dev, rb, block, false, s)) {
+                *p = q;
+                return Status::ok();
+            }
         }
         char buf[256];
         snprintf(buf, sizeof buf, "cudaMalloc(%zu bytes) for %s: %s", bytes, what, cudaGetErrorString(e));
         return Status::make(4, buf);
     }
     if (big) {
-        Block b{*p, round_block(bytes), dev, nullptr};
-        if (cudaEventCreateWithFlags(&b.ready, cudaEventDisableTiming) != cudaSuccess) {
-            cudaGetLastError();
-            cudaFree(*p);
-            *p = nullptr;
-            return Status::make(4, std::string("cudaEventCreate for ") + what);
-        }
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        g_live.push_back(b);
+        g_ranges.emplace((char*)*p, Range{rb, dev, (char*)*p, rb, false, {}});
     }
     return Status::ok();
 }
@@ -270,36 +339,47 @@ static size_t cache_cap_bytes(int dev) {
 
 void dfree(void* p, cudaStream_t s) {
     if (!p) return;
-    std::vector<Block> drop;
     bool cached = false;
+    int dev = -1;
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        for (size_t i = 0; i < g_live.size(); i++) {
-            if (g_live[i].p == p) {
-                Block b = g_live[i];
-                g_live[i] = g_live.back();
-                g_live.pop_back();
-                cudaEventRecord(b.ready, s);    // the block is free once s reaches this point
-                g_cache.push_back(b);
-                g_cached_bytes += b.bytes;
-                cached = true;
-                // bound what stays cached: drop the oldest blocks beyond the cap
-                const size_t cap = cache_cap_bytes(b.dev);
-                while (g_cached_bytes > cap && g_cache.size() > 1) {
-                    drop.push_back(g_cache.front());
-                    g_cached_bytes -= g_cache.front().bytes;
-                    g_cache.erase(g_cache.begin());
-                }
-                break;
+        auto it = g_ranges.find((char*)p);
+        if (it != g_ranges.end() && !it->second.free) {
+            Range& r = it->second;
+            dev = r.dev;
+            if (cudaEvent_t e = ev_get()) {
+                cudaEventRecord(e, s);        // the range is free once s reaches this point
+                r.ready.push_back(e);
             }
+            r.free = true;
+            g_free_bytes += r.bytes;
+            // merge with free neighbours of the same segment (keeping every pending event)
+            auto nx = std::next(it);
+            if (nx != g_ranges.end() && nx->second.free && nx->second.seg == r.seg) {
+                r.bytes += nx->second.bytes;
+                for (auto e : nx->second.ready) r.ready.push_back(e);
+                g_ranges.erase(nx);
+            }
+            if (it != g_ranges.begin()) {
+                auto pv = std::prev(it);
+                if (pv->second.free && pv->second.seg == r.seg) {
+                    pv->second.bytes += r.bytes;
+                    for (auto e : r.ready) pv->second.ready.push_back(e);
+                    g_ranges.erase(it);
+                }
+            }
+            cached = true;
         }
     }
-    for (auto& b : drop) {
-        cudaEventSynchronize(b.ready);
-        cudaEventDestroy(b.ready);
-        cudaFree(b.p);
+    if (!cached) {
+        cudaFreeAsync(p, s);
+        return;
     }
-    if (!cached) cudaFreeAsync(p, s);
+    // bound what stays cached: whole free segments beyond the cap go back to the driver
+    if (g_free_bytes > cache_cap_bytes(dev)) {
+        while (g_free_bytes > cache_cap_bytes(dev) && release_largest(dev)) {
+        }
+    }
 }
 
 // ---------------------------------------------------------------- NCCL, resolved at run time
@@ -713,7 +793,7 @@ Status comm_allgather(cleora_graph* g, const void* mine, void* all, size_t bytes
     Nccl& N = nccl();
     const int W = g->world;
     void* d = nullptr;
-    CL_TRY(dalloc(&d, bytes * W + 16, g->stream, "all-gather buffer"));
+    CL_TRY(dalloc(&d, bytes * W + 16, g->stream, "all-gather buffer", kAllocTransient));
     Status st = Status::ok();
     do {
         if (cudaMemcpyAsync((char*)d + bytes * g->rank, mine, bytes, cudaMemcpyHostToDevice, g->stream) != cudaSuccess) {
@@ -851,12 +931,12 @@ Status build_body(const int32_t* src, const int32_t* dst, const float* w, int64_
     } staged{g, {&bs, &bd, &bw, &gs, &gd}};
     const bool on_dev = o && o->input_on_device;
     if (!on_dev) {
-        CL_TRY(dalloc(&bs, E * sizeof(int32_t), g->stream, "input src"));
-        CL_TRY(dalloc(&bd, E * sizeof(int32_t), g->stream, "input dst"));
+        CL_TRY(dalloc(&bs, E * sizeof(int32_t), g->stream, "input src", kAllocTransient));
+        CL_TRY(dalloc(&bd, E * sizeof(int32_t), g->stream, "input dst", kAllocTransient));
         CL_CUDA_TRY(cudaMemcpyAsync(bs, src, E * sizeof(int32_t), cudaMemcpyHostToDevice, g->stream));
         CL_CUDA_TRY(cudaMemcpyAsync(bd, dst, E * sizeof(int32_t), cudaMemcpyHostToDevice, g->stream));
         if (w) {
-            CL_TRY(dalloc(&bw, E * sizeof(float), g->stream, "input weight"));
+            CL_TRY(dalloc(&bw, E * sizeof(float), g->stream, "input weight", kAllocTransient));
             CL_CUDA_TRY(cudaMemcpyAsync(bw, w, E * sizeof(float), cudaMemcpyHostToDevice, g->stream));
         }
         dsrc = (const int32_t*)bs;
@@ -871,9 +951,9 @@ Status build_body(const int32_t* src, const int32_t* dst, const float* w, int64_
         g->n_graphs = batch->n_graphs;
         void* d_ep = nullptr;
         Status st0 = dalloc((void**)&g->d_base, base.size() * sizeof(int64_t), g->stream, "batch bases");
-        if (st0.good()) st0 = dalloc(&d_ep, base.size() * sizeof(int64_t), g->stream, "batch edge offsets");
-        if (st0.good()) st0 = dalloc(&gs, E * sizeof(int32_t), g->stream, "batch src");
-        if (st0.good()) st0 = dalloc(&gd, E * sizeof(int32_t), g->stream, "batch dst");
+        if (st0.good()) st0 = dalloc(&d_ep, base.size() * sizeof(int64_t), g->stream, "batch edge offsets", kAllocTransient);
+        if (st0.good()) st0 = dalloc(&gs, E * sizeof(int32_t), g->stream, "batch src", kAllocTransient);
+        if (st0.good()) st0 = dalloc(&gd, E * sizeof(int32_t), g->stream, "batch dst", kAllocTransient);
         if (st0.good()) {
             cudaMemcpyAsync(g->d_base, base.data(), base.size() * sizeof(int64_t), cudaMemcpyHostToDevice, g->stream);
             cudaMemcpyAsync(d_ep, batch->edge_ptr, base.size() * sizeof(int64_t), cudaMemcpyHostToDevice, g->stream);
@@ -1100,9 +1180,9 @@ int cleora_expand(const int64_t* he_ptr, const int32_t* he_nodes, const float* h
         if (he_ptr[0] != 0) return usage("cleora_expand: he_ptr[0] must be 0");
         for (int64_t i = 0; i < n_hyperedges; i++)
             if (he_ptr[i + 1] < he_ptr[i]) return usage("cleora_expand: he_ptr must be non-decreasing");
-        st = dalloc(&bp, (n_hyperedges + 1) * sizeof(int64_t), s, "expand he_ptr");
-        if (st.good()) st = dalloc(&bn, (n_members > 0 ? n_members : 1) * sizeof(int32_t), s, "expand members");
-        if (st.good() && he_weight) st = dalloc(&bw, n_hyperedges * sizeof(float), s, "expand weights");
+        st = dalloc(&bp, (n_hyperedges + 1) * sizeof(int64_t), s, "expand he_ptr", kAllocTransient);
+        if (st.good()) st = dalloc(&bn, (n_members > 0 ? n_members : 1) * sizeof(int32_t), s, "expand members", kAllocTransient);
+        if (st.good() && he_weight) st = dalloc(&bw, n_hyperedges * sizeof(float), s, "expand weights", kAllocTransient);
         if (st.good()) {
             cudaMemcpyAsync(bp, he_ptr, (n_hyperedges + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
             if (n_members > 0) cudaMemcpyAsync(bn, he_nodes, n_members * sizeof(int32_t), cudaMemcpyHostToDevice, s);
@@ -1118,9 +1198,9 @@ int cleora_expand(const int64_t* he_ptr, const int32_t* he_nodes, const float* h
                                n_out);
         if (st.good() && *n_out > capacity) st = Status::make(2, "cleora_expand: capacity smaller than the edge count");
         if (st.good() && *n_out > 0) {
-            st = dalloc(&os, *n_out * sizeof(int32_t), s, "expand out src");
-            if (st.good()) st = dalloc(&od, *n_out * sizeof(int32_t), s, "expand out dst");
-            if (st.good() && out_weight) st = dalloc(&ow, *n_out * sizeof(float), s, "expand out weight");
+            st = dalloc(&os, *n_out * sizeof(int32_t), s, "expand out src", kAllocTransient);
+            if (st.good()) st = dalloc(&od, *n_out * sizeof(int32_t), s, "expand out dst", kAllocTransient);
+            if (st.good() && out_weight) st = dalloc(&ow, *n_out * sizeof(float), s, "expand out weight", kAllocTransient);
         }
     }
     if (st.good()) {
@@ -1201,7 +1281,9 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
         free_T(g);
         const size_t tb = (size_t)g->n * dp * sizeof(float);
         Status sa = Status::ok();
-        for (int i = 0; i < 2 && sa.good(); i++) sa = dalloc((void**)&g->T[i], tb, g->stream, "embedding T", true);
+        // peers map T through CUDA IPC, which exports whole allocations: T at a segment's base
+        const int tflags = g->xmode == X_PEER ? kAllocBase : 0;
+        for (int i = 0; i < 2 && sa.good(); i++) sa = dalloc((void**)&g->T[i], tb, g->stream, "embedding T", tflags);
         if (sa.good() && g->xmode == X_LOOPBACK) {
             g->rep[g->rank] = {g->T[0], g->T[1]};
             for (int p = 0; p < g->world && sa.good(); p++) {
@@ -1468,8 +1550,8 @@ int cleora_merge_chunks(cleora_graph* const* chunks, int32_t n_chunks, float* ou
     void* d_ptr = nullptr;
     float* stage = nullptr;
     const bool direct = out_on_device && g0->d == g0->dp;
-    Status st = dalloc(&d_ptr, h_ptr.size() * sizeof(void*), s, "merge pointer table");
-    if (st.good() && !direct) st = dalloc((void**)&stage, (size_t)g0->n * g0->dp * sizeof(float), s, "merge staging");
+    Status st = dalloc(&d_ptr, h_ptr.size() * sizeof(void*), s, "merge pointer table", kAllocTransient);
+    if (st.good() && !direct) st = dalloc((void**)&stage, (size_t)g0->n * g0->dp * sizeof(float), s, "merge staging", kAllocTransient);
     cudaError_t e = cudaSuccess;
     if (st.good()) {
         e = cudaMemcpyAsync(d_ptr, h_ptr.data(), h_ptr.size() * sizeof(void*), cudaMemcpyHostToDevice, s);
@@ -1511,9 +1593,9 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
     const float* dw = weight;
     Status st = Status::ok();
     if (!inputs_on_device) {
-        st = dalloc(&bs, n_edges * sizeof(int32_t), s, "reconstruct new_idx");
-        if (st.good()) st = dalloc(&bd, n_edges * sizeof(int32_t), s, "reconstruct known_idx");
-        if (st.good() && weight) st = dalloc(&bw, n_edges * sizeof(float), s, "reconstruct weight");
+        st = dalloc(&bs, n_edges * sizeof(int32_t), s, "reconstruct new_idx", kAllocTransient);
+        if (st.good()) st = dalloc(&bd, n_edges * sizeof(int32_t), s, "reconstruct known_idx", kAllocTransient);
+        if (st.good() && weight) st = dalloc(&bw, n_edges * sizeof(float), s, "reconstruct weight", kAllocTransient);
         if (st.good()) {
             cudaMemcpyAsync(bs, new_idx, n_edges * sizeof(int32_t), cudaMemcpyHostToDevice, s);
             cudaMemcpyAsync(bd, known_idx, n_edges * sizeof(int32_t), cudaMemcpyHostToDevice, s);
@@ -1543,7 +1625,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
     if (st.good()) st = build_schedule(b.row_ptr, N2, 0, n_new, b.nnz, b.max_degree, g->heavy_thresh, g->chunk_rows, s, &sc);
     if (st.good()) st = dalloc((void**)&Tnew, (size_t)n_new * g->dp * sizeof(float), s, "reconstructed rows");
     if (st.good() && sc.n_slots_max > 0)
-        st = dalloc((void**)&parts, (size_t)sc.n_slots_max * g->dp * sizeof(float), s, "reconstruct partials");
+        st = dalloc((void**)&parts, (size_t)sc.n_slots_max * g->dp * sizeof(float), s, "reconstruct partials", kAllocTransient);
     if (st.good()) {
         SpmmArgs a;
         a.row_ptr = b.row_ptr;
@@ -1833,6 +1915,8 @@ int cleora_probe_gather(int32_t device, int32_t row_bytes, int64_t table_bytes, 
 }
 
 int64_t cleora_ipc_opens(void) { return g_ipc_opens.load(); }
+
+int64_t cleora_oom_fallbacks(void) { return g_oom_fallbacks.load(); }
 
 int cleora_nccl_id_size(void) { return NCCL_UNIQUE_ID_BYTES; }
 

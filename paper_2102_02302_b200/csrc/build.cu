@@ -4,7 +4,8 @@
 // the sum of their weights.  Algorithm 1 line 3 builds M per chunk; here Q = 1.
 // Bit-exact contract with the oracle (readings B1-B4):
 //   B1 entries = originals in input order, then mirrors (undirected, u != v) in input order;
-//      STABLE sort by (src, dst)                      -> cub radix sort (stable) on src*N+dst
+//      STABLE sort by (src, dst)                      -> cub radix sort (stable) on src*N+dst, the
+//                                                        weights as payload
 //   B2 e_ab   = fp64 sum in that stable order        -> one thread per run, sequential
 //   B3 deg(a) = fp64 sum of e_ab over ascending b     -> one warp per row, sequential fold
 //   B4 val    = fp32_rn(e_ab / deg(a))                -> IEEE double divide, one rounding
@@ -59,7 +60,7 @@ __global__ void k_validate_expand(const int32_t* __restrict__ src, const int32_t
             atomicAdd(occ + v, 1);
         }
         keys[i] = keep ? (uint64_t)(uint32_t)u * (uint64_t)N + (uint64_t)(uint32_t)v : sentinel;
-        if (pos) pos[i] = (uint32_t)i;
+        if (pos) pos[i] = __float_as_uint(w ? w[i] : 1.0f);   // sort payload: the weight itself
         unsigned long long drop = keep ? 0 : 1;
         if (!directed) {
             if (!keep || u == v) {
@@ -68,7 +69,7 @@ __global__ void k_validate_expand(const int32_t* __restrict__ src, const int32_t
             } else {
                 keys[E + i] = (uint64_t)(uint32_t)v * (uint64_t)N + (uint64_t)(uint32_t)u;
             }
-            if (pos) pos[E + i] = (uint32_t)(E + i);
+            if (pos) pos[E + i] = __float_as_uint(w ? w[i] : 1.0f);
         }
         if (drop) atomicAdd(n_drop, drop);
     }
@@ -100,10 +101,9 @@ __global__ void k_merge_runs(const uint64_t* __restrict__ keys, const uint32_t* 
         col[u] = (int32_t)(k % (uint64_t)N);
         double acc = 0.0;
         if (w) {
-            for (int64_t i = s; i < e; i++) {
-                int64_t p = pos[i];
-                acc = acc + (double)w[p < E ? p : p - E];
-            }
+            // the payload sorted with the keys is the weight (bits); the sort is stable, so a run's
+            // weights come in input order (originals, then mirrors: reading B2) and are read in sequence
+            for (int64_t i = s; i < e; i++) acc = acc + (double)__uint_as_float(pos[i]);
         } else {
             for (int64_t i = s; i < e; i++) acc = acc + 1.0;
         }
@@ -430,9 +430,11 @@ struct InShard {
     }
 };
 
-__global__ void k_shard_keys(const uint32_t* __restrict__ pos, int64_t n, const int32_t* __restrict__ src,
-                             const int32_t* __restrict__ dst, int64_t E, int32_t N, int32_t lo,
-                             uint64_t* __restrict__ keys) {
+// keys of the selected entries, and (weighted) their weights in place of their positions: the sort
+// payload is the weight itself (see k_merge_runs)
+__global__ void k_shard_keys(uint32_t* __restrict__ pos, int64_t n, const int32_t* __restrict__ src,
+                             const int32_t* __restrict__ dst, const float* __restrict__ w, int64_t E, int32_t N,
+                             int32_t lo, uint64_t* __restrict__ keys) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
         const int64_t i = pos[k];
@@ -440,6 +442,7 @@ __global__ void k_shard_keys(const uint32_t* __restrict__ pos, int64_t n, const 
         const int64_t e = mirror ? i - E : i;
         const int32_t u = mirror ? dst[e] : src[e], v = mirror ? src[e] : dst[e];
         keys[k] = (uint64_t)(uint32_t)(u - lo) * (uint64_t)N + (uint64_t)(uint32_t)v;
+        if (w) pos[k] = __float_as_uint(w[e]);
     }
 }
 
@@ -450,9 +453,10 @@ struct DevBuf {
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     ~DevBuf() { if (p) dfree(p, s); }
-    Status alloc(size_t n, cudaStream_t st, const char* what) {
+    // transient unless the buffer outlives the call (released into a CSR or a schedule)
+    Status alloc(size_t n, cudaStream_t st, const char* what, bool long_lived = false) {
         s = st;
-        return dalloc((void**)&p, n * sizeof(T) + 16, st, what);
+        return dalloc((void**)&p, n * sizeof(T) + 16, st, what, long_lived ? 0 : kAllocTransient);
     }
     T* release() { T* q = p; p = nullptr; return q; }
 };
@@ -476,17 +480,18 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     const int end_bit = 64 - __builtin_clzll(sentinel | 1ull);
 
     DevBuf<uint64_t> keys, keys2;
-    DevBuf<uint32_t> pos, pos2;
+    DevBuf<uint32_t> pos, pos2;                          // sort payload: the entries' weights (fp32 bits)
     DevBuf<unsigned long long> scal;                     // [0] err_first [1] n_self [2] zero_rows [3] max_deg [4] nnz
     DevBuf<int> err_kind;
-    // unit weights: e_ab is the run length, the same in any order, so the sort needs no payload
-    // (positions only order the fp64 sums of weighted duplicates, reading B2) -- a third less traffic
+    // unit weights: e_ab is the run length, the same in any order, so the sort needs no payload -- a
+    // third less traffic.  Weighted: the payload is the weight, so the merge reads each run's weights in
+    // sequence (round 1 sorted positions and gathered w[pos] at random: c4 1.45 ms per build)
     const bool keys_only = d_w == nullptr;
     CL_TRY(keys.alloc(n_ent, s, "sort keys"));
     CL_TRY(keys2.alloc(n_ent, s, "sort keys (alt)"));
     if (!keys_only || shard) CL_TRY(pos.alloc(n_ent, s, "sort payload"));
     if (!keys_only) CL_TRY(pos2.alloc(n_ent, s, "sort payload (alt)"));
-    CL_TRY(scal.alloc(8, s, "scalars"));
+    CL_TRY(scal.alloc(8, s, "scalars", true));
     CL_TRY(err_kind.alloc(1, s, "scalars"));
     CL_CUDA_TRY(cudaMemsetAsync(scal.p, 0, 8 * sizeof(unsigned long long), s));
     CL_CUDA_TRY(cudaMemsetAsync(scal.p, 0xFF, sizeof(unsigned long long), s));   // err_first = max
@@ -503,7 +508,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
             CL_TRY(tmp.alloc(tmp_bytes, s, "shard select temp"));
             CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, pos.p, scal.p + 5, n_all, pred, s));
         }
-        k_shard_keys<<<grid_for(n_ent, 4), kThreads, 0, s>>>(pos.p, n_ent, d_src, d_dst, E, N, lo, keys.p);
+        k_shard_keys<<<grid_for(n_ent, 4), kThreads, 0, s>>>(pos.p, n_ent, d_src, d_dst, d_w, E, N, lo, keys.p);
         CL_CUDA_TRY(cudaGetLastError());
         count_launches(3);
         trace("csr: shard select+keys", s, false);
@@ -569,7 +574,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     DevBuf<int64_t> row_ptr;
     DevBuf<float> val;
     CL_TRY(rows.alloc(n_ent, s, "entry rows"));
-    CL_TRY(col.alloc(n_ent, s, "CSR col"));
+    CL_TRY(col.alloc(n_ent, s, "CSR col", true));
     CL_TRY(e_ab.alloc(n_ent, s, "e_ab"));
     k_merge_runs<<<grid_for(n_ent, 4), kThreads, 0, s>>>(keys.p, pos.p, run_start.p, scal.p + 4, scal.p + 1, n_ent, d_w,
                                                          E, N, lo, rows.p, col.p, e_ab.p);
@@ -581,14 +586,14 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     dfree(pos.release(), s);
     dfree(pos2.release(), s);
 
-    CL_TRY(row_ptr.alloc((size_t)N + 1, s, "CSR row_ptr"));
+    CL_TRY(row_ptr.alloc((size_t)N + 1, s, "CSR row_ptr", true));
     CL_CUDA_TRY(cudaMemsetAsync(row_ptr.p, 0, sizeof(int64_t), s));
     k_row_ptr<<<grid_for(n_ent, 4), kThreads, 0, s>>>(rows.p, scal.p + 4, N, row_ptr.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
 
     trace("csr: row_ptr", s, true);
-    CL_TRY(deg.alloc(N, s, "degree"));
+    CL_TRY(deg.alloc(N, s, "degree", true));
     {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
@@ -599,7 +604,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     trace("csr: degree", s, true);
-    CL_TRY(val.alloc(n_ent, s, "CSR val"));
+    CL_TRY(val.alloc(n_ent, s, "CSR val", true));
     k_values<<<grid_for(n_ent, 4), kThreads, 0, s>>>(rows.p, e_ab.p, deg.p, scal.p + 4, val.p);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
@@ -638,8 +643,8 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
     {
         DevBuf<unsigned> work;
         DevBuf<int64_t> counts;
-        CL_TRY(work.alloc(4, s, "work tickets"));
-        CL_TRY(counts.alloc(4, s, "schedule counts"));
+        CL_TRY(work.alloc(4, s, "work tickets", true));
+        CL_TRY(counts.alloc(4, s, "schedule counts", true));
         CL_CUDA_TRY(cudaMemsetAsync(work.p, 0, 4 * sizeof(unsigned), s));
         CL_CUDA_TRY(cudaMemsetAsync(counts.p, 0, 4 * sizeof(int64_t), s));
         out->work = work.release();
@@ -655,7 +660,7 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         int64_t win = e ? atoll(e) : 1024;
         if (win < 1) win = 1;
         DevBuf<int64_t> starts;
-        CL_TRY(starts.alloc(nr + 1, s, "light chunk starts"));
+        CL_TRY(starts.alloc(nr + 1, s, "light chunk starts", true));
         thrust::counting_iterator<int64_t> it(r0);
         // small graphs: fewer rows per chunk, so that every warp of the persistent grid gets work
         // (c1, 10k rows: 31-row chunks left most of the 2,368 warps idle and one warp walked 31
@@ -727,8 +732,8 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
     out->n_slots_max = 2 * (nnz / per_item) + 1;
     DevBuf<HeavyItem> items;
     DevBuf<unsigned> counters;
-    CL_TRY(items.alloc(out->n_items_max, s, "heavy items"));
-    CL_TRY(counters.alloc(out->n_slots_max, s, "heavy counters"));
+    CL_TRY(items.alloc(out->n_items_max, s, "heavy items", true));
+    CL_TRY(counters.alloc(out->n_slots_max, s, "heavy counters", true));
     CL_CUDA_TRY(cudaMemsetAsync(counters.p, 0, out->n_slots_max * sizeof(unsigned), s));
     k_fill_items<<<grid_for(nh_max), kThreads, 0, s>>>(d_row_ptr, hrows.p, out->counts + 2, nh_max, first.p, sfirst.p,
                                                        per_item, items.p, out->counts);
@@ -912,7 +917,7 @@ Status shard_plan(const int32_t* d_src, const int32_t* d_dst, const float* d_w, 
     DevBuf<int32_t> indeg;
     DevBuf<int> kind;
     CL_TRY(cnt.alloc((size_t)N + 1, s, "row entry counts"));
-    CL_TRY(indeg.alloc(N, s, "in-degree"));
+    CL_TRY(indeg.alloc(N, s, "in-degree", true));
     CL_TRY(scal.alloc(1, s, "scalars"));
     CL_TRY(kind.alloc(1, s, "scalars"));
     CL_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, ((size_t)N + 1) * sizeof(unsigned long long), s));

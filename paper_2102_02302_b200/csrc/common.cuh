@@ -54,7 +54,10 @@ void count_launches(int64_t n);
 // ---------------------------------------------------------------- device buffers
 // Stream-ordered allocation from the device's default pool (release threshold raised so
 // repeated build/destroy cycles do not return memory to the driver).
-Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, bool block = false);
+// flags: kAllocBase -- at the base of a cudaMalloc segment (CUDA IPC exports whole allocations);
+// kAllocTransient -- freed before the API call returns (a hint: the cache serves both alike, api.cu)
+enum { kAllocBase = 1, kAllocTransient = 2 };
+Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, int flags = 0);
 void dfree(void* p, cudaStream_t s);
 
 // SplitMix64 output function (the mixer of the T_0 hash, reading R1, and of the chunk

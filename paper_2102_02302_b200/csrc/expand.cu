@@ -135,8 +135,8 @@ Status expand_hypergraph(const int64_t* d_ptr, const int32_t* d_nodes, const flo
     int64_t *cnt = nullptr, *off = nullptr, *tot = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
-    Status st = dalloc((void**)&cnt, (n_he + 1) * sizeof(int64_t), s, "clique counts");
-    if (st.good()) st = dalloc((void**)&off, (n_he + 1) * sizeof(int64_t), s, "clique offsets");
+    Status st = dalloc((void**)&cnt, (n_he + 1) * sizeof(int64_t), s, "clique counts", kAllocTransient);
+    if (st.good()) st = dalloc((void**)&off, (n_he + 1) * sizeof(int64_t), s, "clique offsets", kAllocTransient);
     if (st.good()) st = dalloc((void**)&tot, 2 * sizeof(int64_t), s, "clique total");
     int64_t total = 0;
     if (st.good()) {
@@ -144,7 +144,7 @@ Status expand_hypergraph(const int64_t* d_ptr, const int32_t* d_nodes, const flo
         count_launches(1);
         cudaMemsetAsync(cnt + n_he, 0, sizeof(int64_t), s);
         cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, off, n_he + 1, s);
-        st = dalloc(&tmp, tmp_bytes, s, "clique scan temp");
+        st = dalloc(&tmp, tmp_bytes, s, "clique scan temp", kAllocTransient);
     }
     if (st.good()) {
         cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, n_he + 1, s);

@@ -97,7 +97,7 @@ Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t see
     if (blocks < 1) blocks = 1;
     int32_t* lid = nullptr;
     if (d_base) {
-        CL_TRY(dalloc((void**)&lid, (size_t)N * sizeof(int32_t), s, "batch local ids"));
+        CL_TRY(dalloc((void**)&lid, (size_t)N * sizeof(int32_t), s, "batch local ids", kAllocTransient));
         int64_t gb = ((int64_t)n_graphs * 32 + 255) / 256;
         if (gb > (int64_t)sms * 8) gb = (int64_t)sms * 8;
         k_local_ids<<<(unsigned)(gb < 1 ? 1 : gb), 256, 0, s>>>(d_base, n_graphs, lid);

@@ -78,8 +78,8 @@ Status probe_gather(int row_bytes, int64_t table_bytes, int64_t n_gathers, cudaS
     int32_t* idx = nullptr;
     unsigned* sink = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    Status st = dalloc((void**)&table, (size_t)rows * row_bytes, s, "probe table");
-    if (st.good()) st = dalloc((void**)&idx, (size_t)n_gathers * 4, s, "probe indices");
+    Status st = dalloc((void**)&table, (size_t)rows * row_bytes, s, "probe table", kAllocTransient);
+    if (st.good()) st = dalloc((void**)&idx, (size_t)n_gathers * 4, s, "probe indices", kAllocTransient);
     if (st.good()) st = dalloc((void**)&sink, 16, s, "probe sink");
     double best = 0.0;
     if (st.good()) {
