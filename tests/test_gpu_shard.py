@@ -140,3 +140,35 @@ def test_full_size_sharded_bitwise(cl, name, world):
     finally:
         G.close()
         cl.cleora_release_cached_memory()
+
+
+@pytest.mark.parametrize("world", [3, 5, 8])
+def test_degenerate_shards(cl, world):
+    """More ranks than rows with entries: empty shards (no rows, or rows without entries), a shard made
+    of one hub row, self-loops only -- every replica still bitwise the 1-GPU result, every shard's CSR
+    bit-exact against the oracle's rows."""
+    cases = [
+        gen.EdgeList("three", 3, np.array([0, 1], np.int32), np.array([1, 2], np.int32), None, False),
+        gen.EdgeList("loops", 6, np.arange(6, dtype=np.int32), np.arange(6, dtype=np.int32), None, True),
+        gen.EdgeList("star", 2000, np.zeros(1999, np.int32), np.arange(1, 2000, dtype=np.int32),
+                     np.linspace(0.5, 2.0, 1999).astype(np.float32), True),     # one row holds every entry
+        gen.EdgeList("sparse", 50000, np.array([7, 49999], np.int32), np.array([49999, 7], np.int32), None, True),
+    ]
+    for g in cases:
+        M = oracle.build_from(g)
+        ref = _embed(cl, g, 33, [3])[0]
+        for T in _embed(cl, g, 33, [2, 1], loopback=True, world=world, rank=world - 1):
+            assert T.tobytes() == ref.tobytes(), g.name
+        cuts = _shard.cuts(g, world)
+        for p in range(world):
+            G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0, loopback=True, world=world, rank=p)
+            try:
+                csr = cl.cleora_fetch_csr(G)
+                info = cl.cleora_info(G)
+            finally:
+                G.close()
+            r0, r1 = int(cuts[p]), int(cuts[p + 1])
+            a, b = int(M.row_ptr[r0]), int(M.row_ptr[r1])
+            assert (info["shard_begin"], info["shard_end"], info["shard_nnz"]) == (r0, r1, b - a), (g.name, p)
+            assert np.array_equal(csr["col"], M.col[a:b]) and csr["val"].tobytes() == M.val[a:b].tobytes()
+            assert np.array_equal(csr["row_ptr"][r0:r1 + 1] + a, M.row_ptr[r0:r1 + 1])
