@@ -458,7 +458,8 @@ struct cleora_graph {
     // loopback -> csr[p] = emulated rank p's shard
     std::vector<Csr> csr;
     int32_t* indeg = nullptr;       // row-sharded builds: the whole graph's in-degree (shard_plan)
-    uint8_t* ref = nullptr;         // exchange: ref[v] = some row gathers v (deferred peer stores)
+    // deferred exchange: per emulated rank (loopback) or for this rank, mask[r] bit q = peer q gathers r
+    std::vector<uint8_t*> pmask;
     bool sharded = false;
     // environment switches, read by cleora_init
     int env_cold_first = -1, env_csr_prefetch = 1;
@@ -892,6 +893,49 @@ Status open_peers(cleora_graph* g) {
         g->xmode = X_NCCL;
     }
     return Status::ok();
+}
+
+// The per-peer masks of the deferred exchange (see cleora_init).  Loopback: every emulated rank's
+// shard is local, so all the need arrays are; otherwise this rank's is all-gathered with the others'.
+Status build_peer_masks(cleora_graph* g) {
+    const int W = g->world;
+    const size_t N = (size_t)g->n;
+    uint8_t* all = nullptr;
+    CL_TRY(dalloc((void**)&all, N * W, g->stream, "need flags", kAllocTransient));
+    Status st = Status::ok();
+    if (g->xmode == X_LOOPBACK) {
+        for (int p = 0; p < W && st.good(); p++) st = need_flags(g->of(p).col, g->of(p).nnz, g->n, g->stream, all + N * p);
+    } else {
+        st = need_flags(g->own().col, g->own().nnz, g->n, g->stream, all + N * g->rank);
+        if (st.good() && g->host_ag) {
+            std::vector<uint8_t> h(N * W);
+            cudaError_t e = cudaMemcpyAsync(h.data() + N * g->rank, all + N * g->rank, N, cudaMemcpyDeviceToHost, g->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+            if (e != cudaSuccess) st = Status::make(4, std::string("need flags: ") + cudaGetErrorString(e));
+            if (st.good()) {
+                std::vector<uint8_t> mine(h.begin() + N * g->rank, h.begin() + N * (g->rank + 1));
+                st = comm_allgather(g, mine.data(), h.data(), N);
+            }
+            if (st.good() && cudaMemcpyAsync(all, h.data(), N * W, cudaMemcpyHostToDevice, g->stream) != cudaSuccess)
+                st = Status::make(4, "need flags upload");
+            if (st.good() && cudaStreamSynchronize(g->stream) != cudaSuccess) st = Status::make(4, "need flags upload");
+        } else if (st.good()) {
+            Nccl& Nc = nccl();
+            ncclResult_t r = Nc.AllGather(all + N * g->rank, all, N, ncclUint8, g->comm, g->stream);
+            if (r != ncclSuccess) st = Status::make(4, std::string("ncclAllGather: ") + Nc.GetErrorString(r));
+        }
+    }
+    const int nm = g->xmode == X_LOOPBACK ? W : 1;
+    for (int i = 0; i < nm && st.good(); i++) {
+        uint8_t* m = nullptr;
+        st = dalloc((void**)&m, N, g->stream, "peer masks");
+        if (st.good()) {
+            g->pmask.push_back(m);
+            st = peer_masks(all, g->n, W, g->xmode == X_LOOPBACK ? i : g->rank, g->stream, m);
+        }
+    }
+    dfree(all, g->stream);
+    return st;
 }
 
 Status exchange(cleora_graph* g, float* buf) {
@@ -1362,13 +1406,15 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
         }
         g->tag_dp = dp;
     }
-    if (g->sharded && (g->xmode == X_PEER || g->xmode == X_LOOPBACK) && !g->ref && g->env_defer) {
-        // rows some row gathers: only they must reach the peers before the next step (H6)
-        Status s = dalloc((void**)&g->ref, (size_t)g->n, g->stream, "referenced rows");
-        if (s.good()) s = ref_flags(g->indeg, g->n, g->stream, g->ref);
+    if (g->sharded && (g->xmode == X_PEER || g->xmode == X_LOOPBACK) && g->pmask.empty() && g->env_defer) {
+        // deferred exchange (reading R20): which peers gather which rows.  Every rank flags the columns
+        // its shard gathers; the flags are all-gathered; rank p's mask of row r has bit q set when its
+        // q-th peer's shard gathers r.  (Collective in X_PEER: every rank takes this branch together.)
+        Status s = build_peer_masks(g);
+        if (s.good() && g->xmode == X_PEER) s = comm_agree(g, s);
         if (!s.good()) {
-            dfree(g->ref, g->stream);
-            g->ref = nullptr;
+            for (auto m : g->pmask) dfree(m, g->stream);
+            g->pmask.clear();
             return fail(s);
         }
     }
@@ -1436,7 +1482,8 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
             a.csr_prefetch = g->env_csr_prefetch;
             // deferred exchange: before the last step of this call only gathered rows go to the peers;
             // the last step sends every row, so a fetch on any rank sees the whole T
-            a.peer_ref = (a.n_peers > 0 && g->ref && i + 1 < k) ? g->ref : nullptr;
+            a.peer_mask = (a.n_peers > 0 && !g->pmask.empty() && i + 1 < k) ? g->pmask[g->pmask.size() > 1 ? p : 0]
+                                                                              : nullptr;
             Status s = launch_spmm_norm(a, g->stream);
             if (!s.good()) return fail(s);
         }
@@ -1649,7 +1696,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
         for (int q = 0; q < kMaxPeers; q++) a.peer_out[q] = nullptr;
         a.skip_zero_rows = 0;
         a.csr_prefetch = 0;
-        a.peer_ref = nullptr;
+        a.peer_mask = nullptr;
         a.gather_mode = g->gmode;
         st = launch_spmm_norm(a, s);
     }
@@ -1851,9 +1898,9 @@ int cleora_trim(cleora_graph* g) {
         c.deg = nullptr;
     }
     dfree(g->indeg, g->stream);
-    dfree(g->ref, g->stream);
     g->indeg = nullptr;
-    g->ref = nullptr;
+    for (auto m : g->pmask) dfree(m, g->stream);
+    g->pmask.clear();
     g->bytes = 0;
     g->trimmed = true;
     return CLEORA_OK;
@@ -1876,7 +1923,8 @@ void cleora_destroy(cleora_graph* g) {
         free_T(g);
         free_csr(g);
         dfree(g->indeg, g->stream);
-        dfree(g->ref, g->stream);
+        for (auto m : g->pmask) dfree(m, g->stream);
+        g->pmask.clear();
         free_schedules(g);
         dfree(g->d_flag, g->stream);
         dfree(g->occ, g->stream);

@@ -968,14 +968,37 @@ Status shard_plan(const int32_t* d_src, const int32_t* d_dst, const float* d_w, 
 }
 
 namespace {
-__global__ void k_ref_flags(const int32_t* __restrict__ indeg, int32_t N, uint8_t* __restrict__ ref) {
+__global__ void k_need_flags(const int32_t* __restrict__ col, int64_t nnz, uint8_t* __restrict__ need) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < N; v += stride) ref[v] = indeg[v] > 0 ? 1 : 0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) need[col[k] & kColMask] = 1;
+}
+// mask[r] bit q = peer q (the ranks other than `rank`, in rank order) gathers row r
+__global__ void k_peer_masks(const uint8_t* __restrict__ need, int32_t N, int world, int rank, uint8_t* __restrict__ mask) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride) {
+        unsigned m = 0;
+        for (int q = 0, p = 0; p < world; p++) {
+            if (p == rank) continue;
+            m |= (unsigned)(need[(int64_t)p * N + r] != 0) << q;
+            q++;
+        }
+        mask[r] = (uint8_t)m;
+    }
 }
 }  // namespace
 
-Status ref_flags(const int32_t* d_indeg, int32_t N, cudaStream_t s, uint8_t* d_ref) {
-    k_ref_flags<<<grid_for(N, 4), kThreads, 0, s>>>(d_indeg, N, d_ref);
+Status need_flags(const int32_t* d_col, int64_t nnz, int32_t N, cudaStream_t s, uint8_t* d_need) {
+    CL_CUDA_TRY(cudaMemsetAsync(d_need, 0, (size_t)N, s));
+    if (nnz > 0) {
+        k_need_flags<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, d_need);
+        CL_CUDA_TRY(cudaGetLastError());
+        count_launches(1);
+    }
+    return Status::ok();
+}
+
+Status peer_masks(const uint8_t* d_need_all, int32_t N, int world, int rank, cudaStream_t s, uint8_t* d_mask) {
+    k_peer_masks<<<grid_for(N, 4), kThreads, 0, s>>>(d_need_all, N, world, rank, d_mask);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     return Status::ok();

@@ -106,9 +106,10 @@ struct SpmmArgs {
     // emulation, the other local replicas -- so the all-gather overlaps the SpMM row by row.
     int32_t n_peers;
     float* peer_out[kMaxPeers];
-    // non-NULL: a non-empty row r goes to the peers only when peer_ref[r] (some row gathers it); the
-    // rest of the exchange is deferred to the last step of an iterate call, which sends every row
-    const uint8_t* peer_ref;
+    // non-NULL: a non-empty row r goes to peer q only when bit q of peer_mask[r] is set (a row of that
+    // peer's shard gathers r); the rest of the exchange is deferred to the last step of an iterate
+    // call, which sends every row to every peer
+    const uint8_t* peer_mask;
     // Rows without entries are already 0 in T_out (written by an earlier iteration): skip them.
     int32_t skip_zero_rows;
     int32_t csr_prefetch;   // register kernel: L1-prefetch each light chunk's CSR words
@@ -120,8 +121,11 @@ struct SpmmArgs {
 __device__ __forceinline__ void put_out4(const SpmmArgs& a, int64_t row, int f, const float4& v, bool empty = false) {
     const int64_t off = row * (int64_t)a.dp;
     __stcs(reinterpret_cast<float4*>(a.T_out + off) + f, v);
-    if (a.n_peers > 0 && (empty || !a.peer_ref || a.peer_ref[row]))
-        for (int p = 0; p < a.n_peers; p++) __stcs(reinterpret_cast<float4*>(a.peer_out[p] + off) + f, v);
+    if (a.n_peers > 0) {
+        const unsigned m = (empty || !a.peer_mask) ? 0xffu : a.peer_mask[row];
+        for (int p = 0; p < a.n_peers; p++)
+            if ((m >> p) & 1u) __stcs(reinterpret_cast<float4*>(a.peer_out[p] + off) + f, v);
+    }
 }
 
 // A CSR of M (or of one row shard of it) on the device
@@ -192,8 +196,11 @@ Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s
 Status shard_plan(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N, int directed,
                   const BuildExtra* extra, int world, cudaStream_t s, int64_t* h_cuts, int64_t* h_ent,
                   int32_t** d_indeg);
-// ref[v] = in-degree(v) > 0 (rows some row gathers)
-Status ref_flags(const int32_t* d_indeg, int32_t N, cudaStream_t s, uint8_t* d_ref);
+// need[v] = 1 if a row of this CSR (shard) gathers v, else 0 (N bytes)
+Status need_flags(const int32_t* d_col, int64_t nnz, int32_t N, cudaStream_t s, uint8_t* d_need);
+// mask[r] bit q = peer q needs row r, from the ranks' need arrays (need_all[p * N + r]); the peers of
+// `rank` are the other ranks in rank order (the order of SpmmArgs::peer_out)
+Status peer_masks(const uint8_t* d_need_all, int32_t N, int world, int rank, cudaStream_t s, uint8_t* d_mask);
 
 // Hot-row tagging for L2 residency hints, in place: col[k] = (col[k] & 0x7fffffff) |
 // (indeg(col[k]) >= 2^b) << 31, b the smallest power of two such that the hot rows' bytes fit
