@@ -465,6 +465,7 @@ struct cleora_graph {
     int env_cold_first = -1, env_csr_prefetch = 1;
     bool env_write_zero = false, env_no_hot = false, env_defer = true;
     int gmode = 0;                  // gather engine for the current dp (gather_mode)
+    bool halves = false;            // dp = 1024 steps run as two half-row passes (cleora_init decides)
     int heavy_thresh = 64;
     Schedule sched;
     int32_t d = 0, dp = 0;
@@ -1364,15 +1365,29 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     // c2 12.68 vs 12.80 ms per step with 64 / 256; c5 427 -> 375 ms, c4@256 8.10 -> 7.27 ms with 256);
     // every sequential fp32 run stays <= 256 terms (256-entry blocks keep the error ~3e-7)
     g->gmode = gather_mode(dp);
+    // Half-row passes (spmm_tma.cu; bitwise the whole-row result for the same schedule): with 2 KB
+    // instead of 4 KB gathers twice as many rows fit the L2, which pays where the gather stream dwarfs
+    // T -- c4: nnz = 13.9 N, 28.2 -> 25.7 ms per step (min; profiles/r02_halves_ab.txt) -- and costs
+    // where it does not (c2: nnz = 5 N, 2.65 -> 3.14 ms; c3: 2.8 N).  The passes gather 2 KB pieces
+    // with cp.async (TMA bulk copies of 2 KB are issue-bound: 36 ms), heavy rows above 256 entries,
+    // light chunks of 12 rows -- the d = 512 settings.  CLEORA_HALVES=0/1 forces them off/on.
+    {
+        const char* e = getenv("CLEORA_HALVES");
+        const bool able = dp == 1024 && g->gmode != kGatherLdg;
+        g->halves = able && (e ? atoi(e) != 0 : g->nnz >= 8 * (int64_t)g->n);
+        if (g->halves && !getenv("CLEORA_GATHER") && !getenv("CLEORA_FORCE_TMA")) g->gmode = kGatherAsync;
+    }
     g->heavy_thresh = heavy_thresh_default(g->gmode == kGatherBulk ? 64 : 256);
     // light-chunk row cap per gather engine and row size (measured, scripts/r01/chunk_sweep*.sh, min
     // launch ms): TMA bulk (d = 1024) 6 rows, c3 2.04 -> 1.42 vs 31; cp.async at d = 512 12 rows, c3
     // 0.86 -> 0.75; cp.async at d = 256 31 rows (c3 0.518 vs 0.581 at 8); LDG at d <= 128 16 rows,
-    // f4 1.39 -> 1.25, c3@128 0.508 -> 0.490, c4@128 4.296 -> 4.306
+    // f4 1.39 -> 1.25, c3@128 0.508 -> 0.490, c4@128 4.296 -> 4.306; half-row passes: 12 (their
+    // 2 KB pieces behave like d = 512 rows)
     {
         const int mode = g->gmode;
-        g->chunk_rows = mode == kGatherBulk ? 6 : mode == kGatherAsync ? (dp > 256 ? 12 : kChunkRows)
-                                                                        : (dp <= 128 ? 16 : kChunkRows);
+        g->chunk_rows = mode == kGatherBulk ? (g->halves ? 12 : 6)
+                                            : mode == kGatherAsync ? (dp > 256 ? 12 : kChunkRows)
+                                                                   : (dp <= 128 ? 16 : kChunkRows);
     }
     if (g->sched_thresh != g->heavy_thresh || g->sched_rows != g->chunk_rows) {
         Status s = make_schedules(g);
@@ -1387,7 +1402,7 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
         if (!s.good()) return fail(s);
         g->partials_floats = (size_t)g->max_items * dp;
     }
-    if (g->tag_dp != dp && !g->env_no_hot && g->nnz > 0) {
+    if (g->tag_dp != dp * (g->halves ? -1 : 1) && !g->env_no_hot && g->nnz > 0) {
         // L2 residency hints: tag (bit 31 of col, in place) the columns whose rows are re-read
         // most (highest in-degree) so that their gathers use an evict_last policy, within a
         // budget of the 126 MB L2.  Row-sharded: every shard's columns, from the whole graph's
@@ -1398,13 +1413,14 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
         // T within the budget: everything fits in L2 anyway, nothing to pin (and no host round trip)
         if ((int64_t)g->n * dp * 4 <= budget) g->n_hot = 0;
         for (size_t p = 0; p < g->csr.size() && s.good() && (int64_t)g->n * dp * 4 > budget; p++)
-            s = hot_tag(g->csr[p].col, g->csr[p].nnz, g->n, (int64_t)dp * 4, budget, g->stream, &g->n_hot, &g->n_ref,
+            s = hot_tag(g->csr[p].col, g->csr[p].nnz, g->n, (int64_t)dp * 4 / (g->halves ? 2 : 1), budget, g->stream,
+                        &g->n_hot, &g->n_ref,
                         g->directed || g->sharded ? nullptr : g->csr[p].row_ptr, g->indeg);
         if (!s.good()) {
             free_T(g);
             return fail(s);
         }
-        g->tag_dp = dp;
+        g->tag_dp = dp * (g->halves ? -1 : 1);      // the tags depend on the gathered row size
     }
     if (g->sharded && (g->xmode == X_PEER || g->xmode == X_LOOPBACK) && g->pmask.empty() && g->env_defer) {
         // deferred exchange (reading R20): which peers gather which rows.  Every rank flags the columns
@@ -1484,7 +1500,14 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
             // the last step sends every row, so a fetch on any rank sees the whole T
             a.peer_mask = (a.n_peers > 0 && !g->pmask.empty() && i + 1 < k) ? g->pmask[g->pmask.size() > 1 ? p : 0]
                                                                               : nullptr;
-            Status s = launch_spmm_norm(a, g->stream);
+            a.pass = 0;
+            Status s = Status::ok();
+            if (g->halves) {
+                a.pass = 1;
+                s = launch_spmm_norm(a, g->stream);
+                a.pass = 2;
+            }
+            if (s.good()) s = launch_spmm_norm(a, g->stream);
             if (!s.good()) return fail(s);
         }
         if (g->timing) {
@@ -1698,6 +1721,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
         a.csr_prefetch = 0;
         a.peer_mask = nullptr;
         a.gather_mode = g->gmode;
+        a.pass = 0;
         st = launch_spmm_norm(a, s);
     }
     if (st.good()) {

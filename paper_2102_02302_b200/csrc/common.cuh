@@ -114,6 +114,10 @@ struct SpmmArgs {
     int32_t skip_zero_rows;
     int32_t csr_prefetch;   // register kernel: L1-prefetch each light chunk's CSR words
     int32_t gather_mode;    // kGather* for this dp (gather_mode(dp), read once by cleora_init)
+    // Half-row passes (dp = 1024 only; spmm_tma.cu): 0 = whole rows; 1 = columns [0, 512), written
+    // unnormalised into T_out and nowhere else; 2 = columns [512, 1024), then the whole row is finished
+    // from T_out's first half -- bitwise the whole-row result (see spmm_tma.cu)
+    int32_t pass;
 };
 
 // Store float4 f of row `row` of the iteration's output into T_out and every peer replica.  `empty`:

@@ -484,7 +484,7 @@ Status launch_v(const SpmmArgs& a, cudaStream_t s) {
 }  // namespace
 
 Status launch_spmm_norm(const SpmmArgs& a, cudaStream_t s) {
-    if (a.gather_mode != kGatherLdg) return launch_spmm_tma(a, s);
+    if (a.gather_mode != kGatherLdg || a.pass > 0) return launch_spmm_tma(a, s);
     if (a.dp <= 128) return launch_v<1>(a, s);
     if (a.dp <= 256) return launch_v<2>(a, s);
     if (a.dp <= 512) return launch_v<4>(a, s);

@@ -125,9 +125,11 @@ struct Ring {
 // stream -- so that positional wait always names the slot being consumed.
 template <int V, bool FULL, int SA>
 __device__ __forceinline__ void ring_issue(const SpmmArgs& a, Ring& r, int slot, int32_t c, int lane) {
+    // a.dp is the row stride; half-row passes gather 128 * V floats starting at column 512 * (pass == 2)
+    const int64_t col0 = a.pass == 2 ? 128 * V : 0;
     if (SA > 0) {
-        const int dp = FULL ? 128 * V : a.dp;
-        const float4* src = reinterpret_cast<const float4*>(a.T_in + (int64_t)(c & 0x7fffffff) * dp) + lane;
+        const int dp = FULL ? 128 * V : a.dp;     // gathered width
+        const float4* src = reinterpret_cast<const float4*>(a.T_in + (int64_t)(c & 0x7fffffff) * a.dp + col0) + lane;
         float4* dst = r.buf + (size_t)slot * r.slot_f4 + lane;
         const uint64_t pol = c < 0 ? r.pol_hot : r.pol_cold;
 #pragma unroll
@@ -141,7 +143,7 @@ __device__ __forceinline__ void ring_issue(const SpmmArgs& a, Ring& r, int slot,
     }
     if (lane == 0) {
         mbar_expect_tx(r.bar + slot, r.bytes);
-        bulk_g2s_hint(r.buf + (size_t)slot * r.slot_f4, a.T_in + (int64_t)(c & 0x7fffffff) * a.dp, r.bytes,
+        bulk_g2s_hint(r.buf + (size_t)slot * r.slot_f4, a.T_in + (int64_t)(c & 0x7fffffff) * a.dp + col0, r.bytes,
                       r.bar + slot, c < 0 ? r.pol_hot : r.pol_cold);
     }
 }
@@ -163,11 +165,46 @@ __device__ __forceinline__ void ring_wait(Ring& r, int sl) {
 
 // `empty`: the row has no entries (its output is the zero vector, reading RZ); with
 // a.skip_zero_rows the zeros are already in T_out and nothing is written.
+//
+// Half-row passes (a.pass, V = 4 of the whole row's 8 float4 per lane): pass 1 stores the first half
+// of y unnormalised into T_out (empty rows: nothing); pass 2 reads that half back, continues the
+// lane's sum of squares over v = 0..3 (first half) then 4..7 (its own) -- the whole-row kernel's
+// order --, so the row scale, and every output bit, are the whole-row kernel's.
 template <int V, bool FULL>
 __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, float4 (&acc)[V], int lane,
                                                bool empty) {
     const int dp = FULL ? 128 * V : a.dp;
     if (empty && a.skip_zero_rows) return;           // acc is still all zeros
+    if (FULL && a.pass == 1) {
+        if (!empty) {
+            float4* out = reinterpret_cast<float4*>(a.T_out + row * (int64_t)a.dp);
+#pragma unroll
+            for (int v = 0; v < V; v++) __stcg(out + lane + 32 * v, acc[v]);
+        }
+#pragma unroll
+        for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    if (FULL && a.pass == 2) {
+        float4 h[V];
+        const float4* out = reinterpret_cast<const float4*>(a.T_out + row * (int64_t)a.dp);
+#pragma unroll
+        for (int v = 0; v < V; v++) h[v] = empty ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldcg(out + lane + 32 * v);
+        double ss = 0.0;
+#pragma unroll
+        for (int v = 0; v < V; v++) ss += sq4(h[v]);
+#pragma unroll
+        for (int v = 0; v < V; v++) ss += sq4(acc[v]);
+        ss = warp_sum(ss);
+        const double inv = inv_norm(ss);
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            put_out4(a, row, lane + 32 * v, scale4(h[v], inv), empty);
+            put_out4(a, row, 32 * V + lane + 32 * v, scale4(acc[v], inv), empty);   // float4 index in the row
+            acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        return;
+    }
     double ss = 0.0;
 #pragma unroll
     for (int v = 0; v < V; v++)
@@ -283,6 +320,66 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
     __syncthreads();
     float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
     double ss = 0.0;
+    if (FULL && a.pass > 0) {
+        // half-row passes: thread t stands for float4 t of the WHOLE row, as in the whole-row kernel
+        // (blockDim = 256 = a.dp / 4).  Pass 1 combines the first half (t < 128); pass 2 the second
+        // half (t >= 128) and takes the first from T_out (single-part rows) or the partials (below).
+        const int half = 128 * V / 4;                 // float4 per half row
+        const bool mine = a.pass == 1 ? t < half : t >= half;
+        const int tc = a.pass == 1 ? t : t - half;
+        if (mine) {
+            y = smem[tc];
+#pragma unroll
+            for (int w = 1; w < kWarpsPerCta; w++) {
+                const float4 q = smem[(size_t)w * ring_f4 + tc];
+                y.x += q.x; y.y += q.y; y.z += q.z; y.w += q.w;
+            }
+        }
+        if (it.nparts == 1) {
+            float4* outr = reinterpret_cast<float4*>(a.T_out + (int64_t)it.row * a.dp);
+            if (a.pass == 1) {
+                if (mine) __stcg(outr + t, y);
+            } else {
+                if (!mine) y = __ldcg(outr + t);
+                const double tot = block_sum(sq4(y), scratch);
+                const double inv = inv_norm(tot);
+                put_out4(a, it.row, t, scale4(y, inv));
+            }
+        } else {
+            float4* part = reinterpret_cast<float4*>(a.partials + (int64_t)it.slot * a.dp);
+            if (mine) part[t] = y;
+            if (a.pass == 2) {
+                __threadfence();
+                __syncthreads();
+                if (t == 0) {
+                    const unsigned prev = atomicAdd(a.counters + (it.slot - it.part), 1u);
+                    *flag = (prev == (unsigned)it.nparts - 1) ? 1 : 0;
+                }
+                __syncthreads();
+                if (*flag) {                          // the whole-row kernel's finish, over the whole row
+                    __threadfence();
+                    const int nqf = a.dp / 4;
+                    const float4* parts = reinterpret_cast<const float4*>(a.partials + (int64_t)(it.slot - it.part) * a.dp);
+                    double zx = 0, zy = 0, zz = 0, zw = 0;
+                    if (t < nqf) {
+                        for (int q = 0; q < it.nparts; q++) {
+                            const float4 p = __ldcg(parts + (int64_t)q * nqf + t);
+                            zx += p.x; zy += p.y; zz += p.z; zw += p.w;
+                        }
+                    }
+                    const double tot = block_sum(zx * zx + zy * zy + zz * zz + zw * zw, scratch);
+                    const double inv = inv_norm(tot);
+                    if (t < nqf)
+                        put_out4(a, it.row, t,
+                                 make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
+                    if (t == 0) a.counters[it.slot - it.part] = 0u;
+                }
+            }
+        }
+        __syncthreads();
+        fence_proxy_async_smem();
+        return;
+    }
     if (t < nq) {
         y = smem[t];
 #pragma unroll
@@ -433,8 +530,9 @@ Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
     {
         std::lock_guard<std::mutex> lk(mu);
         TmaCfg& cc = cfg[dev];
-        if (cc.dp != a.dp) {
-            const int slot = a.dp * 4;
+        const int width = FULL ? 128 * V : a.dp;      // floats gathered per row (half a row in a half pass)
+        if (cc.dp != width) {
+            const int slot = width * 4;
             // per-CTA ring budget ~96 KB so that two CTAs (16 warps) share an SM
             int S = SA > 0 ? SA : (96 * 1024) / (kWarpsPerCta * slot);
             if (S > 16 && SA == 0) S = 16;
@@ -447,7 +545,7 @@ Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
             CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cc.blocks_per_sm, k_spmm_tma<V, FULL, SA>,
                                                                       kWarpsPerCta * 32, cc.smem));
             if (cc.blocks_per_sm < 1) cc.blocks_per_sm = 1;
-            cc.dp = a.dp;
+            cc.dp = width;
         }
         c = cc;
     }
@@ -494,6 +592,10 @@ bool tma_path_supported(int dp) { return gather_mode(dp) != kGatherLdg; }
 
 Status launch_spmm_tma(const SpmmArgs& a, cudaStream_t s) {
     const int mode = a.gather_mode;
+    if (a.pass > 0) {                                 // half-row passes of dp = 1024 rows: 2 KB gathers
+        if (a.dp != 1024) return Status::make(4, "half-row passes need dp = 1024");
+        return launch_mode<4, true>(a, s, mode);
+    }
     if (a.dp == 1024) return launch_mode<8, true>(a, s, mode);
     if (a.dp == 512) return launch_mode<4, true>(a, s, mode);
     if (a.dp == 256) return launch_mode<2, true>(a, s, mode);

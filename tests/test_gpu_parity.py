@@ -436,3 +436,45 @@ def test_trim_keeps_the_embedding_and_frees_the_rest(cl):
                 call()
             assert e.value.code == 2
         G.close()
+
+
+@pytest.mark.parametrize("heavy", ["64", "8"])
+def test_half_row_passes_bitwise(cl, heavy, monkeypatch):
+    """dp = 1024 steps as two half-row passes (CLEORA_HALVES=1; the default where nnz >= 8 N, e.g. c4)
+    give bitwise the whole-row kernel's result (CLEORA_HALVES=0): light rows, single- and multi-part
+    heavy rows (threshold 8 makes most rows heavy), rows without out-edges (the zero-row skip from
+    step 3 on), weights, split iterate calls, and the loopback exchange (peer stores in pass 2)."""
+    monkeypatch.setenv("CLEORA_HEAVY_THRESH", heavy)
+    rng = np.random.default_rng(21)
+    n = 6000
+    hub = gen.EdgeList("hub", n, np.concatenate([np.zeros(5000, np.int32), rng.integers(0, n, 20000).astype(np.int32)]),
+                       np.concatenate([np.arange(1, 5001, dtype=np.int32), rng.integers(0, n, 20000).astype(np.int32)]),
+                       rng.lognormal(0, 1, 25000).astype(np.float32), True)
+    graphs = [hub, gen.rmat_directed(8192, 13, 120000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=22), gen.config("c1")]
+    for g in graphs:
+        outs = {}
+        for halves in ("0", "1"):
+            monkeypatch.setenv("CLEORA_HALVES", halves)
+            for mode in ("bulk", "async"):
+                monkeypatch.setenv("CLEORA_GATHER", mode)
+                for lb in (False, True):
+                    kw = dict(loopback=True, world=3, rank=1) if lb else {}
+                    G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0, **kw)
+                    cl.cleora_init(G, 1024, 3)
+                    cl.cleora_iterate(G, 2)
+                    cl.cleora_iterate(G, 2)
+                    outs[(halves, mode, lb)] = [cl.cleora_fetch_replica(G, p).tobytes() for p in range(3)] if lb else \
+                        [cl.cleora_fetch(G).tobytes()]
+                    G.close()
+        ref = outs[("0", "bulk", False)][0]
+        for key, reps in outs.items():
+            for b in reps:
+                assert b == ref, f"{g.name} heavy={heavy}: {key} differs from the whole-row kernel"
+    M = oracle.build_from(graphs[1])
+    monkeypatch.setenv("CLEORA_HALVES", "1")
+    monkeypatch.delenv("CLEORA_GATHER")
+    G = cl.cleora_build(graphs[1].src, graphs[1].dst, graphs[1].w, graphs[1].n, True, device=0)
+    cl.cleora_init(G, 1024, 3)
+    cl.cleora_iterate(G, 4)
+    compare(cl.cleora_fetch(G), oracle.embed(M, 1024, 3, 4), "halves vs oracle")
+    G.close()
