@@ -123,10 +123,10 @@ struct Ring {
 // `cp.async.wait_group SA-1` (all but the SA-1 most recent groups complete) is the whole
 // handshake.  Exactly one group is committed per issue -- an empty one past the end of the
 // stream -- so that positional wait always names the slot being consumed.
-template <int V, bool FULL, int SA>
+template <int V, bool FULL, int SA, bool HALF>
 __device__ __forceinline__ void ring_issue(const SpmmArgs& a, Ring& r, int slot, int32_t c, int lane) {
     // a.dp is the row stride; half-row passes gather 128 * V floats starting at column 512 * (pass == 2)
-    const int64_t col0 = a.pass == 2 ? 128 * V : 0;
+    const int64_t col0 = (HALF && a.pass == 2) ? 128 * V : 0;
     if (SA > 0) {
         const int dp = FULL ? 128 * V : a.dp;     // gathered width
         const float4* src = reinterpret_cast<const float4*>(a.T_in + (int64_t)(c & 0x7fffffff) * a.dp + col0) + lane;
@@ -170,12 +170,12 @@ __device__ __forceinline__ void ring_wait(Ring& r, int sl) {
 // of y unnormalised into T_out (empty rows: nothing); pass 2 reads that half back, continues the
 // lane's sum of squares over v = 0..3 (first half) then 4..7 (its own) -- the whole-row kernel's
 // order --, so the row scale, and every output bit, are the whole-row kernel's.
-template <int V, bool FULL>
+template <int V, bool FULL, bool HALF>
 __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, float4 (&acc)[V], int lane,
                                                bool empty) {
     const int dp = FULL ? 128 * V : a.dp;
     if (empty && a.skip_zero_rows) return;           // acc is still all zeros
-    if (FULL && a.pass == 1) {
+    if (HALF && a.pass == 1) {
         if (!empty) {
             float4* out = reinterpret_cast<float4*>(a.T_out + row * (int64_t)a.dp);
 #pragma unroll
@@ -185,7 +185,7 @@ __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, f
         for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
         return;
     }
-    if (FULL && a.pass == 2) {
+    if (HALF && a.pass == 2) {
         float4 h[V];
         const float4* out = reinterpret_cast<const float4*>(a.T_out + row * (int64_t)a.dp);
 #pragma unroll
@@ -222,7 +222,7 @@ __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, f
 // Stream CSR entries [E0, E1) through the warp's ring into acc.  ROWS: the entries belong to
 // rows [ra, rz) whose bounds are in rpl (lane i holds row_ptr[rb + i]); rows are finalised at
 // their boundaries (zero rows included).  On return every issued copy has been consumed.
-template <int V, bool FULL, bool ROWS, int SA>
+template <int V, bool FULL, bool ROWS, int SA, bool HALF>
 __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E1, float4 (&acc)[V], int64_t rb,
                                int64_t rpl, int64_t ra, int64_t rz, int lane) {
     const int dp = FULL ? 128 * V : a.dp;
@@ -245,7 +245,7 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
         int sl = r.cs;
         for (int i = 0; i < pro; i++) {
             const int32_t c = __shfl_sync(kFull, mc0, i);
-            ring_issue<V, FULL, SA>(a, r, sl, c, lane);
+            ring_issue<V, FULL, SA, HALF>(a, r, sl, c, lane);
             sl = (sl + 1 == r.S) ? 0 : sl + 1;
         }
         for (int i = pro; i < (SA > 0 ? SA : 0); i++) ring_skip<SA>();
@@ -257,7 +257,7 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
             if (ROWS) {
                 while (e >= kend) {                       // row boundary (warp-uniform)
                     const int64_t kbeg = __shfl_sync(kFull, rpl, (int)(row - rb));
-                    finalize_row_t<V, FULL>(a, row, acc, lane, kbeg == kend);
+                    finalize_row_t<V, FULL, HALF>(a, row, acc, lane, kbeg == kend);
                     row++;
                     kend = __shfl_sync(kFull, rpl, (int)(row - rb + 1));
                 }
@@ -274,7 +274,7 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
             const int jp = j + r.S;
             const int32_t cp = (jp < 32) ? __shfl_sync(kFull, mc0, jp) : __shfl_sync(kFull, mc1, jp - 32);
             if (e + r.S < E1)
-                ring_issue<V, FULL, SA>(a, r, sl, cp, lane);
+                ring_issue<V, FULL, SA, HALF>(a, r, sl, cp, lane);
             else
                 ring_skip<SA>();
             r.cs = (sl + 1 == r.S) ? 0 : sl + 1;
@@ -292,13 +292,13 @@ __device__ void stream_entries(const SpmmArgs& a, Ring& r, int64_t E0, int64_t E
         while (row < rz) {                                // last row and trailing zero rows
             const int64_t kbeg = __shfl_sync(kFull, rpl, (int)(row - rb));
             const int64_t kfin = __shfl_sync(kFull, rpl, (int)(row - rb + 1));
-            finalize_row_t<V, FULL>(a, row, acc, lane, kbeg == kfin);
+            finalize_row_t<V, FULL, HALF>(a, row, acc, lane, kbeg == kfin);
             row++;
         }
     }
 }
 
-template <int V, bool FULL, int SA>
+template <int V, bool FULL, int SA, bool HALF>
 __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* smem, int ring_f4, double* scratch,
                              int* flag) {
     const HeavyItem it = a.items[idx];
@@ -311,7 +311,7 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
     float4 acc[V];
 #pragma unroll
     for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    stream_entries<V, FULL, false, SA>(a, r, wk0, wk1, acc, 0, 0, 0, 0, lane);
+    stream_entries<V, FULL, false, SA, HALF>(a, r, wk0, wk1, acc, 0, 0, 0, 0, lane);
     // this warp's partial vector -> slot 0 of its ring (drained), combined in warp order
     float4* red = r.buf;
 #pragma unroll
@@ -320,7 +320,7 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
     __syncthreads();
     float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
     double ss = 0.0;
-    if (FULL && a.pass > 0) {
+    if (HALF) {
         // half-row passes: thread t stands for float4 t of the WHOLE row, as in the whole-row kernel
         // (blockDim = 256 = a.dp / 4).  Pass 1 combines the first half (t < 128); pass 2 the second
         // half (t >= 128) and takes the first from T_out (single-part rows) or the partials (below).
@@ -425,7 +425,7 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
     fence_proxy_async_smem();     // accesses before the async-proxy writes
 }
 
-template <int V, bool FULL, int SA>
+template <int V, bool FULL, int SA, bool HALF>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArgs a, int S) {
     extern __shared__ __align__(128) float4 smem[];
     __shared__ double scratch[kWarpsPerCta];
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
             const int64_t it = s_item;
             __syncthreads();
             if (it >= n_items) break;
-            heavy_item_t<V, FULL, SA>(a, it, r, smem, ring_f4, scratch, &flag);
+            heavy_item_t<V, FULL, SA, HALF>(a, it, r, smem, ring_f4, scratch, &flag);
         }
     }
     const int64_t nchunks = a.counts[0];
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
                 z++;
             }
             const int64_t E1 = __shfl_sync(kFull, rpl, (int)(z - rb));
-            stream_entries<V, FULL, true, SA>(a, r, E0, E1, acc, rb, rpl, row, z, lane);
+            stream_entries<V, FULL, true, SA, HALF>(a, r, E0, E1, acc, rb, rpl, row, z, lane);
             row = z;
         }
     }
@@ -519,7 +519,7 @@ struct TmaCfg {
 };
 
 // Launch configuration per device (the smem attribute is per device) and row stride.
-template <int V, bool FULL, int SA>
+template <int V, bool FULL, int SA, bool HALF = false>
 Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
     static TmaCfg cfg[kMaxDevices];
     static std::mutex mu;
@@ -539,10 +539,10 @@ Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
             if (S < 2) S = 2;
             cc.S = S;
             cc.smem = (size_t)kWarpsPerCta * S * slot + (SA > 0 ? 0 : (size_t)kWarpsPerCta * S * sizeof(uint64_t));
-            CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_tma<V, FULL, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_tma<V, FULL, SA, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)cc.smem));
             CL_CUDA_TRY(cudaDeviceGetAttribute(&cc.sms, cudaDevAttrMultiProcessorCount, dev));
-            CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cc.blocks_per_sm, k_spmm_tma<V, FULL, SA>,
+            CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cc.blocks_per_sm, k_spmm_tma<V, FULL, SA, HALF>,
                                                                       kWarpsPerCta * 32, cc.smem));
             if (cc.blocks_per_sm < 1) cc.blocks_per_sm = 1;
             cc.dp = width;
@@ -550,7 +550,7 @@ Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
         c = cc;
     }
     if (a.r1 <= a.r0 && a.n_items_max == 0) return Status::ok();
-    k_spmm_tma<V, FULL, SA><<<c.sms * c.blocks_per_sm, kWarpsPerCta * 32, c.smem, s>>>(a, c.S);
+    k_spmm_tma<V, FULL, SA, HALF><<<c.sms * c.blocks_per_sm, kWarpsPerCta * 32, c.smem, s>>>(a, c.S);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     return Status::ok();
@@ -560,10 +560,10 @@ Status launch_tma_v(const SpmmArgs& a, cudaStream_t s) {
 template <int V>
 constexpr int kAsyncSlots = V == 1 ? 24 : (V == 2 ? 12 : (V == 4 ? 6 : 3));
 
-template <int V, bool FULL>
+template <int V, bool FULL, bool HALF = false>
 Status launch_mode(const SpmmArgs& a, cudaStream_t s, int mode) {
-    if (mode == kGatherAsync) return launch_tma_v<V, FULL, kAsyncSlots<V>>(a, s);
-    return launch_tma_v<V, FULL, 0>(a, s);
+    if (mode == kGatherAsync) return launch_tma_v<V, FULL, kAsyncSlots<V>, HALF>(a, s);
+    return launch_tma_v<V, FULL, 0, HALF>(a, s);
 }
 
 }  // namespace
@@ -594,7 +594,7 @@ Status launch_spmm_tma(const SpmmArgs& a, cudaStream_t s) {
     const int mode = a.gather_mode;
     if (a.pass > 0) {                                 // half-row passes of dp = 1024 rows: 2 KB gathers
         if (a.dp != 1024) return Status::make(4, "half-row passes need dp = 1024");
-        return launch_mode<4, true>(a, s, mode);
+        return launch_mode<4, true, true>(a, s, mode);
     }
     if (a.dp == 1024) return launch_mode<8, true>(a, s, mode);
     if (a.dp == 512) return launch_mode<4, true>(a, s, mode);
