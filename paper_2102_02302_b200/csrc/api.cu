@@ -1329,6 +1329,10 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
         // peers map T through CUDA IPC, which exports whole allocations: T at a segment's base
         const int tflags = g->xmode == X_PEER ? kAllocBase : 0;
         for (int i = 0; i < 2 && sa.good(); i++) sa = dalloc((void**)&g->T[i], tb, g->stream, "embedding T", tflags);
+        // test hook: this rank's T allocation fails (CLEORA_TEST_FAIL_T_RANK=r), to exercise the agreement
+        if (const char* fr = getenv("CLEORA_TEST_FAIL_T_RANK"))
+            if (g->world > 1 && atoi(fr) == g->rank && sa.good())
+                sa = Status::make(4, "cleora_init: injected allocation failure (CLEORA_TEST_FAIL_T_RANK)");
         if (sa.good() && g->xmode == X_LOOPBACK) {
             g->rep[g->rank] = {g->T[0], g->T[1]};
             for (int p = 0; p < g->world && sa.good(); p++) {

@@ -1,4 +1,4 @@
-"""The real multi-process exchange on ONE GPU: two processes, each a rank of a world-2 handle,
+"""The real multi-process exchange on ONE GPU: two or three processes, each a rank of one handle,
 collectives through the caller's host all-gather (gloo; NCCL refuses two ranks on one device), the
 fused peer-store exchange through CUDA IPC mappings of each other's T buffers (X_PEER).
 
@@ -56,10 +56,10 @@ def _worker(rank, world, port, q):
             res.append((gr.name, d, calls, info["exchange"], info["shard_begin"], info["shard_end"],
                         cl.cleora_ipc_opens() - opens0, T.tobytes()))
             if rank == 0:
-                G.close()                 # rank 1 still maps this rank's blocks (returned to the cache)
+                G.close()                 # the other ranks still map this rank's blocks (back in its cache)
             dist.barrier()
-            if rank == 1:
-                T2 = cl.cleora_fetch(G)   # its own replica is untouched by rank 0's destroy
+            if rank != 0:
+                T2 = cl.cleora_fetch(G)   # their own replicas are untouched by rank 0's destroy
                 assert T2.tobytes() == T.tobytes()
                 G.close()
             dist.barrier()
@@ -79,7 +79,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_processes_one_gpu_peer_exchange():
+@pytest.mark.parametrize("world", [2, 3])
+def test_processes_one_gpu_peer_exchange(world):
     import torch
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():
@@ -87,18 +88,18 @@ def test_two_processes_one_gpu_peer_exchange():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     got = {}
-    for _ in range(2):
+    for _ in range(world):
         rank, res, out = q.get(timeout=900)
         assert res != "error", out
         got[rank] = (res, out)
     for p in procs:
         p.join(timeout=120)
     refs = got[0][1]
-    for rank in (0, 1):
+    for rank in range(world):
         res = got[rank][0]
         for i, (name, d, calls, mode, b, e, opens, T) in enumerate(res):
             assert mode == 2, f"rank {rank}: exchange mode {mode}, expected fused peer stores (2)"
@@ -106,3 +107,49 @@ def test_two_processes_one_gpu_peer_exchange():
             if i == 1:      # same graph and d as case 0: the peer's blocks come back from its cache
                 assert opens == 0, f"rank {rank}: {opens} new IPC mappings for a repeated handle"
         assert res[0][4] == (0 if rank == 0 else res[0][4]) and res[0][5] > res[0][4]
+
+
+def _fail_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    import gen
+    import paper_2102_02302_b200 as cl
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), CLEORA_TEST_FAIL_T_RANK="1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        ag = cl.host_allgather_from()
+        g = gen.chung_lu(20000, 60000, 2.1, 9.5388, 233115.5 * 20000 / 1134890, seed=2)
+        G = cl.cleora_build(g.src, g.dst, None, g.n, False, device=0, rank=rank, world=world, host_allgather=ag)
+        try:
+            cl.cleora_init(G, 256, 0)
+            q.put((rank, "no error"))
+        except cl.CleoraError as e:
+            q.put((rank, str(e)))
+        G.close()
+    except Exception as e:
+        q.put((rank, "unexpected: " + repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_one_rank_failing_fails_every_rank():
+    """Failure agreement: rank 1's T allocation fails (injected); instead of the others
+    blocking in the next collective (the IPC handle exchange), every rank's cleora_init returns an
+    error -- rank 1 its own, the others "rank 1 of 3 failed"."""
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_fail_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(3))
+    for p in procs:
+        p.join(timeout=60)
+    assert "injected" in got[1], got
+    assert "rank 1 of 3 failed" in got[0] and "rank 1 of 3 failed" in got[2], got
