@@ -554,8 +554,13 @@ def main():
     k_rate, k_nnz, k_ms = kernel_l2_rate(cl, g, dev, local, stream) if world == 1 else (0.0, 0, 0.0)
     best_rate = max(l2_rate, k_rate)
     gather_b = nnz * d * 4 / world
+    lps = info.get("launches_per_step", 1) or 1
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic(g.name, d), "kernel": "k_spmm_tma (fused SpMM + row L2 normalise)",
+                "traffic": load_traffic(g.name, d),
+                "kernel": "k_spmm_tma (fused SpMM + row L2 normalise)" + (
+                    f", {lps} half-row launches per iteration (bitwise the whole-row result); figures per iteration"
+                    if lps > 1 else ""),
+                "launches_per_iteration": lps,
                 "kernel_ms": spmm_ms, "kernel_timing": "CUDA events around cleora_iterate in the timed steps",
                 "algorithmic_bytes_per_launch": b_comp, "peak_source": peak_src,
                 "strict_bytes_per_launch": b_strict, "strict_frac": b_strict / (spmm_ms / 1e3) / 1e9 / peak,

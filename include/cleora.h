@@ -278,6 +278,8 @@ typedef struct cleora_info_t {
     int32_t exchange;       /* 0 one GPU, 1 NCCL all-gather, 2 fused peer stores, 3 loopback */
     int32_t n_graphs;       /* graphs in a batched handle (cleora_build_batch), else 0   */
     int64_t shard_nnz;      /* entries of this rank's rows (= nnz on one GPU)               */
+    int32_t launches_per_step; /* SpMM launches per iteration: 2 when d's 1024 columns run as two
+                                  half-row passes (bitwise the same result), else 1 (0 before init) */
 } cleora_info_t;
 /* Fill *out.  Synchronises the handle's stream (zero_rows and max_degree are computed on the device
  * by cleora_build and read back here, on first use; the handle caches them -- hence non-const).

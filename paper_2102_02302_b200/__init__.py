@@ -79,7 +79,7 @@ class _Info(ctypes.Structure):
                 ("heavy_items", ctypes.c_int64), ("shard_begin", ctypes.c_int64), ("shard_end", ctypes.c_int64),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
                 ("hot_rows", ctypes.c_int64), ("referenced_rows", ctypes.c_int64), ("exchange", ctypes.c_int32),
-                ("n_graphs", ctypes.c_int32), ("shard_nnz", ctypes.c_int64)]
+                ("n_graphs", ctypes.c_int32), ("shard_nnz", ctypes.c_int64), ("launches_per_step", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):

@@ -1853,6 +1853,7 @@ int cleora_info(cleora_graph* g, cleora_info_t* o) {
     o->hot_rows = g->n_hot;
     o->n_graphs = g->n_graphs;
     o->shard_nnz = g->csr.empty() ? 0 : g->own().nnz;
+    o->launches_per_step = g->T[0] ? (g->halves ? 2 : 1) : 0;
     o->referenced_rows = g->n_ref;
     o->exchange = g->xmode;
     o->device_bytes = g->bytes + ((g->T[0] ? 1 : 0) + (g->T[1] ? 1 : 0)) * (int64_t)g->n * g->dp * 4 +

@@ -35,6 +35,9 @@
 #ifndef CLEORA_PAIR_PU
 #define CLEORA_PAIR_PU 3       // paired rows: neighbours per half-warp per step (A/B: 1-4)
 #endif
+#ifndef CLEORA_V1_DPC
+#define CLEORA_V1_DPC 1        // rows of exactly 512 B (dp = 128): a kernel with the stride compiled in
+#endif
 #ifndef CLEORA_V1_BLOCKS
 #define CLEORA_V1_BLOCKS 4     // rows of <= 512 B: resident CTAs per SM
 #endif
@@ -106,12 +109,12 @@ __device__ __forceinline__ float csr_f32(const float* p, const Pol& pol) {
 }
 
 // acc[v] += sum_{k in [k0,k1)} val[k] * T_in[col[k]][cbase + 4*(lane + 32 v) .. +3], ascending k.
-template <int V, bool H>
+template <int V, bool H, int DPC = 0>
 __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, const Pol& pol, int64_t k0, int64_t k1, int cbase,
                                                 int lane, float4 (&acc)[V]) {
     // neighbours per batch: U*V 16-byte loads in flight
     constexpr int U = V == 1 ? CLEORA_V1_U : ((16 / V > 8) ? 8 : 16 / V);
-    const int dp = a.dp;
+    const int dp = DPC > 0 ? DPC : a.dp;
     bool ok[V];
 #pragma unroll
     for (int v = 0; v < V; v++) ok[v] = cbase + 4 * (lane + 32 * v) < dp;
@@ -158,10 +161,10 @@ __device__ __forceinline__ void accumulate_warp(const SpmmArgs& a, const Pol& po
     }
 }
 
-template <int V, bool H>
+template <int V, bool H, int DPC = 0>
 __device__ void light_row(const SpmmArgs& a, const Pol& pol, int64_t row, int64_t k0, int64_t k1, int lane) {
     constexpr int SW = 128 * V;                   // floats per column slice
-    const int dp = a.dp;
+    const int dp = DPC > 0 ? DPC : a.dp;
     const int ns = (dp + SW - 1) / SW;
     if (k1 == k0 && a.skip_zero_rows) return;     // already 0 in T_out (reading RZ)
     float4* out = reinterpret_cast<float4*>(a.T_out + row * (int64_t)dp);
@@ -171,7 +174,7 @@ __device__ void light_row(const SpmmArgs& a, const Pol& pol, int64_t row, int64_
         const int cbase = sl * SW;
 #pragma unroll
         for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        accumulate_warp<V, H>(a, pol, k0, k1, cbase, lane, acc);
+        accumulate_warp<V, H, DPC>(a, pol, k0, k1, cbase, lane, acc);
 #pragma unroll
         for (int v = 0; v < V; v++) {
             const int f = cbase / 4 + lane + 32 * v;
@@ -202,12 +205,13 @@ __device__ void light_row(const SpmmArgs& a, const Pol& pol, int64_t row, int64_
 // tree -- lane hl adds its two columns (= the xor-16 step of the 32-lane butterfly), then the
 // xor 8/4/2/1 steps stay inside the half.  `live` = false: this half has no row (odd tail, heavy
 // row); it still executes every shuffle.
-template <bool H>
+// DPC: the row stride as a compile-time constant (128: f4 batches, c1), 0 = a.dp at run time
+template <bool H, int DPC>
 __device__ void light_row_pair(const SpmmArgs& a, const Pol& pol, int64_t row, int64_t k0, int64_t k1, bool live,
                                int lane) {
     constexpr int PU = CLEORA_PAIR_PU;             // neighbours per half per step
     const int hl = lane & 15, base = lane & 16;
-    const int dp = a.dp;
+    const int dp = DPC > 0 ? DPC : a.dp;
     const bool ok0 = 4 * hl < dp, ok1 = 4 * (hl + 16) < dp;
     const int64_t n_row = live ? k1 - k0 : 0;
     const int64_t n_max = max(n_row, __shfl_xor_sync(kFull, n_row, 16));
@@ -366,7 +370,7 @@ __device__ void heavy_item(const SpmmArgs& a, const Pol& pol, int64_t idx, float
 template <int V>
 constexpr int kNormMinBlocks = V == 1 ? CLEORA_V1_BLOCKS : 2;   // V = 2 at 3 CTAs spills: c5 357 -> 478 ms
 
-template <int V, bool H>
+template <int V, bool H, int DPC>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_norm(const SpmmArgs a) {
     extern __shared__ float4 red[];
     __shared__ double scratch[kWarpsPerCta];
@@ -415,10 +419,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_n
                 const int64_t lim = min((int64_t)CLEORA_V1_PAIR, (int64_t)a.heavy_thresh);
                 if (two && e1 - e0 <= lim && e2 - e1 <= lim) {
                     const bool hi = lane >= 16;
-                    light_row_pair<H>(a, pol, r + (hi ? 1 : 0), hi ? e1 : e0, hi ? e2 : e1, true, lane);
+                    light_row_pair<H, DPC>(a, pol, r + (hi ? 1 : 0), hi ? e1 : e0, hi ? e2 : e1, true, lane);
                     r += 2;
                 } else {
-                    if (e1 - e0 <= a.heavy_thresh) light_row<V, H>(a, pol, r, e0, e1, lane);
+                    if (e1 - e0 <= a.heavy_thresh) light_row<V, H, DPC>(a, pol, r, e0, e1, lane);
                     r += 1;
                 }
             }
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kNormMinBlocks<V>) k_spmm_n
     }
 }
 
-template <int V, bool H>
+template <int V, bool H, int DPC = 0>
 Status launch_vh(const SpmmArgs& a, cudaStream_t s) {
     const size_t smem = (size_t)kWarpsPerCta * 32 * V * sizeof(float4);
     // per device: the smem attribute and the occupancy are per device
@@ -458,10 +462,10 @@ Status launch_vh(const SpmmArgs& a, cudaStream_t s) {
     {
         std::lock_guard<std::mutex> lk(mu);
         if (!bps[dev]) {
-            CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_norm<V, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CL_CUDA_TRY(cudaFuncSetAttribute(k_spmm_norm<V, H, DPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             CL_CUDA_TRY(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
             int b = 0;
-            CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmm_norm<V, H>, kWarpsPerCta * 32, smem));
+            CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmm_norm<V, H, DPC>, kWarpsPerCta * 32, smem));
             bps[dev] = b < 1 ? 1 : b;
         }
         blocks_per_sm = bps[dev];
@@ -469,7 +473,7 @@ Status launch_vh(const SpmmArgs& a, cudaStream_t s) {
     }
     if (a.r1 <= a.r0 && a.n_items_max == 0) return Status::ok();
     const int grid = sms * blocks_per_sm;                // one persistent wave
-    k_spmm_norm<V, H><<<grid, kWarpsPerCta * 32, smem, s>>>(a);
+    k_spmm_norm<V, H, DPC><<<grid, kWarpsPerCta * 32, smem, s>>>(a);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     return Status::ok();
@@ -478,6 +482,8 @@ Status launch_vh(const SpmmArgs& a, cudaStream_t s) {
 // cache hints only when there are hot rows (a.cold_first: hot_tag pinned some rows)
 template <int V>
 Status launch_v(const SpmmArgs& a, cudaStream_t s) {
+    if (CLEORA_V1_DPC && V == 1 && a.dp == 128)   // full 512 B rows: no per-column bounds, shifts for addresses
+        return a.cold_first ? launch_vh<V, true, 128>(a, s) : launch_vh<V, false, 128>(a, s);
     return a.cold_first ? launch_vh<V, true>(a, s) : launch_vh<V, false>(a, s);
 }
 
