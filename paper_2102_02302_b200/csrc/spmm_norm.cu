@@ -33,7 +33,7 @@
 #define CLEORA_V1_PAIR 16      // rows of <= 512 B: two rows of <= this many entries per warp
 #endif
 #ifndef CLEORA_PAIR_PU
-#define CLEORA_PAIR_PU 3       // paired rows: neighbours per half-warp per step (A/B: 1-4)
+#define CLEORA_PAIR_PU 2       // paired rows: neighbours per half-warp per step (A/B: r01 1-4 -> 3; r02 with the compiled-in stride 2-4 -> 2)
 #endif
 #ifndef CLEORA_V1_DPC
 #define CLEORA_V1_DPC 1        // rows of exactly 512 B (dp = 128): a kernel with the stride compiled in
@@ -484,6 +484,8 @@ template <int V>
 Status launch_v(const SpmmArgs& a, cudaStream_t s) {
     if (CLEORA_V1_DPC && V == 1 && a.dp == 128)   // full 512 B rows: no per-column bounds, shifts for addresses
         return a.cold_first ? launch_vh<V, true, 128>(a, s) : launch_vh<V, false, 128>(a, s);
+    if (CLEORA_V1_DPC && V == 1 && a.dp == 64)
+        return a.cold_first ? launch_vh<V, true, 64>(a, s) : launch_vh<V, false, 64>(a, s);
     return a.cold_first ? launch_vh<V, true>(a, s) : launch_vh<V, false>(a, s);
 }
 
