@@ -462,19 +462,64 @@ __global__ void k_shard_keys(uint32_t* __restrict__ pos, int64_t n, const int32_
     }
 }
 
+// Small builds carve their transient buffers out of one block (an arena), so that a graph of 10^5
+// entries costs one allocation instead of ~12 cudaMallocAsync / cudaFreeAsync pairs -- on such graphs
+// the host's enqueue rate, not the GPU, sets the build time (c1: profiles/r02_c1_trace.json).
+struct Arena {
+    char* base = nullptr;
+    size_t cap = 0, used = 0;
+};
+thread_local Arena tl_arena;
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
     cudaStream_t s = nullptr;
+    bool in_arena = false;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
-    ~DevBuf() { if (p) dfree(p, s); }
+    ~DevBuf() { drop(); }
     // transient unless the buffer outlives the call (released into a CSR or a schedule)
     Status alloc(size_t n, cudaStream_t st, const char* what, bool long_lived = false) {
         s = st;
-        return dalloc((void**)&p, n * sizeof(T) + 16, st, what, long_lived ? 0 : kAllocTransient);
+        const size_t bytes = n * sizeof(T) + 16;
+        Arena& a = tl_arena;
+        if (!long_lived && a.base) {
+            const size_t off = (a.used + 255) & ~(size_t)255;
+            if (off + bytes <= a.cap) {
+                p = reinterpret_cast<T*>(a.base + off);
+                a.used = off + bytes;
+                in_arena = true;
+                return Status::ok();
+            }
+        }
+        return dalloc((void**)&p, bytes, st, what, long_lived ? 0 : kAllocTransient);
     }
-    T* release() { T* q = p; p = nullptr; return q; }
+    T* release() { T* q = p; p = nullptr; return q; }      // long-lived buffers only
+    void drop() {                                           // free now (a no-op inside the arena)
+        if (p && !in_arena) dfree(p, s);
+        p = nullptr;
+    }
+};
+
+// Installs an arena of `bytes` for the current thread (if bytes > 0 and it can be had) until the
+// guard goes out of scope; nested guards leave an installed arena alone.
+struct ArenaGuard {
+    bool mine = false;
+    cudaStream_t s;
+    ArenaGuard(size_t bytes, cudaStream_t st) : s(st) {
+        static const bool off = getenv("CLEORA_NO_ARENA") != nullptr;   // A/B switch
+        if (off || bytes == 0 || tl_arena.base) return;
+        void* p = nullptr;
+        if (!dalloc(&p, bytes, st, "build arena", kAllocTransient).good()) return;
+        tl_arena = Arena{(char*)p, bytes, 0};
+        mine = true;
+    }
+    ~ArenaGuard() {
+        if (!mine) return;
+        dfree(tl_arena.base, s);
+        tl_arena = Arena{};
+    }
 };
 
 }  // namespace
@@ -495,6 +540,9 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     const uint64_t sentinel = NN;                        // sorts after every valid key
     const int end_bit = 64 - __builtin_clzll(sentinel | 1ull);
 
+    // small builds: one block for every transient buffer (sort keys x2, payloads x2, flags, run starts,
+    // rows, e_ab, CUB temporaries: < 64 bytes per entry)
+    ArenaGuard arena(n_ent <= (1 << 20) ? (size_t)n_ent * 64 + ((size_t)4 << 20) : 0, s);
     DevBuf<uint64_t> keys, keys2;
     DevBuf<uint32_t> pos, pos2;                          // sort payload: the entries' weights (fp32 bits)
     DevBuf<unsigned long long> scal;                     // [0] err_first [1] n_self [2] zero_rows [3] max_deg [4] nnz
@@ -557,8 +605,8 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         if (kb.Current() != keys.p) std::swap(keys.p, keys2.p);
         if (!keys_only && vb.Current() != pos.p) std::swap(pos.p, pos2.p);
     }
-    dfree(keys2.release(), s);
-    if (keys_only) dfree(pos.release(), s);             // shard mode: positions only made the keys
+    keys2.drop();
+    if (keys_only) pos.drop();             // shard mode: positions only made the keys
     trace("csr: radix sort", s, true);
 
     // B2: run starts of equal keys, merged weights.  Over all n_ent keys (the dropped entries carry
@@ -580,7 +628,7 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         CL_CUDA_TRY(cub::DeviceSelect::Flagged(tmp.p, tmp_bytes, it, flags.p, run_start.p, scal.p + 4, n_ent, s));
         count_launches(2);
     }
-    dfree(flags.release(), s);
+    flags.drop();
     trace("csr: run select", s, false);
 
     // the merged entries are at most the sorted ones: everything below is sized for n_ent and reads the
@@ -597,10 +645,10 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     trace("csr: merge runs", s, true);
-    dfree(run_start.release(), s);
-    dfree(keys.release(), s);
-    dfree(pos.release(), s);
-    dfree(pos2.release(), s);
+    run_start.drop();
+    keys.drop();
+    pos.drop();
+    pos2.drop();
 
     CL_TRY(row_ptr.alloc((size_t)N + 1, s, "CSR row_ptr", true));
     CL_CUDA_TRY(cudaMemsetAsync(row_ptr.p, 0, sizeof(int64_t), s));
