@@ -121,17 +121,15 @@ static bool g_pool_cfg[64];
 namespace {
 constexpr size_t kCacheMin = (size_t)1 << 20;
 constexpr size_t kCacheGrain = (size_t)2 << 20;
-struct Range {                      // a piece of a segment, free or handed out
+struct Segment {                    // a cudaMalloc block, handed out or cached
     size_t bytes;
     int dev;
-    char* seg;                      // base of its segment
-    size_t seg_bytes;
     bool free;
-    std::vector<cudaEvent_t> ready; // free ranges: reuse waits on these
+    std::vector<cudaEvent_t> ready; // cached: the next user waits on these
 };
 std::mutex g_cache_mu;
-std::map<char*, Range> g_ranges;    // every range of every segment, by address
-size_t g_free_bytes = 0;            // bytes in free ranges
+std::map<char*, Segment> g_segs;    // every segment, by address
+size_t g_free_bytes = 0;            // bytes in cached (free) segments
 std::vector<cudaEvent_t> g_ev_pool;
 std::atomic<int64_t> g_oom_fallbacks{0};
 
@@ -151,38 +149,35 @@ cudaEvent_t ev_get() {              // caller holds g_cache_mu
     return e;
 }
 
-// Take the free segments that are whole (one free range) out of the cache: all of `dev` (-1: every
-// device), or only the largest one.  Caller frees them with cudaFree after waiting for their events.
+// Take cached segments out of the cache: all of `dev` (-1: every device), or only the largest one.
+// The caller frees them with cudaFree after waiting for their events.
 struct Dropped {
     char* p;
     int dev;
     std::vector<cudaEvent_t> ready;
 };
-std::vector<Dropped> take_whole_free(int dev, bool largest_only) {
+std::vector<Dropped> take_free(int dev, bool largest_only) {
     std::vector<Dropped> out;
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    char* best = nullptr;
-    size_t best_b = 0;
-    for (auto it = g_ranges.begin(); it != g_ranges.end();) {
-        Range& r = it->second;
-        const bool whole = r.free && it->first == r.seg && r.bytes == r.seg_bytes;
-        if (whole && (dev < 0 || r.dev == dev)) {
+    auto best = g_segs.end();
+    for (auto it = g_segs.begin(); it != g_segs.end();) {
+        Segment& r = it->second;
+        if (r.free && (dev < 0 || r.dev == dev)) {
             if (largest_only) {
-                if (r.bytes > best_b) { best_b = r.bytes; best = it->first; }
+                if (best == g_segs.end() || r.bytes > best->second.bytes) best = it;
             } else {
                 out.push_back({it->first, r.dev, std::move(r.ready)});
                 g_free_bytes -= r.bytes;
-                it = g_ranges.erase(it);
+                it = g_segs.erase(it);
                 continue;
             }
         }
         ++it;
     }
-    if (largest_only && best) {
-        auto it = g_ranges.find(best);
-        out.push_back({best, it->second.dev, std::move(it->second.ready)});
-        g_free_bytes -= it->second.bytes;
-        g_ranges.erase(it);
+    if (largest_only && best != g_segs.end()) {
+        out.push_back({best->first, best->second.dev, std::move(best->second.ready)});
+        g_free_bytes -= best->second.bytes;
+        g_segs.erase(best);
     }
     return out;
 }
@@ -202,64 +197,46 @@ void free_dropped(std::vector<Dropped>& v) {
     v.clear();
 }
 
-void release_cached(int dev /* -1: all */, cudaStream_t s) {
-    auto v = take_whole_free(dev, false);
+void release_cached(int dev /* -1: all */) {
+    auto v = take_free(dev, false);
     free_dropped(v);
-    (void)s;
 }
 
 bool release_largest(int dev) {
-    auto v = take_whole_free(dev, true);
+    auto v = take_free(dev, true);
     if (v.empty()) return false;
     free_dropped(v);
     return true;
 }
 
-// Two size classes that never share a segment: a long-lived small buffer (a row pointer) carved out of
-// a 40 GB segment would keep the whole segment from ever going back to the driver.
-constexpr size_t kBigClass = (size_t)1 << 30;
-inline bool big_class(size_t b) { return b >= kBigClass; }
-
-// best-fit free range of `dev` for `rb` bytes (`base`: starting at a segment base; `tight`: at most
-// 1/8 larger than rb) in segments of rb's size class; split off the tail; the stream waits for the
-// range's events.  Caller holds g_cache_mu.
-void* take_range(int dev, size_t rb, bool base, bool tight, cudaStream_t s) {
-    auto best = g_ranges.end();
-    for (auto it = g_ranges.begin(); it != g_ranges.end(); ++it) {
-        const Range& r = it->second;
-        if (!r.free || r.dev != dev || r.bytes < rb || (base && it->first != r.seg)) continue;
-        // no splitting: a cached segment is handed out whole and of exactly the size asked for (rounded
-        // to 2 MiB).  Two alternatives were measured on c5's e2e pipeline, where one step's working
-        // set nearly fills the 180 GB, and dropped: splitting segments (best fit, merging freed
-        // neighbours) let pieces of long-lived buffers pin large segments, and lending transient
-        // buffers segments up to twice their size wasted the rest; either way a 22.7 GB sort buffer
-        // later found no room and nothing to give back -- a hard out-of-memory error where exact
-        // whole segments only cost cudaFree/cudaMalloc round trips (profiles/r02_bench_c5_oom.txt)
-        (void)tight;
-        if (r.bytes != rb) continue;
-        if (big_class(r.seg_bytes) != big_class(rb)) continue;
-        if (best == g_ranges.end() || r.bytes < best->second.bytes) best = it;
+// A cached segment of `dev` of exactly `rb` bytes (2 MiB-rounded); the stream waits for its events.
+// Caller holds g_cache_mu.  Exact sizes, no splitting: two alternatives were measured on c5's e2e
+// pipeline, where one step's working set nearly fills the 180 GB, and dropped -- splitting segments
+// (best fit, merging freed neighbours) let pieces of long-lived buffers pin large segments, and lending
+// transient buffers segments up to twice their size wasted the rest; either way a 22.7 GB sort buffer
+// later found no room and nothing to give back, a hard out-of-memory error where exact whole segments
+// only cost cudaFree/cudaMalloc round trips (profiles/r02_bench_c5_oom.txt).
+void* take_cached(int dev, size_t rb, cudaStream_t s) {
+    for (auto& kv : g_segs) {
+        Segment& r = kv.second;
+        if (!r.free || r.dev != dev || r.bytes != rb) continue;
+        for (auto e : r.ready) {
+            cudaStreamWaitEvent(s, e, 0);
+            g_ev_pool.push_back(e);
+        }
+        r.ready.clear();
+        r.free = false;
+        g_free_bytes -= r.bytes;
+        return kv.first;
     }
-    if (best == g_ranges.end()) return nullptr;
-    char* p = best->first;
-    Range& r = best->second;
-    for (auto e : r.ready) {
-        cudaStreamWaitEvent(s, e, 0);
-        g_ev_pool.push_back(e);
-    }
-    r.ready.clear();
-    r.free = false;
-    g_free_bytes -= r.bytes;
-    return p;
+    return nullptr;
 }
 }  // namespace
 
 Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, int flags) {
+    // kAllocTransient is a hint only (both kinds are served alike); kAllocBase: a whole cudaMalloc
+    // segment whatever the size (T buffers: CUDA IPC cannot export pool memory)
     const bool block = flags & kAllocBase;
-    // transient buffers (sort keys, run starts, staged inputs: freed before the call returns) may be
-    // carved out of any free range; long-lived ones (CSR, T, schedules) take a range that fits tightly
-    // or a new segment, so that they never pin a large segment they only use a corner of
-    const bool tight = !(flags & kAllocTransient);
     *p = nullptr;
     int dev = 0;
     CL_CUDA_TRY(cudaGetDevice(&dev));
@@ -275,14 +252,12 @@ Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, int flag
         }
     }
     if (bytes == 0) bytes = 16;
-    // block: a range at the base of a cudaMalloc segment whatever the size (T buffers: CUDA IPC cannot
-    // export pool memory, and exports whole allocations)
     static const bool no_cache = getenv("CLEORA_NO_CACHE") != nullptr;
     const bool big = block || (bytes >= kCacheMin && !no_cache);
     const size_t rb = round_block(bytes);
     if (big) {
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        if (void* q = take_range(dev, rb, block, tight, s)) {
+        if (void* q = take_cached(dev, rb, s)) {
             *p = q;
             return Status::ok();
         }
@@ -298,20 +273,12 @@ Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, int flag
         if (e == cudaSuccess) break;
         cudaGetLastError();
         *p = nullptr;
-        // out of memory: give whole free segments back to the driver, largest first, until it fits
+        // out of memory: give cached segments back to the driver, largest first, until it fits
         if (e == cudaErrorMemoryAllocation && release_largest(dev)) {
             g_oom_fallbacks.fetch_add(1);
             static const bool tr = getenv("CLEORA_TRACE") != nullptr;
             if (tr) fprintf(stderr, "[cleora trace] out of memory for %s (%zu bytes): released a cached segment\n", what, bytes);
             continue;
-        }
-        if (e == cudaErrorMemoryAllocation && big && tight) {
-            // nothing left to give back: as a last resort carve a long-lived buffer out of any free range
-            std::lock_guard<std::mutex> lk(g_cache_mu);
-            if (void* q = take_range(dev, rb, block, false, s)) {
-                *p = q;
-                return Status::ok();
-            }
         }
         char buf[256];
         snprintf(buf, sizeof buf, "cudaMalloc(%zu bytes) for %s: %s", bytes, what, cudaGetErrorString(e));
@@ -319,7 +286,7 @@ Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, int flag
     }
     if (big) {
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        g_ranges.emplace((char*)*p, Range{rb, dev, (char*)*p, rb, false, {}});
+        g_segs.emplace((char*)*p, Segment{rb, dev, false, {}});
     }
     return Status::ok();
 }
@@ -343,31 +310,16 @@ void dfree(void* p, cudaStream_t s) {
     int dev = -1;
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        auto it = g_ranges.find((char*)p);
-        if (it != g_ranges.end() && !it->second.free) {
-            Range& r = it->second;
+        auto it = g_segs.find((char*)p);
+        if (it != g_segs.end() && !it->second.free) {
+            Segment& r = it->second;
             dev = r.dev;
             if (cudaEvent_t e = ev_get()) {
-                cudaEventRecord(e, s);        // the range is free once s reaches this point
+                cudaEventRecord(e, s);        // the segment is free once s reaches this point
                 r.ready.push_back(e);
             }
             r.free = true;
             g_free_bytes += r.bytes;
-            // merge with free neighbours of the same segment (keeping every pending event)
-            auto nx = std::next(it);
-            if (nx != g_ranges.end() && nx->second.free && nx->second.seg == r.seg) {
-                r.bytes += nx->second.bytes;
-                for (auto e : nx->second.ready) r.ready.push_back(e);
-                g_ranges.erase(nx);
-            }
-            if (it != g_ranges.begin()) {
-                auto pv = std::prev(it);
-                if (pv->second.free && pv->second.seg == r.seg) {
-                    pv->second.bytes += r.bytes;
-                    for (auto e : r.ready) pv->second.ready.push_back(e);
-                    g_ranges.erase(it);
-                }
-            }
             cached = true;
         }
     }
@@ -375,10 +327,8 @@ void dfree(void* p, cudaStream_t s) {
         cudaFreeAsync(p, s);
         return;
     }
-    // bound what stays cached: whole free segments beyond the cap go back to the driver
-    if (g_free_bytes > cache_cap_bytes(dev)) {
-        while (g_free_bytes > cache_cap_bytes(dev) && release_largest(dev)) {
-        }
+    // bound what stays cached: segments beyond the cap go back to the driver, largest first
+    while (g_free_bytes > cache_cap_bytes(dev) && release_largest(dev)) {
     }
 }
 
@@ -1153,7 +1103,7 @@ int64_t cleora_kernel_launches(void) { return g_launches.load(); }
 
 int cleora_release_cached_memory(void) {
     ipc_close_all();
-    release_cached(-1, nullptr);
+    release_cached(-1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_release_cached_memory: ") + cudaGetErrorString(e)));
     return CLEORA_OK;

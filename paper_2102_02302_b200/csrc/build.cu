@@ -336,22 +336,6 @@ __global__ void k_fill_items(const int64_t* __restrict__ rp, const int64_t* __re
     }
 }
 
-// nnz-balanced cuts: cut p = first row r with row_ptr[r] * world >= p * nnz.
-__global__ void k_cuts(const int64_t* __restrict__ rp, int32_t N, int world, int64_t* __restrict__ cuts) {
-    int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p > world) return;
-    int64_t nnz = rp[N];
-    if (p == 0) { cuts[0] = 0; return; }
-    if (p == world) { cuts[world] = N; return; }
-    int64_t lo = 0, hi = N;   // search in [0, N]
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        // compare row_ptr[mid] * world >= p * nnz without overflow (both < 2^63 / 64 here)
-        if ((__int128)rp[mid] * world >= (__int128)p * nnz) hi = mid; else lo = mid + 1;
-    }
-    cuts[p] = lo;
-}
-
 // ---- row-sharded builds (world > 1): every rank reads the whole COO, counts the
 // entries of every row (after mirroring, before merging), cuts the rows into nnz-balanced shards,
 // and keeps only the entries of its own rows -- M is never materialised whole on any rank.
@@ -1065,16 +1049,6 @@ Status peer_masks(const uint8_t* d_need_all, int32_t N, int world, int rank, cud
     k_peer_masks<<<grid_for(N, 4), kThreads, 0, s>>>(d_need_all, N, world, rank, d_mask);
     CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
-    return Status::ok();
-}
-
-Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts) {
-    DevBuf<int64_t> cuts;
-    CL_TRY(cuts.alloc(world + 1, s, "shard cuts"));
-    k_cuts<<<(world + 128) / 128, 128, 0, s>>>(d_row_ptr, N, world, cuts.p);
-    CL_CUDA_TRY(cudaGetLastError());
-    count_launches(1);
-    CL_TRY(read_small(h_cuts, cuts.p, (world + 1) * sizeof(int64_t), s));
     return Status::ok();
 }
 

@@ -55,7 +55,8 @@ void count_launches(int64_t n);
 // Stream-ordered allocation from the device's default pool (release threshold raised so
 // repeated build/destroy cycles do not return memory to the driver).
 // flags: kAllocBase -- at the base of a cudaMalloc segment (CUDA IPC exports whole allocations);
-// kAllocTransient -- freed before the API call returns (a hint: the cache serves both alike, api.cu)
+// kAllocTransient -- freed before the API call returns (a hint: the cache serves both alike, api.cu;
+// small builds carve such buffers out of one arena, build.cu)
 enum { kAllocBase = 1, kAllocTransient = 2 };
 Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, int flags = 0);
 void dfree(void* p, cudaStream_t s);
@@ -191,7 +192,6 @@ struct Schedule {
 // nnz: entries of rows [r0, r1), max_degree: their longest row (upper bounds are enough)
 Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r1, int64_t nnz, int64_t max_degree,
                       int heavy_thresh, int chunk_rows, cudaStream_t s, Schedule* out);
-Status shard_cuts(const int64_t* d_row_ptr, int32_t N, int world, cudaStream_t s, int64_t* h_cuts);
 // Row-sharded builds (world > 1): validate every edge, count every row's entries (mirrored, before
 // merging), cut the rows into `world` shards balanced on those counts (cut p = first row whose entry
 // prefix reaches p * total / world; h_cuts[world + 1]), h_ent[p] = entries before cut p, and the
