@@ -11,7 +11,9 @@
 //   B4 val    = fp32_rn(e_ab / deg(a))                -> IEEE double divide, one rounding
 // This translation unit must not be compiled with --use_fast_math.
 #include <algorithm>
+#include <mutex>
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -506,6 +508,367 @@ struct ArenaGuard {
     }
 };
 
+// ---- one-kernel build of small graphs (DESIGN §7 "Build kernels").  On a graph of 10^5 entries
+// the general build is ~20 dependent launches of a few microseconds each (c1: 0.136 ms of a 0.25 ms
+// step).  This path does the same B1-B4 in ONE cooperative kernel with five grid-wide barriers:
+//   P0 validate, count every row's entries (after mirroring, before merging)
+//   P1 exclusive scan of the counts -> bucket starts and cursors (two phases around a barrier)
+//   P2 scatter every entry into its row's bucket as (dst << 32 | list position) + weight
+//   P3 a warp per row: sort the bucket by that key (rank sort in shared memory; rows <= kSmallCap)
+//      = the stable (src, dst) order of B1; merge runs of equal dst summing their weights in list
+//      order in fp64 (B2); count the merged entries
+//   P4 scan the merged counts -> row_ptr; per row: deg = the sequential fp64 fold over ascending
+//      dst (B3), val = fp32_rn(e_ab / deg) (B4), written at row_ptr
+// Same bits as the general path (tested: test_small_build_bitwise).  A row longer than kSmallCap
+// entries makes the kernel stop after P1 and report it; the caller then runs the general path.
+constexpr int kSmallCap = 256;
+constexpr int kSmallThreads = 256;
+constexpr int kSmallWarps = kSmallThreads / 32;
+
+struct SmallArgs {
+    const int32_t* src;
+    const int32_t* dst;
+    const float* w;
+    int64_t E;
+    int32_t N;
+    int directed;
+    int32_t* start;      // [N + 1] entry counts, then bucket starts (zeroed by the caller)
+    int32_t* flags;      // [4] (zeroed): [0] error kind, [1] longest row (entries), [2] 1 = too long
+    int32_t* cur;        // [N] bucket cursors
+    int32_t* ucnt;       // [N] merged entries per row
+    int64_t* bsum;       // [2 * gridDim.x] block totals: entries, merged entries
+    uint64_t* bkey;      // [n_all] bucketed entries: dst << 32 | position in the mirrored list
+    float* bw;           // [n_all] their weights (weighted graphs)
+    int32_t* mcol;       // [n_all] merged entries at bucket positions: column, e_ab
+    double* me;
+    int64_t* row_ptr;    // outputs (the CSR of build_csr)
+    int32_t* col;
+    float* val;
+    double* deg;
+    unsigned long long* scal;   // (zeroed) [0] first bad edge [2] zero rows [3] longest row [4] nnz
+};
+
+union SmallScanTmp {
+    typename cub::BlockScan<int64_t, kSmallThreads>::TempStorage scan;
+    typename cub::BlockReduce<int64_t, kSmallThreads>::TempStorage red;
+};
+
+__device__ __forceinline__ bool small_edge(const SmallArgs& a, int64_t i, int32_t& u, int32_t& v) {
+    u = a.src[i];
+    v = a.dst[i];
+    bool bad_w = false;
+    if (a.w) {
+        const float x = a.w[i];
+        bad_w = !(isfinite(x) && x > 0.0f);
+    }
+    const bool bad_id = u < 0 || u >= a.N || v < 0 || v >= a.N;
+    return !(bad_id || bad_w);
+}
+
+// sum of bsum[q * G + 0 .. q * G + b), b = this block (all threads get it)
+__device__ int64_t small_block_offset(const int64_t* bsum, SmallScanTmp& tmp, int64_t* bcast) {
+    int64_t x = 0;
+    for (int q = threadIdx.x; q < (int)blockIdx.x; q += blockDim.x) x += bsum[q];
+    x = cub::BlockReduce<int64_t, kSmallThreads>(tmp.red).Sum(x);
+    if (threadIdx.x == 0) *bcast = x;
+    __syncthreads();
+    x = *bcast;
+    __syncthreads();
+    return x;
+}
+
+// rows [r0, r1) of this block, a contiguous sub-range per thread: out[r] = offset + exclusive prefix
+// of in[] (and out2[r], if given); returns the block's total
+template <class T>
+__device__ int64_t small_block_scan(const int32_t* in, int64_t r0, int64_t r1, int64_t offset, T* out, int32_t* out2,
+                                    SmallScanTmp& tmp) {
+    const int64_t n = r1 - r0, per = (n + blockDim.x - 1) / blockDim.x;
+    const int64_t a0 = r0 + min(n, per * threadIdx.x), a1 = r0 + min(n, per * (threadIdx.x + 1));
+    int64_t x = 0;
+    for (int64_t r = a0; r < a1; r++) x += in[r];
+    int64_t ex = 0, tot = 0;
+    cub::BlockScan<int64_t, kSmallThreads>(tmp.scan).ExclusiveSum(x, ex, tot);
+    __syncthreads();
+    int64_t run = offset + ex;
+    for (int64_t r = a0; r < a1; r++) {
+        const int32_t c = in[r];
+        out[r] = (T)run;
+        if (out2) out2[r] = (int32_t)run;
+        run += c;
+    }
+    return tot;
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_build_small(const SmallArgs a) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    extern __shared__ unsigned char small_smem[];
+    __shared__ SmallScanTmp tmp;
+    __shared__ int64_t bcast;
+    __shared__ int64_t s_tot[kSmallWarps];
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t N = a.N;
+    const int64_t G = gridDim.x;
+    // this block's rows in P1, P3, P4
+    const int64_t R = (N + G - 1) / G;
+    const int64_t r0 = min((int64_t)N, (int64_t)blockIdx.x * R), r1 = min((int64_t)N, r0 + R);
+
+    // P0: validate and count
+    for (int64_t i = tid; i < a.E; i += nth) {
+        int32_t u, v;
+        if (!small_edge(a, i, u, v)) {
+            atomicMax(a.scal + 0, ~(unsigned long long)i);     // the first bad edge is the largest ~i
+            atomicOr(a.flags + 0, (u < 0 || u >= N || v < 0 || v >= N) ? 1 : 2);
+            continue;
+        }
+        atomicAdd(a.start + u, 1);
+        if (!a.directed && u != v) atomicAdd(a.start + v, 1);   // the mirror of a self-loop is dropped (R5)
+    }
+    grid.sync();
+
+    // P1a: block totals and the longest row
+    {
+        int64_t x = 0;
+        int32_t mx = 0;
+        for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+            const int32_t c = a.start[r];
+            x += c;
+            mx = max(mx, c);
+        }
+        x = cub::BlockReduce<int64_t, kSmallThreads>(tmp.red).Sum(x);
+        if (threadIdx.x == 0) a.bsum[blockIdx.x] = x;
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0 && mx > 0) atomicMax(a.flags + 1, mx);
+    }
+    grid.sync();
+    if (*(volatile int32_t*)(a.flags + 1) > kSmallCap) {      // the general path builds this graph
+        if (tid == 0) a.flags[2] = 1;
+        return;
+    }
+    // P1b: bucket starts and cursors (start[N] = all entries)
+    {
+        const int64_t off = small_block_offset(a.bsum, tmp, &bcast);
+        const int64_t tot = small_block_scan<int32_t>(a.start, r0, r1, off, a.start, a.cur, tmp);
+        if (r1 == N && r1 > r0 && threadIdx.x == 0) a.start[N] = (int32_t)(off + tot);
+        if (N == 0 && tid == 0) a.start[0] = 0;
+    }
+    grid.sync();
+
+    // P2: scatter (position in the mirrored list: i for an edge as given, E + i for its mirror)
+    for (int64_t i = tid; i < a.E; i += nth) {
+        int32_t u, v;
+        if (!small_edge(a, i, u, v)) continue;
+        const float x = a.w ? a.w[i] : 1.0f;
+        int32_t q = atomicAdd(a.cur + u, 1);
+        a.bkey[q] = ((uint64_t)(uint32_t)v << 32) | (uint64_t)i;
+        if (a.w) a.bw[q] = x;
+        if (!a.directed && u != v) {
+            q = atomicAdd(a.cur + v, 1);
+            a.bkey[q] = ((uint64_t)(uint32_t)u << 32) | (uint64_t)(a.E + i);
+            if (a.w) a.bw[q] = x;
+        }
+    }
+    grid.sync();
+
+    // P3: a warp per row of this block: sort, merge runs, count
+    {
+        uint64_t* kin = reinterpret_cast<uint64_t*>(small_smem) + (size_t)warp * 2 * kSmallCap;
+        uint64_t* kout = kin + kSmallCap;
+        float* win = reinterpret_cast<float*>(reinterpret_cast<uint64_t*>(small_smem) + (size_t)kSmallWarps * 2 * kSmallCap) +
+                     (size_t)warp * 2 * kSmallCap;
+        float* wout = win + kSmallCap;
+        int64_t wtot = 0;
+        for (int64_t r = r0 + warp; r < r1; r += kSmallWarps) {
+            const int32_t b = a.start[r], n = a.start[r + 1] - b;
+            for (int j = lane; j < n; j += 32) {
+                kin[j] = a.bkey[b + j];
+                if (a.w) win[j] = a.bw[b + j];
+            }
+            __syncwarp();
+            for (int j = lane; j < n; j += 32) {       // keys are distinct (positions): rank = slot
+                const uint64_t k = kin[j];
+                int rk = 0;
+                for (int t = 0; t < n; t++) rk += kin[t] < k;
+                kout[rk] = k;
+                if (a.w) wout[rk] = win[j];
+            }
+            __syncwarp();
+            int32_t u = 0;                             // merged entries so far
+            for (int c = 0; c < n; c += 32) {
+                const int j = c + lane;
+                const uint32_t cj = j < n ? (uint32_t)(kout[j] >> 32) : 0u;
+                const bool head = j < n && (j == 0 || (uint32_t)(kout[j - 1] >> 32) != cj);
+                const unsigned m = __ballot_sync(0xffffffffu, head);
+                if (head) {
+                    double acc = 0.0;                  // B2: list order within the run
+                    for (int t = j; t < n && (uint32_t)(kout[t] >> 32) == cj; t++)
+                        acc = acc + (a.w ? (double)wout[t] : 1.0);
+                    const int32_t ui = u + __popc(m & ((1u << lane) - 1u));
+                    a.mcol[b + ui] = (int32_t)cj;
+                    a.me[b + ui] = acc;
+                }
+                u += __popc(m);
+            }
+            if (lane == 0) a.ucnt[r] = u;
+            wtot += u;
+            __syncwarp();
+        }
+        if (lane == 0) s_tot[warp] = wtot;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t x = 0;
+            for (int q = 0; q < kSmallWarps; q++) x += s_tot[q];
+            a.bsum[G + blockIdx.x] = x;
+        }
+    }
+    grid.sync();
+
+    // P4: row_ptr, then degree and values of this block's rows
+    {
+        const int64_t off = small_block_offset(a.bsum + G, tmp, &bcast);
+        const int64_t tot = small_block_scan<int64_t>(a.ucnt, r0, r1, off, a.row_ptr, nullptr, tmp);
+        if (r1 == N && r1 > r0 && threadIdx.x == 0) {
+            a.row_ptr[N] = off + tot;
+            a.scal[4] = (unsigned long long)(off + tot);
+        }
+        if (N == 0 && tid == 0) a.row_ptr[0] = 0;
+        if (tid == 0)                                  // the verdict: first bad edge, as build_csr's scal[0]
+            a.scal[0] = *(volatile int32_t*)(a.flags + 0) ? ~*(volatile unsigned long long*)(a.scal + 0) : ~0ull;
+        __syncthreads();                               // this block's row_ptr
+        unsigned long long zeros = 0, mx = 0;
+        for (int64_t r = r0 + warp; r < r1; r += kSmallWarps) {
+            const int32_t b = a.start[r], u = a.ucnt[r];
+            const int64_t rp = a.row_ptr[r];
+            double s = 0.0;                            // B3: sequential over ascending dst
+            for (int c = 0; c < u; c += 32) {
+                const int n = min(32, u - c);
+                const double x = lane < n ? a.me[b + c + lane] : 0.0;
+                for (int t = 0; t < n; t++) s = s + __shfl_sync(0xffffffffu, x, t);
+            }
+            for (int j = lane; j < u; j += 32) {
+                a.col[rp + j] = a.mcol[b + j];
+                a.val[rp + j] = __double2float_rn(a.me[b + j] / s);   // B4
+            }
+            if (lane == 0) {
+                a.deg[r] = s;
+                if (u == 0) zeros++;
+                else mx = max(mx, (unsigned long long)u);
+            }
+        }
+        if (lane == 0) {
+            if (zeros) atomicAdd(a.scal + 2, zeros);
+            if (mx) atomicMax(a.scal + 3, mx);
+        }
+    }
+}
+
+// The one-kernel build (above) of a graph of <= kSmallMaxEntries mirrored entries.  *done = false:
+// a row is longer than kSmallCap, nothing was built (the general path follows).
+constexpr int64_t kSmallMaxEntries = (int64_t)1 << 21;
+constexpr int32_t kSmallMaxRows = 1 << 21;
+
+Status build_small(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N, int directed,
+                   cudaStream_t s, BuildOut* out, bool* done) {
+    *done = false;
+    const int64_t n_all = directed ? E : 2 * E;
+    constexpr size_t smem = (size_t)kSmallWarps * 2 * kSmallCap * (sizeof(uint64_t) + sizeof(float));
+    static int occ[kMaxDevices], nsm[kMaxDevices];
+    static std::mutex mu;
+    int dev = 0;
+    CL_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev >= kMaxDevices) return Status::make(4, "build: device ordinal beyond kMaxDevices");
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!occ[dev]) {
+            CL_CUDA_TRY(cudaFuncSetAttribute(k_build_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CL_CUDA_TRY(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
+            int b = 0;
+            CL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_build_small, kSmallThreads, smem));
+            occ[dev] = b < 1 ? -1 : b;
+        }
+    }
+    if (occ[dev] < 1) return Status::ok();             // cannot be co-resident: general path
+    // every block resident (cooperative launch); no more blocks than a thread per edge or row needs
+    const int64_t want = (std::max<int64_t>(E, N) + kSmallThreads - 1) / kSmallThreads;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm[dev] * occ[dev], want));
+
+    ArenaGuard arena((size_t)n_all * 32 + (size_t)N * 16 + ((size_t)1 << 20), s);
+    DevBuf<int32_t> zeroed, cur, ucnt, mcol;
+    DevBuf<int64_t> bsum;
+    DevBuf<uint64_t> bkey;
+    DevBuf<float> bw;
+    DevBuf<double> me;
+    DevBuf<unsigned long long> scal;
+    DevBuf<int64_t> row_ptr;
+    DevBuf<int32_t> col;
+    DevBuf<float> val;
+    DevBuf<double> deg;
+    CL_TRY(zeroed.alloc((size_t)N + 1 + 4, s, "small build counts"));
+    CL_TRY(cur.alloc(N, s, "small build cursors"));
+    CL_TRY(ucnt.alloc(N, s, "small build merged counts"));
+    CL_TRY(bsum.alloc(2 * (size_t)grid, s, "small build block sums"));
+    CL_TRY(bkey.alloc(n_all, s, "small build buckets"));
+    if (d_w) CL_TRY(bw.alloc(n_all, s, "small build bucket weights"));
+    CL_TRY(mcol.alloc(n_all, s, "small build merged cols"));
+    CL_TRY(me.alloc(n_all, s, "small build e_ab"));
+    CL_TRY(scal.alloc(8, s, "scalars", true));
+    CL_TRY(row_ptr.alloc((size_t)N + 1, s, "CSR row_ptr", true));
+    CL_TRY(col.alloc(n_all, s, "CSR col", true));
+    CL_TRY(val.alloc(n_all, s, "CSR val", true));
+    CL_TRY(deg.alloc(N, s, "degree", true));
+    CL_CUDA_TRY(cudaMemsetAsync(zeroed.p, 0, ((size_t)N + 1 + 4) * sizeof(int32_t), s));
+    CL_CUDA_TRY(cudaMemsetAsync(scal.p, 0, 8 * sizeof(unsigned long long), s));
+    SmallArgs a;
+    a.src = d_src;
+    a.dst = d_dst;
+    a.w = d_w;
+    a.E = E;
+    a.N = N;
+    a.directed = directed;
+    a.start = zeroed.p;
+    a.flags = zeroed.p + N + 1;
+    a.cur = cur.p;
+    a.ucnt = ucnt.p;
+    a.bsum = bsum.p;
+    a.bkey = bkey.p;
+    a.bw = bw.p;
+    a.mcol = mcol.p;
+    a.me = me.p;
+    a.row_ptr = row_ptr.p;
+    a.col = col.p;
+    a.val = val.p;
+    a.deg = deg.p;
+    a.scal = scal.p;
+    void* args[] = {&a};
+    CL_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_build_small, dim3(grid), dim3(kSmallThreads), args, smem, s));
+    count_launches(1);
+    unsigned long long h_scal[5] = {0, 0, 0, 0, 0};
+    int32_t h_flags[4] = {0, 0, 0, 0};
+    {
+        const SmallRead rd[2] = {{h_scal, scal.p, 5 * sizeof(unsigned long long)}, {h_flags, a.flags, 4 * sizeof(int32_t)}};
+        CL_TRY(read_small_n(rd, 2, s));
+    }
+    trace("csr: one-kernel build", s, false);
+    if (h_flags[0]) {
+        char buf[256];
+        snprintf(buf, sizeof buf, "cleora_build: edge %llu: %s", (unsigned long long)h_scal[0],
+                 (h_flags[0] & 1) ? "node id outside [0, n_nodes)" : "weight not finite or <= 0");
+        return Status::make(3, buf);
+    }
+    if (h_flags[2]) return Status::ok();               // a row longer than kSmallCap: general path
+    out->nnz = (int64_t)h_scal[4];
+    out->zero_rows = (int64_t)h_scal[2];
+    out->max_degree = (int64_t)h_scal[3];
+    out->d_scal = scal.release();
+    out->row_ptr = row_ptr.release();
+    out->col = col.release();
+    out->val = val.release();
+    out->deg = deg.release();
+    *done = true;
+    return Status::ok();
+}
+
 }  // namespace
 
 Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N,
@@ -518,6 +881,15 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     const bool shard = x.row_hi >= 0;
     const int32_t lo = shard ? x.row_lo : 0, hi = shard ? x.row_hi : N;
     const int64_t n_all = directed ? E : 2 * E;         // entries of the mirrored list
+    // small whole graphs: one kernel (CLEORA_SMALL_BUILD=0: always the general path, for A/B and tests)
+    if (!shard && x.n_chunks <= 1 && !x.occ && x.dst_limit < 0 && n_all <= kSmallMaxEntries && N <= kSmallMaxRows) {
+        const char* e = getenv("CLEORA_SMALL_BUILD");
+        if (!e || atoi(e) != 0) {
+            bool done = false;
+            CL_TRY(build_small(d_src, d_dst, d_w, E, N, directed, s, out, &done));
+            if (done) return Status::ok();
+        }
+    }
     const int64_t n_ent = shard ? x.shard_entries : n_all;
     if (n_all >= (int64_t)UINT32_MAX) return Status::make(2, "cleora_build: too many edges (entry positions are 32-bit)");
     const uint64_t NN = (uint64_t)(hi - lo) * (uint64_t)N;
