@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_build_small(const SmallArgs a
 // The one-kernel build (above) of a graph of <= kSmallMaxEntries mirrored entries.  *done = false:
 // a row is longer than kSmallCap, nothing was built (the general path follows).
 constexpr int64_t kSmallMaxEntries = (int64_t)1 << 21;
-constexpr int32_t kSmallMaxRows = 1 << 21;
+constexpr int32_t kSmallMaxRows = 1 << 24;
 
 Status build_small(const int32_t* d_src, const int32_t* d_dst, const float* d_w, int64_t E, int32_t N, int directed,
                    cudaStream_t s, BuildOut* out, bool* done) {
@@ -790,7 +790,8 @@ Status build_small(const int32_t* d_src, const int32_t* d_dst, const float* d_w,
     }
     if (occ[dev] < 1) return Status::ok();             // cannot be co-resident: general path
     // every block resident (cooperative launch); no more blocks than a thread per edge or row needs
-    const int64_t want = (std::max<int64_t>(E, N) + kSmallThreads - 1) / kSmallThreads;
+    // (P3/P4 walk a warp's rows one after another: ~2 rows per warp keeps that chain short)
+    const int64_t want = std::max<int64_t>((E + kSmallThreads - 1) / kSmallThreads, ((int64_t)N + 2 * kSmallWarps - 1) / (2 * kSmallWarps));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm[dev] * occ[dev], want));
 
     ArenaGuard arena((size_t)n_all * 32 + (size_t)N * 16 + ((size_t)1 << 20), s);
@@ -882,7 +883,9 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
     const int32_t lo = shard ? x.row_lo : 0, hi = shard ? x.row_hi : N;
     const int64_t n_all = directed ? E : 2 * E;         // entries of the mirrored list
     // small whole graphs: one kernel (CLEORA_SMALL_BUILD=0: always the general path, for A/B and tests)
-    if (!shard && x.n_chunks <= 1 && !x.occ && x.dst_limit < 0 && n_all <= kSmallMaxEntries && N <= kSmallMaxRows) {
+    const char* sme = getenv("CLEORA_SMALL_MAX_ENTRIES");            // A/B of the size limit
+    const int64_t small_max = sme ? atoll(sme) : kSmallMaxEntries;
+    if (!shard && x.n_chunks <= 1 && !x.occ && x.dst_limit < 0 && n_all <= small_max && N <= kSmallMaxRows) {
         const char* e = getenv("CLEORA_SMALL_BUILD");
         if (!e || atoi(e) != 0) {
             bool done = false;

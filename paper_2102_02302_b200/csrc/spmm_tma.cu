@@ -469,11 +469,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
     float4 acc[V];
 #pragma unroll
     for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // few chunks: static round robin, no ticket (as k_spmm_norm)
+    const int64_t nw = (int64_t)gridDim.x * kWarpsPerCta;
+    const bool stat = nchunks <= 4 * nw;
+    int64_t sc = (int64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
     for (;;) {
         unsigned c = 0;
-        if (lane == 0) c = atomicAdd(a.work + 1, 1u);
-        c = __shfl_sync(kFull, c, 0);
-        if ((int64_t)c >= nchunks) break;
+        if (stat) {
+            if (sc >= nchunks) break;
+            c = (unsigned)sc;
+            sc += nw;
+        } else {
+            if (lane == 0) c = atomicAdd(a.work + 1, 1u);
+            c = __shfl_sync(kFull, c, 0);
+            if ((int64_t)c >= nchunks) break;
+        }
         const int64_t rb = a.light_start[c];
         const int64_t re = a.light_start[c + 1];
         const int64_t rpl = (lane <= re - rb) ? a.row_ptr[rb + lane] : 0;
@@ -501,6 +511,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) k_spmm_tma(const SpmmArg
     // peer stores (multi-GPU) are system-scope visible before this launch counts as done; the
     // rank barrier that follows on the stream then publishes them to the other ranks
     if (a.n_peers > 0) __threadfence_system();
+    if (stat && n_items == 0) return;             // no ticket was taken: nothing to reset
     if (lane == 0) {
         __threadfence();
         const unsigned done = atomicAdd(a.work + 2, 1u);
