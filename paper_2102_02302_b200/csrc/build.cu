@@ -293,6 +293,13 @@ __global__ void k_put_end(int64_t* __restrict__ starts, const int64_t* __restric
     starts[*n] = end;
 }
 
+// chunks of one row each: starts[i] = r0 + i for i <= nr, and their count
+__global__ void k_iota_starts(int64_t* __restrict__ starts, int64_t r0, int64_t nr, int64_t* __restrict__ n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nr; i += stride) starts[i] = r0 + i;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n = nr;
+}
+
 // h < *nh (heavy rows found): items of the row, and its partial-vector slots (multi-part rows only);
 // h in [*nh, nh_max]: 0, so the scans' last entries are the totals
 __global__ void k_items_per_row(const int64_t* __restrict__ rp, const int64_t* __restrict__ hrows,
@@ -642,7 +649,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_build_small(const SmallArgs a
         if (lane == 0 && mx > 0) atomicMax(a.flags + 1, mx);
     }
     grid.sync();
-    if (*(volatile int32_t*)(a.flags + 1) > kSmallCap) {      // the general path builds this graph
+    if (__ldcg(a.flags + 1) > kSmallCap) {                    // the general path builds this graph
         if (tid == 0) a.flags[2] = 1;
         return;
     }
@@ -734,7 +741,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_build_small(const SmallArgs a
         }
         if (N == 0 && tid == 0) a.row_ptr[0] = 0;
         if (tid == 0)                                  // the verdict: first bad edge, as build_csr's scal[0]
-            a.scal[0] = *(volatile int32_t*)(a.flags + 0) ? ~*(volatile unsigned long long*)(a.scal + 0) : ~0ull;
+            a.scal[0] = __ldcg(a.flags + 0) ? ~__ldcg(a.scal + 0) : ~0ull;
         __syncthreads();                               // this block's row_ptr
         unsigned long long zeros = 0, mx = 0;
         for (int64_t r = r0 + warp; r < r1; r += kSmallWarps) {
@@ -1100,15 +1107,22 @@ Status build_schedule(const int64_t* d_row_ptr, int32_t N, int64_t r0, int64_t r
         int64_t rows = nr / ((int64_t)sms * 16 * 4);
         if (rows < 1) rows = 1;
         if (rows > cap) rows = cap;
-        IsChunkStart pred{d_row_ptr, r0, win, rows};
-        size_t tmp_bytes = 0;
-        CL_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, it, starts.p, out->counts + 0, nr, pred, s));
-        DevBuf<uint8_t> tmp;
-        CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
-        CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, starts.p, out->counts + 0, nr, pred, s));
-        k_put_end<<<1, 1, 0, s>>>(starts.p, out->counts + 0, r1);       // starts[n_light] = r1
-        CL_CUDA_TRY(cudaGetLastError());
-        count_launches(3);
+        if (rows == 1) {
+            // one row per chunk (small graphs): every row starts a chunk -- one kernel, no selection
+            k_iota_starts<<<grid_for(nr + 1, 4), kThreads, 0, s>>>(starts.p, r0, nr, out->counts + 0);
+            CL_CUDA_TRY(cudaGetLastError());
+            count_launches(1);
+        } else {
+            IsChunkStart pred{d_row_ptr, r0, win, rows};
+            size_t tmp_bytes = 0;
+            CL_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, it, starts.p, out->counts + 0, nr, pred, s));
+            DevBuf<uint8_t> tmp;
+            CL_TRY(tmp.alloc(tmp_bytes, s, "select temp"));
+            CL_CUDA_TRY(cub::DeviceSelect::If(tmp.p, tmp_bytes, it, starts.p, out->counts + 0, nr, pred, s));
+            k_put_end<<<1, 1, 0, s>>>(starts.p, out->counts + 0, r1);       // starts[n_light] = r1
+            CL_CUDA_TRY(cudaGetLastError());
+            count_launches(3);
+        }
         out->light_start = starts.release();
     }
     // heavy rows: at most nnz / (heavy_thresh + 1) of them
