@@ -188,15 +188,15 @@ __device__ double degree_long_row(const double* __restrict__ e_ab, int64_t k0, i
                 stage[lane] = cur[u];
                 __syncwarp();
                 if (lane == 0) {
-                    int j = 0;
-                    for (; j + 4 <= n; j += 4) {
-                        const double a0 = stage[j], a1 = stage[j + 1], a2 = stage[j + 2], a3 = stage[j + 3];
-                        s = s + a0;
-                        s = s + a1;
-                        s = s + a2;
-                        s = s + a3;
-                    }
-                    for (; j < n; j++) s = s + stage[j];
+                    // all 32 values into registers first, then the dependent chain of adds alone
+                    // (4 at a time, the shared-memory latency sat inside the chain: c4's 92k-entry hub
+                    // row folded at ~23 cycles per entry)
+                    double v[32];
+#pragma unroll
+                    for (int q = 0; q < 32; q++) v[q] = stage[q];
+#pragma unroll
+                    for (int q = 0; q < 32; q++)
+                        if (q < n) s = s + v[q];
                 }
                 __syncwarp();
             }
@@ -206,10 +206,16 @@ __device__ double degree_long_row(const double* __restrict__ e_ab, int64_t k0, i
     return s;
 }
 
+// Rows longer than this are folded by k_degree_long, one warp per row: the warp that owns a group of
+// 32 rows would otherwise fold its long rows one after another -- on R-MAT the hubs share low ids
+// (c4: one warp folded several hub rows of up to 92k weighted entries in sequence, 1.9 ms per build)
+constexpr int64_t kDegLong = 1024;
+
 // zero rows are counted inside [row_lo, row_hi) only (a shard's rows; the whole graph otherwise)
 __global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __restrict__ e_ab, int32_t N,
                          int32_t row_lo, int32_t row_hi, double* __restrict__ deg,
-                         unsigned long long* __restrict__ zero_rows, unsigned long long* __restrict__ max_deg) {
+                         unsigned long long* __restrict__ zero_rows, unsigned long long* __restrict__ max_deg,
+                         int32_t* __restrict__ long_rows, unsigned long long* __restrict__ n_long) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     __shared__ double stage[kThreads / 32][32];
@@ -228,10 +234,20 @@ __global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __re
         const bool lng = a < N && k1 - k0 > 32;
         if (a < N && !lng) {
             double s = 0.0;
-            for (int64_t k = k0; k < k1; k++) s = s + e_ab[k];
+            int64_t k = k0;
+            for (; k + 4 <= k1; k += 4) {            // 4 loads in flight, the same left-to-right sum
+                const double x0 = e_ab[k], x1 = e_ab[k + 1], x2 = e_ab[k + 2], x3 = e_ab[k + 3];
+                s = s + x0;
+                s = s + x1;
+                s = s + x2;
+                s = s + x3;
+            }
+            for (; k < k1; k++) s = s + e_ab[k];
             deg[a] = s;
         }
-        unsigned m = __ballot_sync(0xffffffffu, lng);
+        const bool defer = lng && k1 - k0 > kDegLong;
+        if (defer) long_rows[atomicAdd(n_long, 1ull)] = (int32_t)a;
+        unsigned m = __ballot_sync(0xffffffffu, lng && !defer);
         while (m) {
             const int l = __ffs(m) - 1;
             m &= m - 1;
@@ -259,6 +275,21 @@ __global__ void k_degree(const int64_t* __restrict__ row_ptr, const double* __re
         }
         if (z) atomicAdd(zero_rows, z);
         if (mx) atomicMax(max_deg, mx);
+    }
+}
+
+// the rows k_degree deferred, one warp each (any order: each row's fold is its own)
+__global__ void k_degree_long(const int64_t* __restrict__ row_ptr, const double* __restrict__ e_ab,
+                              const int32_t* __restrict__ long_rows, const unsigned long long* __restrict__ n_long,
+                              double* __restrict__ deg) {
+    const int lane = threadIdx.x & 31;
+    __shared__ double stage[kThreads / 32][32];
+    const int64_t n = (int64_t)*n_long;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+        const int32_t a = long_rows[i];
+        const double v = degree_long_row(e_ab, row_ptr[a], row_ptr[a + 1], lane, stage[threadIdx.x >> 5]);
+        if (lane == 0) deg[a] = v;
     }
 }
 
@@ -1029,9 +1060,20 @@ Status build_csr(const int32_t* d_src, const int32_t* d_dst, const float* d_w, i
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int blocks = std::min(grid_for(N, 1), sms * 16);   // 32 rows per warp step, grid-stride
-        k_degree<<<blocks, kThreads, 0, s>>>(row_ptr.p, e_ab.p, N, lo, hi, deg.p, scal.p + 2, scal.p + 3);
+        // rows of > kDegLong entries: at most n_ent / (kDegLong + 1) of them
+        const int64_t nl_max = std::max<int64_t>(1, n_ent / (kDegLong + 1));
+        DevBuf<int32_t> long_rows;
+        CL_TRY(long_rows.alloc(nl_max, s, "long rows"));
+        k_degree<<<blocks, kThreads, 0, s>>>(row_ptr.p, e_ab.p, N, lo, hi, deg.p, scal.p + 2, scal.p + 3, long_rows.p,
+                                             scal.p + 6);
+        CL_CUDA_TRY(cudaGetLastError());
+        if (n_ent > kDegLong) {
+            const int lb = (int)std::min<int64_t>(sms * 8, (nl_max + kThreads / 32 - 1) / (kThreads / 32));
+            k_degree_long<<<lb, kThreads, 0, s>>>(row_ptr.p, e_ab.p, long_rows.p, scal.p + 6, deg.p);
+            CL_CUDA_TRY(cudaGetLastError());
+            count_launches(1);
+        }
     }
-    CL_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     trace("csr: degree", s, true);
     CL_TRY(val.alloc(n_ent, s, "CSR val", true));

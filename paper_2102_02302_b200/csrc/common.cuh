@@ -119,6 +119,13 @@ struct SpmmArgs {
     // unnormalised into T_out and nowhere else; 2 = columns [512, 1024), then the whole row is finished
     // from T_out's first half -- bitwise the whole-row result (see spmm_tma.cu)
     int32_t pass;
+    // Lazy normalisation between the half-row steps of one iterate call (world 1; spmm_tma.cu):
+    // scale_out non-NULL (pass 2): y is written unnormalised and scale_out[row] = 1 / ||y||; ss_half
+    // non-NULL: pass 1 stores each light row's fp64 sum of squares over the first half, pass 2 adds it
+    // instead of reading the half back.  The next step gathers those rows with weights that carry the
+    // scales (launch_lazy_vals), so its kernels need nothing else.
+    float* scale_out;
+    double* ss_half;
 };
 
 // Store float4 f of row `row` of the iteration's output into T_out and every peer replica.  `empty`:
@@ -245,5 +252,10 @@ int gather_mode(int dp);          // which gather engine serves rows of dp float
 Status probe_gather(int row_bytes, int64_t table_bytes, int64_t n_gathers, cudaStream_t s, double* gbs);
 bool tma_path_supported(int dp);  // gather_mode(dp) uses the shared-memory ring kernel
 Status launch_spmm_tma(const SpmmArgs& a, cudaStream_t s);
+// Lazy normalisation (reading R21): val_out[e] = fp32_rn(val[e] * scale[col[e]]) for the step that
+// gathers unnormalised rows -- the scales are folded into the weights before the SpMM, so its gather
+// stream carries no scale lookups (spmm_tma.cu)
+Status launch_lazy_vals(const float* val, const int32_t* col, const float* scale, int64_t nnz, float* val_out,
+                        cudaStream_t s);
 
 }  // namespace cleora

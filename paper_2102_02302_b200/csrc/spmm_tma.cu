@@ -19,6 +19,7 @@
 // the last CTA (atomic ticket) with an fp64 sum in part order.  Each row accumulates its entries
 // in ascending order from 0, exactly as spmm_norm.cu does, so every engine produces bitwise
 // identical results (tested).
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -180,9 +181,34 @@ __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, f
             float4* out = reinterpret_cast<float4*>(a.T_out + row * (int64_t)a.dp);
 #pragma unroll
             for (int v = 0; v < V; v++) __stcg(out + lane + 32 * v, acc[v]);
+            if (a.ss_half) {                         // lazy step: this half's sum of squares for pass 2
+                double ss = 0.0;
+#pragma unroll
+                for (int v = 0; v < V; v++) ss += sq4(acc[v]);
+                ss = warp_sum(ss);
+                if (lane == 0) a.ss_half[row] = ss;
+            }
         }
 #pragma unroll
         for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    if (HALF && a.pass == 2 && a.scale_out) {
+        // lazy step: both halves stay unnormalised in T_out (the first from pass 1), the row scale goes
+        // to scale_out -- no read-back and rewrite of the first half (c4: 2 x 4.7 GB per step)
+        double ss = 0.0;
+#pragma unroll
+        for (int v = 0; v < V; v++) ss += sq4(acc[v]);
+        ss = warp_sum(ss);
+        if (!empty) ss += __ldcg(a.ss_half + row);
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            if (empty) put_out4(a, row, lane + 32 * v, z, true);
+            put_out4(a, row, 32 * V + lane + 32 * v, acc[v], empty);
+            acc[v] = z;
+        }
+        if (lane == 0) a.scale_out[row] = (float)inv_norm(ss);
         return;
     }
     if (HALF && a.pass == 2) {
@@ -343,7 +369,12 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
                 if (!mine) y = __ldcg(outr + t);
                 const double tot = block_sum(sq4(y), scratch);
                 const double inv = inv_norm(tot);
-                put_out4(a, it.row, t, scale4(y, inv));
+                if (a.scale_out) {                    // lazy step: unnormalised, the scale aside
+                    if (mine) put_out4(a, it.row, t, y);
+                    if (t == 0) a.scale_out[it.row] = (float)inv;
+                } else {
+                    put_out4(a, it.row, t, scale4(y, inv));
+                }
             }
         } else {
             float4* part = reinterpret_cast<float4*>(a.partials + (int64_t)it.slot * a.dp);
@@ -369,9 +400,13 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
                     }
                     const double tot = block_sum(zx * zx + zy * zy + zz * zz + zw * zw, scratch);
                     const double inv = inv_norm(tot);
-                    if (t < nqf)
+                    if (a.scale_out) {                // lazy step: unnormalised, the scale aside
+                        if (t < nqf) put_out4(a, it.row, t, make_float4((float)zx, (float)zy, (float)zz, (float)zw));
+                        if (t == 0) a.scale_out[it.row] = (float)inv;
+                    } else if (t < nqf) {
                         put_out4(a, it.row, t,
                                  make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));
+                    }
                     if (t == 0) a.counters[it.slot - it.part] = 0u;
                 }
             }
@@ -577,7 +612,30 @@ Status launch_mode(const SpmmArgs& a, cudaStream_t s, int mode) {
     return launch_tma_v<V, FULL, 0, HALF>(a, s);
 }
 
+// val_out[e] = fp32_rn(val[e] * scale[col[e]]): one rounding of the exact product (a float times a
+// float is exact in fp64) -- the weight of an entry whose column row is stored unnormalised
+__global__ void k_lazy_vals(const float* __restrict__ val, const int32_t* __restrict__ col,
+                            const float* __restrict__ scale, int64_t nnz, float* __restrict__ val_out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += stride)
+        val_out[e] = (float)((double)val[e] * (double)__ldg(scale + (col[e] & 0x7fffffff)));
+}
+
 }  // namespace
+
+Status launch_lazy_vals(const float* val, const int32_t* col, const float* scale, int64_t nnz, float* val_out,
+                        cudaStream_t s) {
+    if (nnz <= 0) return Status::ok();
+    int dev = 0, sms = 148;
+    CL_CUDA_TRY(cudaGetDevice(&dev));
+    CL_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t want = (nnz + 255) / 256;
+    const int grid = (int)std::min<int64_t>(want, (int64_t)sms * 16);
+    k_lazy_vals<<<grid, 256, 0, s>>>(val, col, scale, nnz, val_out);
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    return Status::ok();
+}
 
 // Gather engine by row size (measured on B200, ms per SpMM launch):
 //  - 4 KB rows (dp = 1024): TMA bulk copies, one per neighbour row issued by one lane (c2 2.54 min,

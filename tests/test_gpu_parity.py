@@ -69,7 +69,9 @@ def ill_conditioned(M, T_prev):
     return bool(live.any() and nr[live].min() < 1e-4)
 
 
-def run_case(cl, g, d, iters, seed=0, per_iter=True):
+def run_case(cl, g, d, iters, seed=0, per_iter=True, one_call=False):
+    """one_call: the GPU runs cleora_iterate(iters) once -- the launch sequence bench.py times (with
+    half-row passes every step but the last is lazy, reading R21) -- against the oracle's T_iters."""
     M = oracle.build_from(g)
     G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0)
     try:
@@ -80,6 +82,11 @@ def run_case(cl, g, d, iters, seed=0, per_iter=True):
         assert np.array_equal(T.view(np.uint32), R.view(np.uint32)), "T_0 not bit-exact"
         worst = (0.0, 1.0)
         del T
+        if one_call:
+            cl.cleora_iterate(G, iters)
+            for i in range(iters):
+                R = oracle.step(M, R)
+            return compare(cl.cleora_fetch(G), R, f"{g.name} d={d} iterate({iters})")
         for i in range(1, iters + 1):
             if ill_conditioned(M, R):
                 break
@@ -151,8 +158,9 @@ def test_c2_full(cl):
 
 
 def test_c4_full(cl):
+    """c4 as bench.py runs it: iterate(4) in one call (half-row passes, lazy normalisation in steps 1-3)"""
     g = gen.config("c4")
-    _record("c4", run_case(cl, g, g.d, g.iters, per_iter=False))
+    _record("c4", run_case(cl, g, g.d, g.iters, one_call=True))
 
 
 def test_determinism_and_composability(cl):
@@ -445,6 +453,7 @@ def test_half_row_passes_bitwise(cl, heavy, monkeypatch):
     heavy rows (threshold 8 makes most rows heavy), rows without out-edges (the zero-row skip from
     step 3 on), weights, split iterate calls, and the loopback exchange (peer stores in pass 2)."""
     monkeypatch.setenv("CLEORA_HEAVY_THRESH", heavy)
+    monkeypatch.setenv("CLEORA_LAZY", "0")          # bitwise: every step normalised (lazy steps: below)
     rng = np.random.default_rng(21)
     n = 6000
     hub = gen.EdgeList("hub", n, np.concatenate([np.zeros(5000, np.int32), rng.integers(0, n, 20000).astype(np.int32)]),
@@ -478,3 +487,47 @@ def test_half_row_passes_bitwise(cl, heavy, monkeypatch):
     cl.cleora_iterate(G, 4)
     compare(cl.cleora_fetch(G), oracle.embed(M, 1024, 3, 4), "halves vs oracle")
     G.close()
+
+
+@pytest.mark.parametrize("heavy", ["256", "8"])
+def test_lazy_normalisation_between_steps(cl, heavy, monkeypatch):
+    """Half-row steps inside one iterate call leave their rows unnormalised with the row scales aside
+    and the next step folds the scales into its weights; only the call's last step normalises (reading
+    R21).  Against the oracle's T_k within the bars, against every-step-normalised (CLEORA_LAZY=0)
+    within rounding, bitwise reproducible, and split calls (each call's last step normalises) agree:
+    light rows, single- and multi-part heavy rows (threshold 8), rows without out-edges, weights, both
+    gather engines."""
+    monkeypatch.setenv("CLEORA_HEAVY_THRESH", heavy)
+    monkeypatch.setenv("CLEORA_HALVES", "1")
+    rng = np.random.default_rng(31)
+    n = 6000
+    hub = gen.EdgeList("hub", n, np.concatenate([np.zeros(5000, np.int32), rng.integers(0, n, 20000).astype(np.int32)]),
+                       np.concatenate([np.arange(1, 5001, dtype=np.int32), rng.integers(0, n, 20000).astype(np.int32)]),
+                       rng.lognormal(0, 1, 25000).astype(np.float32), True)
+    graphs = [hub, gen.rmat_directed(8192, 13, 120000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=32), gen.config("c1")]
+    for g in graphs:
+        M = oracle.build_from(g)
+        R4 = oracle.embed(M, 1024, 3, 4)
+        for mode in ("async", "bulk"):
+            monkeypatch.setenv("CLEORA_GATHER", mode)
+            outs = {}
+            for lazy, split in (("1", (4,)), ("1", (4,)), ("0", (4,)), ("1", (1, 3)), ("1", (2, 2))):
+                monkeypatch.setenv("CLEORA_LAZY", lazy)
+                G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0)
+                try:
+                    cl.cleora_init(G, 1024, 3)
+                    for k in split:
+                        cl.cleora_iterate(G, k)
+                        T = cl.cleora_fetch(G)          # between calls T holds normalised rows
+                        nz = T.any(1)
+                        assert np.allclose(np.linalg.norm(T[nz].astype(np.float64), axis=1), 1.0, atol=1e-6)
+                    key = (lazy, split)
+                    if key in outs:
+                        assert outs[key].tobytes() == T.tobytes(), f"{g.name}: lazy run not reproducible"
+                    outs[key] = T
+                finally:
+                    G.close()
+            for key, T in outs.items():
+                compare(T, R4, f"{g.name} {mode} heavy={heavy} lazy={key}")
+            compare(outs[("1", (4,))], outs[("0", (4,))], f"{g.name} {mode}: lazy vs every step normalised")
+
