@@ -558,7 +558,9 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": load_traffic(g.name, d),
                 "kernel": "k_spmm_tma (fused SpMM + row L2 normalise)" + (
-                    f", {lps} half-row launches per iteration (bitwise the whole-row result); figures per iteration"
+                    f", {lps} half-row launches per iteration; inside one iterate call every step but the last leaves its "
+                    "rows unnormalised with their scales aside and the next step runs on pre-scaled weights (one short "
+                    "k_lazy_vals launch, inside the timed events; DESIGN reading R21); figures per iteration"
                     if lps > 1 else ""),
                 "launches_per_iteration": lps,
                 "kernel_ms": spmm_ms, "kernel_timing": "CUDA events around cleora_iterate in the timed steps",

@@ -72,6 +72,16 @@ def test_loopback_shards_bit_exact(cl, world):
             assert not csr["deg"][:r0].any() and not csr["deg"][r1:].any()
 
 
+def _close(a, b, tol=1e-5):
+    """within the parity bars (max|d| <= 1e-5, cosine >= 0.99999 per non-zero row), same zero rows"""
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    assert np.abs(a64 - b64).max() <= tol
+    nz = b64.any(1)
+    assert np.array_equal(a64.any(1), nz)
+    cos = (a64[nz] * b64[nz]).sum(1) / (np.linalg.norm(a64[nz], axis=1) * np.linalg.norm(b64[nz], axis=1))
+    assert cos.min() >= 0.99999
+
+
 def _embed(cl, g, d, calls, **kw):
     G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0, **kw)
     try:
@@ -88,9 +98,13 @@ def _embed(cl, g, d, calls, **kw):
 @pytest.mark.parametrize("d", [96, 512, 1024])
 def test_deferred_exchange_bitwise(cl, d, monkeypatch):
     """iterate(4) (3 deferred steps + a full one), iterate(1) x 4 (every step full) and the undeferred
-    exchange all give every replica the 1-GPU bits."""
+    exchange all give every replica the 1-GPU bits (every step normalised: lazy steps, reading R21, are
+    one GPU's only; its default result is checked against the sharded one within the parity bars)."""
     g = gen.rmat_directed(8192, 13, 120000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=4)   # 50% never-gathered rows
+    lazy = _embed(cl, g, d, [4])[0]
+    monkeypatch.setenv("CLEORA_LAZY", "0")
     ref = _embed(cl, g, d, [4])[0]
+    _close(lazy, ref)
     for calls in ([4], [1, 1, 1, 1], [3, 1]):
         for T in _embed(cl, g, d, calls, loopback=True, world=3, rank=1):
             assert T.tobytes() == ref.tobytes(), calls
@@ -112,9 +126,11 @@ def test_chunked_sharded_equals_single(cl):
 
 
 @pytest.mark.parametrize("name,world", [("c2", 4), ("c4", 2)])
-def test_full_size_sharded_bitwise(cl, name, world):
+def test_full_size_sharded_bitwise(cl, name, world, monkeypatch):
     """The bench configs row-sharded in loopback (every replica of every emulated rank) against one
-    GPU, bitwise, on row blocks across the graph (host memory: a few GB per replica block)."""
+    GPU, bitwise, on row blocks across the graph (host memory: a few GB per replica block).  One GPU
+    with every step normalised (CLEORA_LAZY=0): lazy steps (reading R21) are one GPU's only."""
+    monkeypatch.setenv("CLEORA_LAZY", "0")
     import torch
     g = gen.config(name)
     dev = torch.device("cuda", 0)
