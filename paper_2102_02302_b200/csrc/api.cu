@@ -416,9 +416,9 @@ struct cleora_graph {
     bool env_write_zero = false, env_no_hot = false, env_defer = true;
     int gmode = 0;                  // gather engine for the current dp (gather_mode)
     bool halves = false;            // dp = 1024 steps run as two half-row passes (cleora_init decides)
-    // lazy normalisation between the half-row steps of one iterate call (one GPU): fp64 first-half sums
-    // of squares [0..N), then fp32 scales of T[0] [N..1.5N) and of T[1], then nnz fp32 scaled weights
-    // (spmm_tma.cu); zeroed once
+    // lazy normalisation between the half-row steps of one iterate call: fp64 first-half sums of squares
+    // [0..N), then the scaled weights of the largest shard (fp32); the row scales live behind each T
+    // buffer's rows (spmm_tma.cu, reading R21)
     double* lazy_buf = nullptr;
     bool env_lazy = true;
     int heavy_thresh = 64;
@@ -1282,7 +1282,9 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     g->env_lazy = !(getenv("CLEORA_LAZY") && atoi(getenv("CLEORA_LAZY")) == 0);
     if (dp != g->dp || !g->T[0]) {
         free_T(g);
-        const size_t tb = (size_t)g->n * dp * sizeof(float);
+        // N x dp rows, then N fp32 row scales (lazy steps, reading R21: a peer's scales ride in the same
+        // allocation, so the IPC mapping of its T covers them); the scales start at 0
+        const size_t tb = ((size_t)g->n * dp + (size_t)g->n) * sizeof(float);
         Status sa = Status::ok();
         // peers map T through CUDA IPC, which exports whole allocations: T at a segment's base
         const int tflags = g->xmode == X_PEER ? kAllocBase : 0;
@@ -1299,6 +1301,15 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
                     sa = dalloc((void**)&g->rep[p][i], tb, g->stream, "loopback replica");
             }
         }
+        for (int i = 0; i < 2 && sa.good(); i++)
+            if (cudaMemsetAsync(g->T[i] + (size_t)g->n * dp, 0, (size_t)g->n * sizeof(float), g->stream) != cudaSuccess)
+                sa = Status::make(4, "cleora_init: memset of the row scales failed");
+        if (sa.good() && g->xmode == X_LOOPBACK)
+            for (int p = 0; p < g->world && sa.good(); p++)
+                for (int i = 0; i < 2 && sa.good(); i++)
+                    if (p != g->rank &&
+                        cudaMemsetAsync(g->rep[p][i] + (size_t)g->n * dp, 0, (size_t)g->n * sizeof(float), g->stream) != cudaSuccess)
+                        sa = Status::make(4, "cleora_init: memset of the row scales failed");
         // every rank must have its replicas before any maps them (failure agreement)
         if (g->xmode == X_PEER || g->xmode == X_NCCL) sa = comm_agree(g, sa);
         if (sa.good() && g->xmode == X_PEER) sa = open_peers(g);   // collective; may switch every rank to X_NCCL
@@ -1418,12 +1429,15 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
     // last leaves its rows unnormalised with their scales aside, and the next step folds the scales
     // into its weights -- the last step writes normalised rows, so what T holds between calls is
     // unchanged.  Saves the first half's read-back and rewrite (c4: 9.4 GB of 188 GB per step).
-    const bool lazy = g->halves && g->world == 1 && g->xmode != X_LOOPBACK && g->env_lazy && k >= 2;
+    // One GPU, loopback and peer stores alike (the peers receive the unnormalised halves and the scales
+    // like any row, so P does not change a bit); not with the NCCL all-gather fallback.
+    const bool lazy = g->halves && g->env_lazy && k >= 2 &&
+                      (g->world == 1 || g->xmode == X_LOOPBACK || g->xmode == X_PEER);
     if (lazy && !g->lazy_buf) {
-        const size_t bytes = (size_t)2 * g->n * sizeof(double) + (size_t)g->own().nnz * sizeof(float);
-        Status s = dalloc((void**)&g->lazy_buf, bytes, g->stream, "lazy scales");
-        if (s.good() && cudaMemsetAsync(g->lazy_buf, 0, bytes, g->stream) != cudaSuccess)
-            s = Status::make(4, "cleora_iterate: memset of the lazy scales failed");
+        int64_t nnz_max = 0;
+        for (const Csr& c : g->csr) nnz_max = std::max(nnz_max, c.nnz);
+        const size_t bytes = (size_t)g->n * sizeof(double) + (size_t)nnz_max * sizeof(float);
+        Status s = dalloc((void**)&g->lazy_buf, bytes, g->stream, "lazy sums and weights");
         if (!s.good()) return fail(s);
     }
     for (int32_t i = 0; i < k; i++) {
@@ -1475,21 +1489,21 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
             a.peer_mask = (a.n_peers > 0 && !g->pmask.empty() && i + 1 < k) ? g->pmask[g->pmask.size() > 1 ? p : 0]
                                                                               : nullptr;
             a.pass = 0;
-            float* scales = g->lazy_buf ? reinterpret_cast<float*>(g->lazy_buf + g->n) : nullptr;
+            a.scale_off = (int64_t)g->n * g->dp;
             a.ss_half = lazy && i + 1 < k ? g->lazy_buf : nullptr;
-            a.scale_out = nullptr;
+            a.lazy_out = 0;
             Status s = Status::ok();
             if (lazy && i > 0) {
                 // T_in holds the previous step's rows unnormalised: fold their scales into the weights
-                float* lv = scales + (size_t)2 * g->n;
-                s = launch_lazy_vals(c.val, c.col, scales + (size_t)in * g->n, c.nnz, lv, g->stream);
+                float* lv = reinterpret_cast<float*>(g->lazy_buf + g->n);
+                s = launch_lazy_vals(c.val, c.col, a.T_in + a.scale_off, c.nnz, lv, g->stream);
                 a.val = lv;
             }
             if (g->halves && s.good()) {
                 a.pass = 1;
                 s = launch_spmm_norm(a, g->stream);
                 a.pass = 2;
-                a.scale_out = lazy && i + 1 < k ? scales + (size_t)out * g->n : nullptr;
+                a.lazy_out = lazy && i + 1 < k ? 1 : 0;
             }
             if (s.good()) s = launch_spmm_norm(a, g->stream);
             if (!s.good()) return fail(s);
@@ -1703,7 +1717,8 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
         for (int q = 0; q < kMaxPeers; q++) a.peer_out[q] = nullptr;
         a.skip_zero_rows = 0;
         a.csr_prefetch = 0;
-        a.scale_out = nullptr;
+        a.lazy_out = 0;
+        a.scale_off = 0;
         a.ss_half = nullptr;
         a.peer_mask = nullptr;
         a.gather_mode = g->gmode;

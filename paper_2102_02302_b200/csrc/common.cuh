@@ -119,14 +119,26 @@ struct SpmmArgs {
     // unnormalised into T_out and nowhere else; 2 = columns [512, 1024), then the whole row is finished
     // from T_out's first half -- bitwise the whole-row result (see spmm_tma.cu)
     int32_t pass;
-    // Lazy normalisation between the half-row steps of one iterate call (world 1; spmm_tma.cu):
-    // scale_out non-NULL (pass 2): y is written unnormalised and scale_out[row] = 1 / ||y||; ss_half
-    // non-NULL: pass 1 stores each light row's fp64 sum of squares over the first half, pass 2 adds it
-    // instead of reading the half back.  The next step gathers those rows with weights that carry the
+    // Lazy normalisation between the half-row steps of one iterate call (spmm_tma.cu, reading R21).
+    // ss_half non-NULL (a lazy step): pass 1 stores each light row's fp64 sum of squares over the first
+    // half and sends that half, unnormalised, to the peers too; lazy_out (its pass 2): y is written
+    // unnormalised and 1 / ||y|| goes to the row scales, which sit scale_off floats behind the rows of
+    // T_out and of every peer replica.  The next step gathers those rows with weights that carry the
     // scales (launch_lazy_vals), so its kernels need nothing else.
-    float* scale_out;
+    int32_t lazy_out;
+    int64_t scale_off;
     double* ss_half;
 };
+
+// A lazy step's row scale: into T_out's scales and every peer replica's (the row's peer mask, as its rows)
+__device__ __forceinline__ void put_scale(const SpmmArgs& a, int64_t row, float v, bool empty = false) {
+    a.T_out[a.scale_off + row] = v;
+    if (a.n_peers > 0) {
+        const unsigned m = (empty || !a.peer_mask) ? 0xffu : a.peer_mask[row];
+        for (int p = 0; p < a.n_peers; p++)
+            if ((m >> p) & 1u) a.peer_out[p][a.scale_off + row] = v;
+    }
+}
 
 // Store float4 f of row `row` of the iteration's output into T_out and every peer replica.  `empty`:
 // the row has no entries (its zeros always reach the peers, which then skip it like this rank does).

@@ -178,24 +178,27 @@ __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, f
     if (empty && a.skip_zero_rows) return;           // acc is still all zeros
     if (HALF && a.pass == 1) {
         if (!empty) {
-            float4* out = reinterpret_cast<float4*>(a.T_out + row * (int64_t)a.dp);
-#pragma unroll
-            for (int v = 0; v < V; v++) __stcg(out + lane + 32 * v, acc[v]);
-            if (a.ss_half) {                         // lazy step: this half's sum of squares for pass 2
-                double ss = 0.0;
+            if (a.ss_half) {                         // lazy step: this half's sum of squares for pass 2, and
+                double ss = 0.0;                     // the half itself, unnormalised, to the peers as well
 #pragma unroll
                 for (int v = 0; v < V; v++) ss += sq4(acc[v]);
                 ss = warp_sum(ss);
                 if (lane == 0) a.ss_half[row] = ss;
+#pragma unroll
+                for (int v = 0; v < V; v++) put_out4(a, row, lane + 32 * v, acc[v]);
+            } else {
+                float4* out = reinterpret_cast<float4*>(a.T_out + row * (int64_t)a.dp);
+#pragma unroll
+                for (int v = 0; v < V; v++) __stcg(out + lane + 32 * v, acc[v]);
             }
         }
 #pragma unroll
         for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
         return;
     }
-    if (HALF && a.pass == 2 && a.scale_out) {
+    if (HALF && a.pass == 2 && a.lazy_out) {
         // lazy step: both halves stay unnormalised in T_out (the first from pass 1), the row scale goes
-        // to scale_out -- no read-back and rewrite of the first half (c4: 2 x 4.7 GB per step)
+        // to the row scales -- no read-back and rewrite of the first half (c4: 2 x 4.7 GB per step)
         double ss = 0.0;
 #pragma unroll
         for (int v = 0; v < V; v++) ss += sq4(acc[v]);
@@ -208,7 +211,7 @@ __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, f
             put_out4(a, row, 32 * V + lane + 32 * v, acc[v], empty);
             acc[v] = z;
         }
-        if (lane == 0) a.scale_out[row] = (float)inv_norm(ss);
+        if (lane == 0) put_scale(a, row, (float)inv_norm(ss), empty);
         return;
     }
     if (HALF && a.pass == 2) {
@@ -364,14 +367,17 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
         if (it.nparts == 1) {
             float4* outr = reinterpret_cast<float4*>(a.T_out + (int64_t)it.row * a.dp);
             if (a.pass == 1) {
-                if (mine) __stcg(outr + t, y);
+                if (mine) {
+                    if (a.ss_half) put_out4(a, it.row, t, y);   // lazy step: the peers get the half too
+                    else __stcg(outr + t, y);
+                }
             } else {
                 if (!mine) y = __ldcg(outr + t);
                 const double tot = block_sum(sq4(y), scratch);
                 const double inv = inv_norm(tot);
-                if (a.scale_out) {                    // lazy step: unnormalised, the scale aside
+                if (a.lazy_out) {                     // lazy step: unnormalised, the scale aside
                     if (mine) put_out4(a, it.row, t, y);
-                    if (t == 0) a.scale_out[it.row] = (float)inv;
+                    if (t == 0) put_scale(a, it.row, (float)inv);
                 } else {
                     put_out4(a, it.row, t, scale4(y, inv));
                 }
@@ -400,9 +406,9 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
                     }
                     const double tot = block_sum(zx * zx + zy * zy + zz * zz + zw * zw, scratch);
                     const double inv = inv_norm(tot);
-                    if (a.scale_out) {                // lazy step: unnormalised, the scale aside
+                    if (a.lazy_out) {                 // lazy step: unnormalised, the scale aside
                         if (t < nqf) put_out4(a, it.row, t, make_float4((float)zx, (float)zy, (float)zz, (float)zw));
-                        if (t == 0) a.scale_out[it.row] = (float)inv;
+                        if (t == 0) put_scale(a, it.row, (float)inv);
                     } else if (t < nqf) {
                         put_out4(a, it.row, t,
                                  make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));

@@ -44,7 +44,9 @@ def _worker(rank, world, port, q):
         g = gen.rmat_directed(8192, 13, 120000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=4)
         u = gen.chung_lu(20000, 60000, 2.1, 9.5388, 233115.5 * 20000 / 1134890, seed=2)
         res = []
-        for gr, d, calls in ((g, 256, [3]), (g, 256, [1, 2]), (u, 1024, [4]), (u, 64, [2, 2])):
+        # (g, 1024): nnz = 14 N, so half-row passes with lazy steps (reading R21) through the peer mappings
+        for gr, d, calls in ((g, 256, [3]), (g, 256, [1, 2]), (u, 1024, [4]), (u, 64, [2, 2]), (g, 1024, [4]),
+                             (g, 1024, [1, 3])):
             opens0 = cl.cleora_ipc_opens()
             G = cl.cleora_build(gr.src, gr.dst, gr.w, gr.n, gr.directed, device=0, rank=rank, world=world,
                                 host_allgather=ag)
@@ -64,12 +66,14 @@ def _worker(rank, world, port, q):
                 G.close()
             dist.barrier()
         # 1-GPU references, computed by rank 0 in its own process
+        # (the same call split: lazy steps are placed by the calls)
         if rank == 0:
-            for gr, d, calls in ((g, 256, [3]), (u, 1024, [4]), (u, 64, [4])):
+            for gr, d, calls in ((g, 256, [3]), (u, 1024, [4]), (u, 64, [4]), (g, 1024, [4]), (g, 1024, [1, 3])):
                 G = cl.cleora_build(gr.src, gr.dst, gr.w, gr.n, gr.directed, device=0)
                 cl.cleora_init(G, d, 0)
-                cl.cleora_iterate(G, sum(calls))
-                out[(gr.name, d)] = cl.cleora_fetch(G).tobytes()
+                for k in calls:
+                    cl.cleora_iterate(G, k)
+                out[(gr.name, d, tuple(calls))] = cl.cleora_fetch(G).tobytes()
                 G.close()
         q.put((rank, res, out))
     except Exception as e:  # report instead of hanging the parent
@@ -103,7 +107,8 @@ def test_processes_one_gpu_peer_exchange(world):
         res = got[rank][0]
         for i, (name, d, calls, mode, b, e, opens, T) in enumerate(res):
             assert mode == 2, f"rank {rank}: exchange mode {mode}, expected fused peer stores (2)"
-            assert T == refs[(name, d)], f"rank {rank} {name} d={d} calls={calls}: differs from 1 GPU"
+            key = (name, d, tuple(calls)) if (name, d, tuple(calls)) in refs else (name, d, (sum(calls),))
+            assert T == refs[key], f"rank {rank} {name} d={d} calls={calls}: differs from 1 GPU"
             if i == 1:      # same graph and d as case 0: the peer's blocks come back from its cache
                 assert opens == 0, f"rank {rank}: {opens} new IPC mappings for a repeated handle"
         assert res[0][4] == (0 if rank == 0 else res[0][4]) and res[0][5] > res[0][4]

@@ -95,19 +95,21 @@ def _embed(cl, g, d, calls, **kw):
         G.close()
 
 
+@pytest.mark.parametrize("lazy", ["1", "0"])
 @pytest.mark.parametrize("d", [96, 512, 1024])
-def test_deferred_exchange_bitwise(cl, d, monkeypatch):
+def test_deferred_exchange_bitwise(cl, d, lazy, monkeypatch):
     """iterate(4) (3 deferred steps + a full one), iterate(1) x 4 (every step full) and the undeferred
-    exchange all give every replica the 1-GPU bits (every step normalised: lazy steps, reading R21, are
-    one GPU's only; its default result is checked against the sharded one within the parity bars)."""
+    exchange all give every replica the 1-GPU bits -- with lazy half-row steps at d = 1024 (reading R21:
+    the peers receive the unnormalised halves and the row scales like any row) and with every step
+    normalised (CLEORA_LAZY=0)."""
+    monkeypatch.setenv("CLEORA_LAZY", lazy)
     g = gen.rmat_directed(8192, 13, 120000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=4)   # 50% never-gathered rows
-    lazy = _embed(cl, g, d, [4])[0]
-    monkeypatch.setenv("CLEORA_LAZY", "0")
     ref = _embed(cl, g, d, [4])[0]
-    _close(lazy, ref)
-    for calls in ([4], [1, 1, 1, 1], [3, 1]):
+    for calls in ([4], [1, 1, 1, 1], [3, 1], [2, 2]):
+        ref_c = ref if lazy == "0" or calls == [4] else _embed(cl, g, d, calls)[0]
         for T in _embed(cl, g, d, calls, loopback=True, world=3, rank=1):
-            assert T.tobytes() == ref.tobytes(), calls
+            assert T.tobytes() == ref_c.tobytes(), calls
+        _close(ref_c, ref)
     monkeypatch.setenv("CLEORA_NO_DEFER", "1")
     for T in _embed(cl, g, d, [4], loopback=True, world=3, rank=0):
         assert T.tobytes() == ref.tobytes()
@@ -126,11 +128,10 @@ def test_chunked_sharded_equals_single(cl):
 
 
 @pytest.mark.parametrize("name,world", [("c2", 4), ("c4", 2)])
-def test_full_size_sharded_bitwise(cl, name, world, monkeypatch):
+def test_full_size_sharded_bitwise(cl, name, world):
     """The bench configs row-sharded in loopback (every replica of every emulated rank) against one
-    GPU, bitwise, on row blocks across the graph (host memory: a few GB per replica block).  One GPU
-    with every step normalised (CLEORA_LAZY=0): lazy steps (reading R21) are one GPU's only."""
-    monkeypatch.setenv("CLEORA_LAZY", "0")
+    GPU, bitwise, on row blocks across the graph (host memory: a few GB per replica block); c4 with
+    its lazy half-row steps (reading R21) on both sides."""
     import torch
     g = gen.config(name)
     dev = torch.device("cuda", 0)
