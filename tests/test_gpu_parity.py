@@ -142,6 +142,36 @@ def _record(name, worst):
             f.write(line + "\n")
 
 
+def test_degree_of_long_weighted_rows_bit_exact(cl):
+    """deg(a) is the sequential fp64 fold over ascending b (reading B3).  Rows of > 32 entries take a
+    parallel sum when it provably equals that fold (every e_ab a multiple of 2^q and the total below
+    2^(53+q): no partial sum in any order rounds), else the sequential fold.  Rows built to fall on
+    either side -- dyadic weights, fp32 lognormal weights (c4's kind), weights spanning 1e-7..1e7 whose
+    partial sums round, duplicates merged first -- must give the oracle's bits, through both builds."""
+    rng = np.random.default_rng(61)
+    n, m = 3000, 6000
+    rows = []
+    ws = [rng.integers(1, 4096, m).astype(np.float32) / np.float32(8.0),          # multiples of 1/8
+          rng.lognormal(0.0, 1.0, m).astype(np.float32),                         # c4-like
+          (10.0 ** rng.uniform(-7, 7, m)).astype(np.float32),                    # rounds: sequential fold
+          np.float32(2.0 ** 100) * rng.integers(1, 9, m).astype(np.float32),     # large dyadic
+          rng.lognormal(0.0, 1.0, m).astype(np.float32)]
+    src = np.concatenate([np.full(m, r, np.int32) for r in range(len(ws))])
+    dst = np.concatenate([rng.integers(0, n, m).astype(np.int32) for _ in ws])
+    dst[-m:] = rng.integers(0, 40, m).astype(np.int32)                           # many duplicates per run
+    g = gen.EdgeList("longw", n, src, dst, np.concatenate(ws), True)
+    M = oracle.build_from(g)
+    import os
+    for small in ("1", "0"):
+        os.environ["CLEORA_SMALL_BUILD"] = small
+        try:
+            G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0)
+            check_csr(cl.cleora_fetch_csr(G), M)
+            G.close()
+        finally:
+            os.environ.pop("CLEORA_SMALL_BUILD", None)
+
+
 def test_c1_full(cl):
     g = gen.config("c1")
     _record("c1", run_case(cl, g, g.d, g.iters))
