@@ -1425,7 +1425,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
     DeviceGuard guard(g->device);
     order_after_side(g);
     const int nsh = g->xmode == X_LOOPBACK ? g->world : 1;
-    // Lazy normalisation (reading R21): with half-row passes on one GPU, every step of this call but the
+    // Lazy normalisation (reading R21): with half-row passes, every step of this call but the
     // last leaves its rows unnormalised with their scales aside, and the next step folds the scales
     // into its weights -- the last step writes normalised rows, so what T holds between calls is
     // unchanged.  Saves the first half's read-back and rewrite (c4: 9.4 GB of 188 GB per step).
