@@ -537,7 +537,8 @@ def test_lazy_normalisation_between_steps(cl, heavy, monkeypatch):
     graphs = [hub, gen.rmat_directed(8192, 13, 120000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=32), gen.config("c1")]
     for g in graphs:
         M = oracle.build_from(g)
-        R4 = oracle.embed(M, 1024, 3, 4)
+        R_all = oracle.embed(M, 1024, 3, 4, keep_all=True)
+        R4 = R_all[4]
         for mode in ("async", "bulk"):
             monkeypatch.setenv("CLEORA_GATHER", mode)
             outs = {}
@@ -546,11 +547,14 @@ def test_lazy_normalisation_between_steps(cl, heavy, monkeypatch):
                 G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0)
                 try:
                     cl.cleora_init(G, 1024, 3)
+                    done = 0
                     for k in split:
                         cl.cleora_iterate(G, k)
-                        T = cl.cleora_fetch(G)          # between calls T holds normalised rows
-                        nz = T.any(1)
+                        done += k
+                        T = cl.cleora_fetch(G)          # between calls T is T_done: normalised rows, and the
+                        nz = T.any(1)                   # rows without entries 0 (inner steps skip the ungathered)
                         assert np.allclose(np.linalg.norm(T[nz].astype(np.float64), axis=1), 1.0, atol=1e-6)
+                        compare(T, R_all[done], f"{g.name} {mode} after {done} steps ({split})")
                     key = (lazy, split)
                     if key in outs:
                         assert outs[key].tobytes() == T.tobytes(), f"{g.name}: lazy run not reproducible"
