@@ -420,7 +420,12 @@ struct cleora_graph {
     // [0..N), then the scaled weights of the largest shard (fp32); the row scales live behind each T
     // buffer's rows (spmm_tma.cu, reading R21)
     double* lazy_buf = nullptr;
-    bool env_lazy = true;
+    bool env_lazy = true, env_t0_all = false;
+    // T_0 written only for the rows a step can gather (in-degree > 0, g->indeg): the other rows are
+    // never read before the first step overwrites them, unless T_0 itself is read -- complete_t0 fills
+    // them in then (fetch, trim, merge, reconstruct, set_rows)
+    mutable bool t0_partial = false;
+    uint64_t t0_seed = 0;
     int heavy_thresh = 64;
     Schedule sched;
     int32_t d = 0, dp = 0;
@@ -684,6 +689,23 @@ void order_after_side(const cleora_graph* g) {
         cudaStreamWaitEvent(g->stream, g->ev_copied, 0);
         g->copy_pending = false;
     }
+}
+
+// T_0 is read before any step (fetch, trim, merge, reconstruct, set_rows): write the rows init left
+// out (in-degree 0), in every local replica
+Status complete_t0(const cleora_graph* gc) {
+    cleora_graph* g = const_cast<cleora_graph*>(gc);
+    if (!g->t0_partial) return Status::ok();
+    if (g->iters == 0 && g->cur == 0 && g->T[0] && g->indeg) {
+        CL_TRY(launch_hash_init(g->T[0], g->n, g->d, g->dp, g->t0_seed, g->stream, g->d_base, g->n_graphs, g->indeg, 2));
+        if (g->xmode == X_LOOPBACK)
+            for (int p = 0; p < g->world; p++)
+                if (p != g->rank && g->rep[p][0])
+                    CL_TRY(launch_hash_init(g->rep[p][0], g->n, g->d, g->dp, g->t0_seed, g->stream, g->d_base,
+                                            g->n_graphs, g->indeg, 2));
+    }
+    g->t0_partial = false;
+    return Status::ok();
 }
 
 void free_T(cleora_graph* g) {
@@ -1280,6 +1302,7 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     g->env_no_hot = getenv("CLEORA_NO_HOT") != nullptr;
     g->env_defer = getenv("CLEORA_NO_DEFER") == nullptr;
     g->env_lazy = !(getenv("CLEORA_LAZY") && atoi(getenv("CLEORA_LAZY")) == 0);
+    g->env_t0_all = getenv("CLEORA_T0_ALL") && atoi(getenv("CLEORA_T0_ALL")) != 0;
     if (dp != g->dp || !g->T[0]) {
         free_T(g);
         // N x dp rows, then N fp32 row scales (lazy steps, reading R21: a peer's scales ride in the same
@@ -1323,16 +1346,32 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     g->cur = 0;
     g->iters = 0;
     g->zclean[0] = g->zclean[1] = false;
-    // a9: T_0
+    // a9: T_0 -- on graphs whose T exceeds the L2 hot-row budget (where the write is milliseconds), only
+    // the rows a step can gather (in-degree > 0; the in-degree is the hot-row tags' input anyway);
+    // the rest is filled in only if T_0 itself is read (complete_t0).  c4: 2.3M of 4.85M rows.
     {
-        Status s = launch_hash_init(g->T[0], g->n, d, dp, seed, g->stream, g->d_base, g->n_graphs);
+        const char* hb = getenv("CLEORA_HOT_MB");
+        const int64_t budget = (int64_t)(hb ? atof(hb) : 72.0) * 1024 * 1024;
+        const int32_t* sel = nullptr;
+        if (!g->env_t0_all && g->nnz > 0 && (int64_t)g->n * dp * 4 > budget) {
+            if (!g->indeg && !g->sharded) {
+                Status s = in_degree(g->csr[0].col, g->csr[0].nnz, g->n, g->directed ? nullptr : g->csr[0].row_ptr,
+                                     g->stream, &g->indeg);
+                if (!s.good()) return fail(s);
+            }
+            sel = g->indeg;
+        }
+        Status s = launch_hash_init(g->T[0], g->n, d, dp, seed, g->stream, g->d_base, g->n_graphs, sel, sel ? 1 : 0);
         if (!s.good()) return fail(s);
         if (g->xmode == X_LOOPBACK)   // every emulated rank initialises its own replica
             for (int p = 0; p < g->world; p++)
                 if (p != g->rank) {
-                    s = launch_hash_init(g->rep[p][0], g->n, d, dp, seed, g->stream, g->d_base, g->n_graphs);
+                    s = launch_hash_init(g->rep[p][0], g->n, d, dp, seed, g->stream, g->d_base, g->n_graphs, sel,
+                                         sel ? 1 : 0);
                     if (!s.good()) return fail(s);
                 }
+        g->t0_partial = sel != nullptr;
+        g->t0_seed = seed;
     }
     // heavy rows: > 64 entries with TMA bulk gathers, > 256 with cp.async / LDG gathers (measured:
     // c2 12.68 vs 12.80 ms per step with 64 / 256; c5 427 -> 375 ms, c4@256 8.10 -> 7.27 ms with 256);
@@ -1541,6 +1580,10 @@ int cleora_fetch(const cleora_graph* g, int64_t row_begin, int64_t row_end, floa
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_fetch: rows outside [0, N]");
     if (row_end == row_begin) return CLEORA_OK;
     DeviceGuard guard(g->device);
+    {
+        Status st0 = complete_t0(g);
+        if (!st0.good()) return fail(st0);
+    }
     order_after_side(g);
     const float* src = g->T[g->cur] + row_begin * (int64_t)g->dp;
     const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -1562,6 +1605,10 @@ int cleora_fetch_async(cleora_graph* g, int64_t row_begin, int64_t row_end, floa
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_fetch_async: rows outside [0, N]");
     if (row_end == row_begin) return CLEORA_OK;
     DeviceGuard guard(g->device);
+    {
+        Status st0 = complete_t0(g);
+        if (!st0.good()) return fail(st0);
+    }
     cudaError_t e = cudaSuccess;
     if (!g->copy_stream) {
         e = cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking);
@@ -1604,6 +1651,10 @@ int cleora_merge_chunks(cleora_graph* const* chunks, int32_t n_chunks, float* ou
     }
     DeviceGuard guard(g0->device);
     cudaStream_t s = g0->stream;
+    for (int q = 0; q < n_chunks; q++) {
+        Status st0 = complete_t0(chunks[q]);
+        if (!st0.good()) return fail(st0);
+    }
     for (int q = 0; q < n_chunks; q++) order_after_side(chunks[q]);
     for (int q = 1; q < n_chunks; q++)
         if (chunks[q]->stream != s) {
@@ -1652,6 +1703,10 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
     if (n_new < 1) return usage("cleora_reconstruct: n_new must be >= 1");
     if (n_edges < 1) return usage("cleora_reconstruct: n_edges must be >= 1");
     DeviceGuard guard(g->device);
+    {
+        Status st0 = complete_t0(g);
+        if (!st0.good()) return fail(st0);
+    }
     order_after_side(g);
     cudaStream_t s = g->stream;
     const int32_t N2 = std::max(n_new, g->n);   // row space of the new nodes' transition rows
@@ -1765,6 +1820,10 @@ int cleora_fetch_replica(const cleora_graph* g, int32_t rank, int64_t row_begin,
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_fetch_replica: rows outside [0, N]");
     if (row_end == row_begin) return CLEORA_OK;
     DeviceGuard guard(g->device);
+    {
+        Status st0 = complete_t0(g);
+        if (!st0.good()) return fail(st0);
+    }
     order_after_side(g);
     const float* src = g->rep[rank][g->cur] + row_begin * (int64_t)g->dp;
     cudaError_t e = cudaMemcpy2DAsync(host_out, (size_t)g->d * sizeof(float), src, (size_t)g->dp * sizeof(float),
@@ -1783,6 +1842,10 @@ int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const f
     if (row_begin < 0 || row_end > g->n || row_begin > row_end) return usage("cleora_set_rows: rows outside [0, N]");
     if (row_end == row_begin) return CLEORA_OK;
     DeviceGuard guard(g->device);
+    {
+        Status st0 = complete_t0(g);
+        if (!st0.good()) return fail(st0);
+    }
     order_after_side(g);
     // loopback: every emulated rank sets the same rows in its own replica
     const int nrep = g->xmode == X_LOOPBACK ? g->world : 1;
@@ -1888,6 +1951,10 @@ int cleora_trim(cleora_graph* g) {
     if (!g->T[0]) return usage("cleora_trim: call cleora_init first");
     if (g->trimmed) return CLEORA_OK;
     DeviceGuard guard(g->device);
+    {
+        Status st0 = complete_t0(g);
+        if (!st0.good()) return fail(st0);
+    }
     // no order_after_side here: an asynchronous fetch of T[cur] keeps running on the copy stream and
     // reads nothing freed below (T[cur] stays); copy_pending stays set, so later fetches, merges and
     // destroy still order after it.  (Waiting here made the handle's stream -- often shared with the

@@ -1284,6 +1284,22 @@ __global__ void k_tag(int32_t* __restrict__ col, int64_t nnz, const int32_t* __r
 }
 }  // namespace
 
+Status in_degree(const int32_t* d_col, int64_t nnz, int32_t N, const int64_t* d_row_ptr_sym, cudaStream_t s,
+                 int32_t** out) {
+    DevBuf<int32_t> indeg;
+    CL_TRY(indeg.alloc(N, s, "in-degree", true));
+    if (d_row_ptr_sym) {
+        k_row_lengths<<<grid_for(N, 4), kThreads, 0, s>>>(d_row_ptr_sym, N, indeg.p);
+    } else {
+        CL_CUDA_TRY(cudaMemsetAsync(indeg.p, 0, (size_t)N * 4, s));
+        if (nnz > 0) k_indegree<<<grid_for(nnz, 4), kThreads, 0, s>>>(d_col, nnz, indeg.p);
+    }
+    CL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    *out = indeg.release();
+    return Status::ok();
+}
+
 Status hot_tag(int32_t* d_col, int64_t nnz, int32_t N, int64_t row_bytes, int64_t budget_bytes, cudaStream_t s,
                int64_t* n_hot, int64_t* n_ref, const int64_t* d_row_ptr_sym, const int32_t* d_indeg_in) {
     // hot rows = the K = budget / row_bytes rows of largest in-degree (exact threshold: the K-th

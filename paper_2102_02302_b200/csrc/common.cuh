@@ -247,8 +247,14 @@ Status expand_hypergraph(const int64_t* d_ptr, const int32_t* d_nodes, const flo
                          int64_t capacity, int64_t* n_out);
 
 // init.cu
+// sel (NULL: every row): an in-degree array; sel_mode 1 writes only the rows with in-degree > 0 (the
+// rows a step can gather), 2 only the others (completing T_0 when it is read before any step)
 Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s,
-                        const int64_t* d_base = nullptr, int32_t n_graphs = 0);
+                        const int64_t* d_base = nullptr, int32_t n_graphs = 0, const int32_t* sel = nullptr,
+                        int sel_mode = 0);
+// In-degree of every column of a CSR (undirected: the row lengths), device int32[N], long-lived
+Status in_degree(const int32_t* d_col, int64_t nnz, int32_t N, const int64_t* d_row_ptr_sym, cudaStream_t s,
+                 int32_t** out);
 
 // build.cu, batched handles: global ids = local ids + base[graph of the edge]; edge_ptr and
 // base are [n_graphs + 1] device arrays.  Returns EDATA (with the first bad edge) for a local id

@@ -47,12 +47,14 @@ __device__ __forceinline__ float hash_elem(const RowHash& r, uint32_t j) {
 // 64-bit division per element, 512 contiguous bytes per warp store instruction.
 // lid (batched handles, NULL otherwise): every row's id local to its graph; the hash keys on it, so
 // each graph of a batch gets its own T_0.
+// sel (NULL: every row): the in-degree; sel_mode 1 writes the rows with in-degree > 0, 2 the others
 __global__ void k_hash_init(float4* __restrict__ T, int64_t N, int32_t d, int32_t dp, uint64_t s,
-                            const int32_t* __restrict__ lid) {
+                            const int32_t* __restrict__ lid, const int32_t* __restrict__ sel, int sel_mode) {
     const int lane = threadIdx.x & 31;
     const int q = dp / 4;
     const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < N; v += wstride) {
+        if (sel && ((sel[v] != 0) != (sel_mode == 1))) continue;     // warp-uniform
         const int64_t id = lid ? (int64_t)lid[v] : v;
         const RowHash rh = row_hash(s ^ ((uint64_t)id << 32));
         float4* row = T + v * q;
@@ -86,7 +88,7 @@ __global__ void k_local_ids(const int64_t* __restrict__ base, int32_t n_graphs, 
 }  // namespace
 
 Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t seed, cudaStream_t s,
-                        const int64_t* d_base, int32_t n_graphs) {
+                        const int64_t* d_base, int32_t n_graphs, const int32_t* sel, int sel_mode) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -103,7 +105,7 @@ Status launch_hash_init(float* T, int64_t N, int32_t d, int32_t dp, uint64_t see
         k_local_ids<<<(unsigned)(gb < 1 ? 1 : gb), 256, 0, s>>>(d_base, n_graphs, lid);
         count_launches(1);
     }
-    k_hash_init<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4*>(T), N, d, dp, key, lid);
+    k_hash_init<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4*>(T), N, d, dp, key, lid, sel, sel_mode);
     const cudaError_t e = cudaGetLastError();
     count_launches(1);
     if (lid) dfree(lid, s);

@@ -565,3 +565,102 @@ def test_lazy_normalisation_between_steps(cl, heavy, monkeypatch):
                 compare(T, R4, f"{g.name} {mode} heavy={heavy} lazy={key}")
             compare(outs[("1", (4,))], outs[("0", (4,))], f"{g.name} {mode}: lazy vs every step normalised")
 
+
+
+def test_partial_t0_is_completed_on_every_read(cl, monkeypatch):
+    """On graphs whose T exceeds the hot-row budget, cleora_init writes T_0 only for rows a step can
+    gather (in-degree > 0) and fills in the others when T_0 itself is read.  Forced here on small
+    graphs (CLEORA_HOT_MB tiny): every read before the first step -- fetch, partial fetch, async fetch,
+    set_rows, trim, reconstruct, merge of chunks, loopback replicas, batches -- sees the full T_0 (bit-
+    exact vs the oracle), and every embedding is bitwise the one from a fully written T_0
+    (CLEORA_T0_ALL=1)."""
+    import torch
+    monkeypatch.setenv("CLEORA_HOT_MB", "0.001")
+    rng = np.random.default_rng(71)
+    graphs = [gen.rmat_directed(8192, 13, 50000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=72),   # many rows unreferenced
+              gen.chung_lu(20000, 60000, 2.1, 9.5388, 233115.5 * 20000 / 1134890, seed=73),  # isolated nodes
+              gen.tiny_graph(74, n_max=400, e_max=600, directed=True, weighted=True)]
+    d, seed = 96, 3
+
+    def mk(g, **kw):
+        G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0, **kw)
+        cl.cleora_init(G, d, seed)
+        return G
+
+    for g in graphs:
+        R0 = oracle.hash_init(g.n, d, seed)
+        G = mk(g)
+        assert cl.cleora_fetch(G).tobytes() == R0.tobytes(), g.name
+        G.close()
+        G = mk(g)
+        a, b = g.n // 3, min(g.n, g.n // 3 + 777)
+        assert cl.cleora_fetch(G, a, b).tobytes() == R0[a:b].tobytes()
+        G.close()
+        G = mk(g)
+        buf = torch.empty((g.n, d), dtype=torch.float32).pin_memory()
+        cl.cleora_fetch_async(G, 0, g.n, buf)
+        cl.cleora_sync(G)
+        assert buf.numpy().tobytes() == R0.tobytes()
+        G.close()
+        G = mk(g)
+        X = rng.standard_normal((5, d)).astype(np.float32)
+        cl.cleora_set_rows(G, 10, X)
+        R = R0.copy()
+        R[10:15] = X
+        assert cl.cleora_fetch(G).tobytes() == R.tobytes()
+        G.close()
+        G = mk(g)
+        cl.cleora_trim(G)
+        assert cl.cleora_fetch(G).tobytes() == R0.tobytes()
+        G.close()
+        new = np.arange(3, dtype=np.int32).repeat(4)
+        known = rng.integers(0, g.n, new.size).astype(np.int32)
+        outs = {}
+        for full in ("0", "1"):
+            monkeypatch.setenv("CLEORA_T0_ALL", full)
+            G = mk(g)
+            rec = cl.cleora_reconstruct(G, new, known, None, 3)
+            G.close()
+            G = mk(g)
+            cl.cleora_iterate(G, 3)
+            T3 = cl.cleora_fetch(G)
+            G.close()
+            G = mk(g)
+            cl.cleora_iterate(G, 1)
+            cl.cleora_iterate(G, 2)
+            T12 = cl.cleora_fetch(G)
+            G.close()
+            G = mk(g, loopback=True, world=3, rank=1)
+            reps0 = [cl.cleora_fetch_replica(G, p) for p in range(3)]
+            G.close()
+            G = mk(g, loopback=True, world=3, rank=2)
+            cl.cleora_iterate(G, 2)
+            reps2 = [cl.cleora_fetch_replica(G, p) for p in range(3)]
+            G.close()
+            hs = [mk(g, n_chunks=2, chunk=q, chunk_seed=5) for q in range(2)]
+            merged = cl.cleora_merge_chunks(hs)
+            for h in hs:
+                h.close()
+            outs[full] = (rec, T3, T12, reps0, reps2, merged)
+        monkeypatch.delenv("CLEORA_T0_ALL")
+        p, f = outs["0"], outs["1"]
+        assert p[0].tobytes() == f[0].tobytes(), f"{g.name}: reconstruct on T_0"
+        assert p[1].tobytes() == f[1].tobytes() and p[2].tobytes() == f[2].tobytes(), f"{g.name}: iterate"
+        for x, y in zip(p[3], f[3]):
+            assert x.tobytes() == y.tobytes() == R0.tobytes(), f"{g.name}: loopback T_0 replicas"
+        for x, y in zip(p[4], f[4]):
+            assert x.tobytes() == y.tobytes(), f"{g.name}: loopback iterate"
+        assert p[5].tobytes() == f[5].tobytes(), f"{g.name}: merge of T_0 chunks"
+    # a batch: T_0 keyed on local ids, rows left out by init filled in on the read
+    bg = [gen.tiny_graph(800 + i, n_max=300, e_max=400, directed=True) for i in range(10)]
+    ep = np.zeros(len(bg) + 1, np.int64)
+    ep[1:] = np.cumsum([x.n_edges for x in bg])
+    B = cl.cleora_build_batch(np.concatenate([x.src for x in bg]), np.concatenate([x.dst for x in bg]), None, ep,
+                              np.array([x.n for x in bg], np.int32), True, device=0)
+    cl.cleora_init(B, d, seed)
+    T0 = cl.cleora_fetch(B)
+    B.close()
+    base = 0
+    for x in bg:
+        assert T0[base:base + x.n].tobytes() == oracle.hash_init(x.n, d, seed).tobytes()
+        base += x.n
