@@ -183,6 +183,9 @@ CLEORA_API int cleora_build_batch(const int32_t* src, const int32_t* dst, const 
  *   h = mix(mix(seed + 0x9E3779B97F4A7C15) XOR (v << 32 | j)), mix = SplitMix64 finaliser
  * (reading R1 / I1: a realisation of "T_0 ~ U(-1,1)").  T_0 is NOT
  * normalised (reading R7).  May be called again to restart from T_0 (same or new d / seed).
+ * On graphs whose T exceeds the L2 hot-row budget only the rows some step can gather (in-degree
+ * > 0) are written here; the others are written by the first call that reads T_0 itself (fetch,
+ * trim, set_rows, reconstruct, merge) -- every read sees the whole T_0 (CLEORA_T0_ALL=1: all now).
  *   d >= 1 (any d; rows are stored with a stride padded to 4 floats, padding kept at 0).
  *   Errors: EUSAGE (g NULL, d < 1, d > CLEORA_MAX_D), EINTERNAL (out of memory).
  */
