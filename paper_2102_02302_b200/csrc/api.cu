@@ -1475,7 +1475,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
     if (lazy && !g->lazy_buf) {
         int64_t nnz_max = 0;
         for (const Csr& c : g->csr) nnz_max = std::max(nnz_max, c.nnz);
-        const size_t bytes = (size_t)g->n * sizeof(double) + (size_t)nnz_max * sizeof(float);
+        const size_t bytes = (size_t)(g->n + 1) / 2 * 2 * sizeof(double) + (size_t)nnz_max * sizeof(float);
         Status s = dalloc((void**)&g->lazy_buf, bytes, g->stream, "lazy sums and weights");
         if (!s.good()) return fail(s);
     }
@@ -1534,7 +1534,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
             Status s = Status::ok();
             if (lazy && i > 0) {
                 // T_in holds the previous step's rows unnormalised: fold their scales into the weights
-                float* lv = reinterpret_cast<float*>(g->lazy_buf + g->n);
+                float* lv = reinterpret_cast<float*>(g->lazy_buf + (g->n + 1) / 2 * 2);   // 16-byte aligned
                 s = launch_lazy_vals(c.val, c.col, a.T_in + a.scale_off, c.nnz, lv, g->stream);
                 a.val = lv;
             }
