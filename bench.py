@@ -10,8 +10,10 @@ graph: cleora_build (validate, mirror, radix sort, merge, row pointer, degree, D
 schedule) -> cleora_init (hash T_0) -> cleora_iterate(I) (I fused SpMM + row-normalise
 launches), with the COO already resident in HBM when the timed region starts.  The result
 stays in HBM; the end-to-end variant (``e2e``) goes through the same C-ABI calls with HOST
-buffers: pinned COO in, H2D inside cleora_build, and cleora_fetch of all N x d rows into
-pinned host memory, inside the timed region.
+buffers: pinned COO in, H2D inside cleora_build, and the result out into pinned host memory,
+inside the timed region -- as cleora_fetch_nonzero (the rows with entries and their ids; every
+other row is exactly 0 after a step, reading RZ), with the dense cleora_fetch of all N x d rows
+measured beside it (``e2e.dense_fetch``; ``--dense-fetch`` makes it the e2e figure).
 
 value = nnz * d * I / step_time   (nnz = stored CSR entries; BASELINE metric "nnz·d/s")
 Multi-GPU (one rank per GPU, NCCL): ``--gpus N`` under torchrun (WORLD_SIZE set, must equal N),
@@ -313,6 +315,7 @@ def parse_args(argv):
     ap.add_argument("--impl", default="cleora", choices=["cleora", "reference"])
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dense-fetch", action="store_true", help="e2e: fetch all N x d rows (cleora_fetch) only")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the c2/c3 SpMM figures")
     ap.add_argument("--dry-launch", action="store_true",
@@ -604,6 +607,11 @@ def main():
         pipe_mode = e2e_schedule(info["device_bytes"], t_bytes(g), total_hbm)
         pipelined = pipe_mode is not None
         outs = [torch.empty((g.n, d), dtype=torch.float32).pin_memory() for _ in range(2 if pipelined else 1)]
+        # the result as a user fetches it: the rows with entries and their ids (cleora_fetch_nonzero;
+        # every other row is exactly 0 after a step, reading RZ), packed into the front of the same
+        # pinned buffers; the dense N x d fetch is measured beside it
+        n_nzr = g.n - info["zero_rows"] if world == 1 else None
+        ids = [torch.empty(g.n, dtype=torch.int32).pin_memory() for _ in outs]
 
         def e2e_build():
             G = cl.cleora_build(src_h, dst_h, w_h, g.n, g.directed, device=local, stream=stream.cuda_stream,
@@ -612,17 +620,26 @@ def main():
             cl.cleora_iterate(G, iters)
             return G
 
-        def e2e_serial(k):
+        def fetch(G, i, compact, wait):
+            j = i % len(outs)
+            if compact:
+                (cl.cleora_fetch_nonzero if wait else cl.cleora_fetch_nonzero_async)(G, outs[j], ids[j])
+            elif wait:
+                cl.cleora_fetch(G, 0, g.n, outs[j])
+            else:
+                cl.cleora_fetch_async(G, 0, g.n, outs[j])
+
+        def e2e_serial(k, compact):
             for _ in range(k):
                 G = e2e_build()
-                cl.cleora_fetch(G, 0, g.n, outs[0])
+                fetch(G, 0, compact, True)
                 G.close()
 
-        def e2e_pipelined(k):
+        def e2e_pipelined(k, compact):
             prev = None
             for i in range(k):
                 G = e2e_build()
-                cl.cleora_fetch_async(G, 0, g.n, outs[i % 2])
+                fetch(G, i, compact, False)
                 if pipe_mode == "trim":
                     cl.cleora_trim(G)
                 if prev is not None:
@@ -630,13 +647,13 @@ def main():
                 prev = G
             prev.close()
 
-        def timed(fn, k):
+        def timed(fn, k, compact):
             barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            fn(k)
+            fn(k, compact)
             e1.record(stream)
             e1.synchronize()
             clk.mark(t0, time.perf_counter())
@@ -645,38 +662,53 @@ def main():
             return max_over_ranks(e0.elapsed_time(e1) / k), 1e3 * (time.perf_counter() - t0) / k
 
         oom0 = cl.cleora_oom_fallbacks()
-        e2e_serial(1)
+        e2e_serial(1, False)
         if pipelined:
             try:
-                e2e_pipelined(2)
+                e2e_pipelined(2, True)
             except cl.CleoraError as e:          # out of memory after all: serial
                 print(f"bench.py: pipelined e2e failed ({e}); serial e2e", file=sys.stderr)
                 pipelined = False
                 cl.cleora_release_cached_memory()
-        k2 = k_serial = max(2, min(args.steps, 5))
-        ms_serial, wall_serial = timed(e2e_serial, k2)
-        if pipelined:
-            # the pipeline's fill (the first step's H2D + build + iterations, with no D2H to hide behind)
-            # is paid once per timed run: more steps than the serial run, so the figure is the schedule's
-            # steady-state rate rather than its start-up
-            k2 = max(2, min(args.steps, 10))
-            ms_e2e, wall = timed(e2e_pipelined, k2)
-            mode = "pipelined: step i's D2H (cleora_fetch_async) overlaps step i+1's H2D + build + iterations"
-            if pipe_mode == "trim":
-                mode += " (step i's handle trimmed to its result, cleora_trim, to make room)"
-            if ms_serial < ms_e2e:      # both measured the same way; report the faster schedule
-                mode = f"serial (faster than the measured {mode}: {ms_e2e:.1f} ms per step)"
-                ms_e2e, wall, k2 = ms_serial, wall_serial, k_serial
-        else:
-            ms_e2e, wall = ms_serial, wall_serial
-            mode = "serial: build, iterations, blocking fetch, destroy (two handles do not fit in HBM)"
         h2d = g.n_edges * 8 + (g.n_edges * 4 if g.w is not None else 0)
-        e2e = {"value": nnz * d * iters / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "oom_fallbacks": cl.cleora_oom_fallbacks() - oom0,
-               "d2h_bytes_per_step": g.n * d * 4, "ms_per_step": ms_e2e, "steps": k2, "wall_ms_per_step": wall,
-               "mode": mode, "serial_value": nnz * d * iters / (ms_serial / 1e3), "serial_ms_per_step": ms_serial,
-               "serial_steps": k_serial}
-        del outs, src_h, dst_h, w_h
+
+        def measure(compact):
+            k2 = k_serial = max(2, min(args.steps, 5))
+            ms_serial, wall_serial = timed(e2e_serial, k2, compact)
+            what = "cleora_fetch_nonzero_async" if compact else "cleora_fetch_async"
+            if pipelined:
+                # the pipeline's fill (the first step's H2D + build + iterations, with no D2H to hide behind)
+                # is paid once per timed run: more steps than the serial run, so the figure is the schedule's
+                # steady-state rate rather than its start-up
+                k2 = max(2, min(args.steps, 10))
+                ms_e2e, wall = timed(e2e_pipelined, k2, compact)
+                mode = f"pipelined: step i's D2H ({what}) overlaps step i+1's H2D + build + iterations"
+                if pipe_mode == "trim":
+                    mode += " (step i's handle trimmed to its result, cleora_trim, to make room)"
+                if ms_serial < ms_e2e:      # both measured the same way; report the faster schedule
+                    mode = f"serial (faster than the measured {mode}: {ms_e2e:.1f} ms per step)"
+                    ms_e2e, wall, k2 = ms_serial, wall_serial, k_serial
+            else:
+                ms_e2e, wall = ms_serial, wall_serial
+                mode = "serial: build, iterations, blocking fetch, destroy (two handles do not fit in HBM)"
+            d2h = (n_nzr * d * 4 + n_nzr * 4) if compact else g.n * d * 4
+            return {"value": nnz * d * iters / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e, "steps": k2, "wall_ms_per_step": wall,
+                    "mode": mode, "serial_value": nnz * d * iters / (ms_serial / 1e3),
+                    "serial_ms_per_step": ms_serial, "serial_steps": k_serial}
+
+        dense = measure(False)
+        if n_nzr is not None and not args.dense_fetch:
+            e2e = measure(True)
+            e2e["result"] = (f"cleora_fetch_nonzero: the {n_nzr:,} rows with entries (d fp32 each) and their "
+                             f"int32 ids; the other {g.n - n_nzr:,} rows are exactly 0 after a step (reading RZ)")
+            e2e["dense_fetch"] = {k: dense[k] for k in ("value", "ms_per_step", "d2h_bytes_per_step", "mode",
+                                                        "serial_ms_per_step")}
+        else:
+            e2e = dense
+            e2e["result"] = "cleora_fetch of all N x d rows"
+        e2e["oom_fallbacks"] = cl.cleora_oom_fallbacks() - oom0
+        del outs, ids, src_h, dst_h, w_h
     clk.stop()
 
     # secondary configs (N = 1): the c2 / c3 SpMM figures beside the headline

@@ -260,6 +260,32 @@ CLEORA_API int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx,
 CLEORA_API int cleora_fetch_async(cleora_graph* g, int64_t row_begin, int64_t row_end, float* out,
                                   int32_t out_on_device);
 
+/*
+ * cleora_fetch_nonzero_async -- the result without its rows that are 0 by construction.  A row of M
+ * without entries has y = 0 in every step (Algorithm 1 line 7: T <- M T), so
+ * after the first step its row of T is exactly 0 (reading RZ).  This call copies only the rows of the
+ * handle's shard [shard_begin, shard_end) (all of [0, N) on one GPU) that have entries in M:
+ *   out_ids[k]  = the k-th such row, ascending (int32);
+ *   out_rows[k] = that row of the current T, d fp32 (row-major, n_rows x d);
+ * every other row of the shard is exactly 0.  Before the first step (T_0) and after cleora_set_rows
+ * (until the next step) every row of the shard is returned (out_ids = shard_begin, shard_begin+1, ...).
+ *   *n_rows (always written, at once): the number of rows returned.  out_rows = out_ids = NULL only
+ *   queries that count.  capacity: rows out_rows / out_ids hold (>= *n_rows, else EUSAGE).  Either
+ *   output may be NULL alone.  out_on_device = 0: host memory (pinned for full PCIe rate); 1: device
+ *   memory on the handle's device.
+ * Enqueued like cleora_fetch_async (the library's copy stream, after the work enqueued so far; rows are
+ * packed on the device in 256 MB slices, each copied out as one DMA); the outputs must stay valid
+ * until cleora_sync(g) or cleora_destroy(g).  The row selection is made once per handle, so a trimmed
+ * handle (cleora_trim) answers only if it was called before the trim.
+ * cleora_fetch_nonzero: the same, and waits for the copy.
+ *   Errors: EUSAGE (NULL g / n_rows, before cleora_init, capacity too small, trimmed before the first
+ *   call), EINTERNAL; a copy failure of the async form is reported by cleora_sync.
+ */
+CLEORA_API int cleora_fetch_nonzero_async(cleora_graph* g, float* out_rows, int32_t* out_ids, int64_t capacity,
+                                          int64_t* n_rows, int32_t out_on_device);
+CLEORA_API int cleora_fetch_nonzero(cleora_graph* g, float* out_rows, int32_t* out_ids, int64_t capacity,
+                                    int64_t* n_rows, int32_t out_on_device);
+
 /* Facts about a handle (all sizes in elements). */
 typedef struct cleora_info_t {
     int64_t n_nodes;        /* N                                                        */

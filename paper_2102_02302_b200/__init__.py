@@ -21,7 +21,7 @@ __all__ = [
     "CleoraError", "Graph", "LIB_PATH",
     "cleora_build", "cleora_init", "cleora_iterate", "cleora_fetch", "cleora_info", "cleora_stats",
     "cleora_sync", "cleora_destroy", "cleora_last_error", "cleora_fetch_csr", "cleora_set_rows", "cleora_fetch_replica",
-    "cleora_fetch_async", "cleora_trim",
+    "cleora_fetch_async", "cleora_trim", "cleora_fetch_nonzero", "cleora_fetch_nonzero_async", "cleora_nonzero_count",
     "cleora_nccl_id_size", "cleora_nccl_get_unique_id", "cleora_plan_shards", "cleora_kernel_launches",
     "cleora_release_cached_memory", "cleora_merge_chunks", "cleora_reconstruct", "cleora_build_batch",
     "cleora_expand", "EXPAND_CLIQUE", "EXPAND_STAR", "cleora_probe_gather", "cleora_ipc_opens", "cleora_oom_fallbacks", "host_allgather_from",
@@ -98,6 +98,8 @@ _SIGS = {
     "cleora_iterate": (ctypes.c_int, [_vp, _i32]),
     "cleora_fetch": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i32]),
     "cleora_fetch_async": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i32]),
+    "cleora_fetch_nonzero_async": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i32]),
+    "cleora_fetch_nonzero": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i32]),
     "cleora_info": (ctypes.c_int, [_vp, ctypes.POINTER(_Info)]),
     "cleora_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_Stats), _i32]),
     "cleora_sync": (ctypes.c_int, [_vp]),
@@ -378,6 +380,48 @@ def cleora_fetch_async(g: Graph, row_begin: int, row_end: int, out):
     _order_after_torch([out], None)
     _check(_lib.cleora_fetch_async(g.handle, int(row_begin), int(row_end), p, 1 if on_dev else 0))
     return out
+
+
+def _fetch_nonzero(fn, g, out_rows, out_ids, sync):
+    n = ctypes.c_int64(0)
+    _check(fn(g.handle, None, None, 0, ctypes.byref(n), 0))
+    rows = n.value
+    if out_rows is None and out_ids is None:
+        d = cleora_info(g, sync=False)["d"]
+        out_rows = np.empty((rows, d), np.float32)
+        out_ids = np.empty(rows, np.int32)
+    pr, dev_r, kr = _ptr(out_rows, np.float32)
+    pi, dev_i, ki = _ptr(out_ids, np.int32)
+    if (out_rows is not None and kr is not out_rows) or (out_ids is not None and ki is not out_ids):
+        raise CleoraError(EUSAGE, "out_rows / out_ids must be contiguous fp32 / int32 arrays")
+    if out_rows is not None and out_ids is not None and dev_r != dev_i:
+        raise CleoraError(EUSAGE, "out_rows and out_ids must both be host or both be device memory")
+    cap = min(len(out_rows) if out_rows is not None else rows, len(out_ids) if out_ids is not None else rows)
+    _order_after_torch([out_rows, out_ids], None)
+    _check(fn(g.handle, pr, pi, int(cap), ctypes.byref(n), 1 if (dev_r or dev_i) else 0))
+    k = n.value
+    return (out_rows[:k] if out_rows is not None else None), (out_ids[:k] if out_ids is not None else None)
+
+
+def cleora_fetch_nonzero(g: Graph, out_rows=None, out_ids=None):
+    """(rows, ids): the rows of this handle's shard with entries in M (ascending ids) and their rows of
+    the current T; every other row is exactly 0 (see include/cleora.h).  Outputs are allocated as numpy
+    arrays when both are None, else written into the given host / CUDA arrays (views of the first n
+    rows are returned)."""
+    return _fetch_nonzero(_lib.cleora_fetch_nonzero, g, out_rows, out_ids, True)
+
+
+def cleora_fetch_nonzero_async(g: Graph, out_rows, out_ids):
+    """Enqueue cleora_fetch_nonzero into preallocated outputs (pinned host or CUDA); returns the views
+    at once.  Keep the outputs alive until cleora_sync(g) or g.close()."""
+    return _fetch_nonzero(_lib.cleora_fetch_nonzero_async, g, out_rows, out_ids, False)
+
+
+def cleora_nonzero_count(g: Graph) -> int:
+    """Rows cleora_fetch_nonzero would return now."""
+    n = ctypes.c_int64(0)
+    _check(_lib.cleora_fetch_nonzero(g.handle, None, None, 0, ctypes.byref(n), 0))
+    return n.value
 
 
 def cleora_info(g: Graph, sync: bool = True) -> dict:

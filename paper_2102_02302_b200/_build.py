@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libcleora.so")
-SOURCES = ["api.cu", "build.cu", "chunks.cu", "expand.cu", "init.cu", "probe.cu", "spmm_norm.cu", "spmm_tma.cu"]
+SOURCES = ["api.cu", "build.cu", "chunks.cu", "expand.cu", "fetch.cu", "init.cu", "probe.cu", "spmm_norm.cu", "spmm_tma.cu"]
 HEADERS = ["common.cuh", "spmm_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

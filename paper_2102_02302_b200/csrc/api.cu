@@ -439,6 +439,14 @@ struct cleora_graph {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_copied = nullptr;
     mutable bool copy_pending = false;
+    // cleora_fetch_nonzero: this shard's rows with entries (or every row: nz_all), selected once per
+    // handle, and the device staging buffer of the packed copy (both freed by free_T after the copy)
+    int32_t* nz_ids = nullptr;
+    int64_t nz_n = -1;
+    bool nz_all = false;
+    float* stage = nullptr;
+    size_t stage_bytes = 0;
+    bool rows_set = false;          // cleora_set_rows since the last step: a row without entries may be != 0
     bool trimmed = false;           // cleora_trim: only T[cur] (and occ, d_scal) left
     int32_t* occ = nullptr;         // chunked builds: endpoint occurrences per node (reading R14)
     int32_t n_graphs = 0;           // batched handles (cleora_build_batch): graphs in the batch
@@ -711,6 +719,12 @@ Status complete_t0(const cleora_graph* gc) {
 void free_T(cleora_graph* g) {
     if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);    // the blocks go back to the cache
     g->copy_pending = false;
+    dfree(g->nz_ids, g->stream);
+    g->nz_ids = nullptr;
+    g->nz_n = -1;
+    dfree(g->stage, g->stream);
+    g->stage = nullptr;
+    g->stage_bytes = 0;
     close_peers(g);
     for (size_t p = 0; p < g->rep.size(); p++)
         if ((int)p != g->rank)
@@ -1120,6 +1134,78 @@ Status do_build(const int32_t* src, const int32_t* dst, const float* w, int64_t 
     // no final synchronisation: the CSR's last kernels run on while the caller goes on to
     // cleora_init (stream order keeps everything that reads them behind them)
     return st;
+}
+
+}  // namespace
+
+namespace {
+
+constexpr size_t kStageBytes = 256ull << 20;    // packed rows per device-to-host slice
+
+Status ensure_copy_stream(cleora_graph* g) {
+    if (g->copy_stream) return Status::ok();
+    CL_CUDA_TRY(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+    CL_CUDA_TRY(cudaEventCreateWithFlags(&g->ev_ready, cudaEventDisableTiming));
+    CL_CUDA_TRY(cudaEventCreateWithFlags(&g->ev_copied, cudaEventDisableTiming));
+    return Status::ok();
+}
+
+Status fetch_nonzero(cleora_graph* g, float* out_rows, int32_t* out_ids, int64_t capacity, int64_t* n_rows,
+                     int32_t out_on_device, bool wait) {
+    // every row while T may hold non-zero rows without entries: T_0 (no step yet) or rows the caller set
+    const bool all = g->iters == 0 || g->rows_set;
+    const int64_t n = all ? g->r1 - g->r0 : (g->r1 - g->r0) - g->own().zero_rows;
+    *n_rows = n;
+    if (!out_rows && !out_ids) return Status::ok();
+    if (capacity < n) return Status::make(2, "cleora_fetch_nonzero: capacity below the row count (query it first)");
+    if (n == 0) return Status::ok();
+    CL_TRY(complete_t0(g));
+    CL_TRY(ensure_copy_stream(g));
+    if (!g->nz_ids || g->nz_all != all) {
+        if (!all && g->trimmed)
+            return Status::make(2, "cleora_fetch_nonzero: the handle was trimmed before its rows were selected "
+                                   "(call cleora_fetch_nonzero_async before cleora_trim)");
+        if (g->nz_ids) {            // the copy stream may still read the previous selection
+            CL_CUDA_TRY(cudaStreamSynchronize(g->copy_stream));
+            dfree(g->nz_ids, g->stream);
+            g->nz_ids = nullptr;
+        }
+        CL_TRY(dalloc((void**)&g->nz_ids, (size_t)n * sizeof(int32_t), g->stream, "nonzero row ids"));
+        CL_TRY(select_rows_with_entries(all ? nullptr : g->own().row_ptr, g->r0, g->r1, all, g->nz_ids, g->stream));
+        g->nz_n = n;
+        g->nz_all = all;
+    }
+    const size_t row_bytes = (size_t)g->d * sizeof(float);
+    const int64_t slice = std::max<int64_t>(1, (int64_t)(kStageBytes / row_bytes));
+    if (out_rows && !out_on_device && !g->stage) {
+        g->stage_bytes = (size_t)std::min<int64_t>(n, slice) * row_bytes;
+        CL_TRY(dalloc((void**)&g->stage, g->stage_bytes, g->stream, "fetch staging"));
+    }
+    // the copy starts when the work enqueued so far on the handle's stream is done
+    order_after_side(g);
+    CL_CUDA_TRY(cudaEventRecord(g->ev_ready, g->stream));
+    CL_CUDA_TRY(cudaStreamWaitEvent(g->copy_stream, g->ev_ready, 0));
+    const float* T = g->T[g->cur];
+    if (out_rows && out_on_device) {
+        CL_TRY(pack_rows(T, g->dp, g->d, g->nz_ids, n, out_rows, g->copy_stream));
+    } else if (out_rows) {
+        // slice k: pack on the SMs, then one linear DMA; the next slice's pack queues behind this copy
+        // on the same stream, so one staging buffer suffices
+        const int64_t per = (int64_t)(g->stage_bytes / row_bytes);
+        for (int64_t k0 = 0; k0 < n; k0 += per) {
+            const int64_t cnt = std::min<int64_t>(per, n - k0);
+            CL_TRY(pack_rows(T, g->dp, g->d, g->nz_ids + k0, cnt, g->stage, g->copy_stream));
+            CL_CUDA_TRY(cudaMemcpyAsync(out_rows + k0 * (int64_t)g->d, g->stage, (size_t)cnt * row_bytes,
+                                        cudaMemcpyDeviceToHost, g->copy_stream));
+        }
+    }
+    if (out_ids)
+        CL_CUDA_TRY(cudaMemcpyAsync(out_ids, g->nz_ids, (size_t)n * sizeof(int32_t),
+                                    out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, g->copy_stream));
+    CL_CUDA_TRY(cudaEventRecord(g->ev_copied, g->copy_stream));
+    g->copy_pending = true;
+    if (wait) CL_CUDA_TRY(cudaStreamSynchronize(g->copy_stream));
+    return Status::ok();
 }
 
 }  // namespace
@@ -1569,6 +1655,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
         g->zclean[out] = true;     // every row of T[out] was written (or was already 0)
         g->cur = out;
         g->iters++;
+        g->rows_set = false;
     }
     return CLEORA_OK;
 }
@@ -1633,6 +1720,26 @@ int cleora_fetch_async(cleora_graph* g, int64_t row_begin, int64_t row_end, floa
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_fetch_async: ") + cudaGetErrorString(e)));
     g->copy_pending = true;
     return CLEORA_OK;
+}
+
+int cleora_fetch_nonzero_async(cleora_graph* g, float* out_rows, int32_t* out_ids, int64_t capacity, int64_t* n_rows,
+                               int32_t out_on_device) {
+    NvtxRange _nvtx("cleora_fetch_nonzero_async");
+    if (!g || !n_rows) return usage("cleora_fetch_nonzero_async: NULL argument");
+    if (!g->T[0]) return usage("cleora_fetch_nonzero_async: call cleora_init first");
+    DeviceGuard guard(g->device);
+    Status st = fetch_nonzero(g, out_rows, out_ids, capacity, n_rows, out_on_device, false);
+    return st.good() ? CLEORA_OK : fail(st);
+}
+
+int cleora_fetch_nonzero(cleora_graph* g, float* out_rows, int32_t* out_ids, int64_t capacity, int64_t* n_rows,
+                         int32_t out_on_device) {
+    NvtxRange _nvtx("cleora_fetch_nonzero");
+    if (!g || !n_rows) return usage("cleora_fetch_nonzero: NULL argument");
+    if (!g->T[0]) return usage("cleora_fetch_nonzero: call cleora_init first");
+    DeviceGuard guard(g->device);
+    Status st = fetch_nonzero(g, out_rows, out_ids, capacity, n_rows, out_on_device, true);
+    return st.good() ? CLEORA_OK : fail(st);
 }
 
 int cleora_merge_chunks(cleora_graph* const* chunks, int32_t n_chunks, float* out, int32_t out_on_device) {
@@ -1857,6 +1964,7 @@ int cleora_set_rows(cleora_graph* g, int64_t row_begin, int64_t row_end, const f
                               (size_t)(row_end - row_begin), cudaMemcpyHostToDevice, g->stream);
     }
     g->zclean[g->cur] = false;
+    g->rows_set = true;
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
     if (e != cudaSuccess) return fail(Status::make(4, std::string("cleora_set_rows: ") + cudaGetErrorString(e)));
     return CLEORA_OK;

@@ -61,6 +61,12 @@ enum { kAllocBase = 1, kAllocTransient = 2 };
 Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, int flags = 0);
 void dfree(void* p, cudaStream_t s);
 
+// fetch.cu: the rows of [r0, r1) with entries in M (all = every row), ascending, into ids[0 .. n);
+// and the packing of T rows ids[0 .. n) into dense rows of d floats (cleora_fetch_nonzero)
+Status select_rows_with_entries(const int64_t* row_ptr, int64_t r0, int64_t r1, bool all, int32_t* ids,
+                                cudaStream_t s);
+Status pack_rows(const float* T, int32_t dp, int32_t d, const int32_t* ids, int64_t n, float* out, cudaStream_t s);
+
 // SplitMix64 output function (the mixer of the T_0 hash, reading R1, and of the chunk
 // assignment, reading R13).
 __host__ __device__ __forceinline__ uint64_t sm64(uint64_t z) {
