@@ -273,9 +273,11 @@ CLEORA_API int cleora_fetch_async(cleora_graph* g, int64_t row_begin, int64_t ro
  *   queries that count.  capacity: rows out_rows / out_ids hold (>= *n_rows, else EUSAGE).  Either
  *   output may be NULL alone.  out_on_device = 0: host memory (pinned for full PCIe rate); 1: device
  *   memory on the handle's device.
- * Enqueued like cleora_fetch_async (the library's copy stream, after the work enqueued so far; rows are
- * packed on the device in 256 MB slices, each copied out as one DMA); the outputs must stay valid
- * until cleora_sync(g) or cleora_destroy(g).  The row selection is made once per handle, so a trimmed
+ * Enqueued like cleora_fetch_async: the rows are packed on the device in the handle's stream order
+ * (into a staging buffer for the whole result, which the handle keeps until cleora_destroy or the
+ * next cleora_init; in 256 MB slices on the copy stream if that buffer cannot be had), then leave on
+ * the library's copy stream; device outputs are packed in the handle's stream order directly.  The
+ * outputs must stay valid until cleora_sync(g) or cleora_destroy(g).  The row selection is made once per handle, so a trimmed
  * handle (cleora_trim) answers only if it was called before the trim.
  * cleora_fetch_nonzero: the same, and waits for the copy.
  *   Errors: EUSAGE (NULL g / n_rows, before cleora_init, capacity too small, trimmed before the first

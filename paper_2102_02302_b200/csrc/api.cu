@@ -1176,22 +1176,56 @@ Status fetch_nonzero(cleora_graph* g, float* out_rows, int32_t* out_ids, int64_t
         g->nz_all = all;
     }
     const size_t row_bytes = (size_t)g->d * sizeof(float);
-    const int64_t slice = std::max<int64_t>(1, (int64_t)(kStageBytes / row_bytes));
-    if (out_rows && !out_on_device && !g->stage) {
-        g->stage_bytes = (size_t)std::min<int64_t>(n, slice) * row_bytes;
-        CL_TRY(dalloc((void**)&g->stage, g->stage_bytes, g->stream, "fetch staging"));
-    }
-    // the copy starts when the work enqueued so far on the handle's stream is done
+    // nothing enqueued from here on may overwrite what an earlier copy of this handle still reads
     order_after_side(g);
-    CL_CUDA_TRY(cudaEventRecord(g->ev_ready, g->stream));
-    CL_CUDA_TRY(cudaStreamWaitEvent(g->copy_stream, g->ev_ready, 0));
     const float* T = g->T[g->cur];
     if (out_rows && out_on_device) {
-        CL_TRY(pack_rows(T, g->dp, g->d, g->nz_ids, n, out_rows, g->copy_stream));
+        // device outputs: packed in stream order, nothing for the copy engine
+        CL_TRY(pack_rows(T, g->dp, g->d, g->nz_ids, n, out_rows, g->stream));
+        if (out_ids)
+            CL_CUDA_TRY(cudaMemcpyAsync(out_ids, g->nz_ids, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                        g->stream));
+        if (wait) CL_CUDA_TRY(cudaStreamSynchronize(g->stream));
+        return Status::ok();
+    }
+    // Host outputs.  The rows are packed on the handle's stream right behind the steps, into one staging
+    // buffer for the whole result when it can be had, and leave in one DMA on the copy stream.  (Packing
+    // slice by slice on the copy stream instead made every slice's pack wait for SMs behind the next
+    // graph's persistent SpMM launch: c4's pipelined e2e 240 ms where the DMA alone needs ~172.)  If the
+    // whole result does not fit beside the handle, 256 MB slices are packed and copied one after another
+    // on the copy stream.
+    const size_t full = (size_t)n * row_bytes;
+    bool whole = false;
+    if (out_rows) {
+        // CLEORA_FETCH_SLICES=1 (read per call): always the sliced path (tests, A/B)
+        const char* fs = getenv("CLEORA_FETCH_SLICES");
+        const bool force_slices = fs && fs[0] == '1';
+        if (!force_slices) {
+            if (g->stage && g->stage_bytes < full) {
+                dfree(g->stage, g->stream);      // ordered after the earlier copy by order_after_side
+                g->stage = nullptr;
+                g->stage_bytes = 0;
+            }
+            if (!g->stage && dalloc((void**)&g->stage, full, g->stream, "fetch staging (whole result)").good())
+                g->stage_bytes = full;
+            whole = g->stage != nullptr;
+        }
+        if (!g->stage) {
+            g->stage_bytes = (size_t)std::min<int64_t>(n, std::max<int64_t>(1, (int64_t)(kStageBytes / row_bytes))) *
+                             row_bytes;
+            CL_TRY(dalloc((void**)&g->stage, g->stage_bytes, g->stream, "fetch staging"));
+        }
+        if (whole) CL_TRY(pack_rows(T, g->dp, g->d, g->nz_ids, n, g->stage, g->stream));
+    }
+    // the copy starts when the work enqueued so far on the handle's stream is done
+    CL_CUDA_TRY(cudaEventRecord(g->ev_ready, g->stream));
+    CL_CUDA_TRY(cudaStreamWaitEvent(g->copy_stream, g->ev_ready, 0));
+    if (out_rows && whole) {
+        CL_CUDA_TRY(cudaMemcpyAsync(out_rows, g->stage, full, cudaMemcpyDeviceToHost, g->copy_stream));
     } else if (out_rows) {
         // slice k: pack on the SMs, then one linear DMA; the next slice's pack queues behind this copy
         // on the same stream, so one staging buffer suffices
-        const int64_t per = (int64_t)(g->stage_bytes / row_bytes);
+        const int64_t per = (int64_t)(std::min(g->stage_bytes, kStageBytes) / row_bytes);
         for (int64_t k0 = 0; k0 < n; k0 += per) {
             const int64_t cnt = std::min<int64_t>(per, n - k0);
             CL_TRY(pack_rows(T, g->dp, g->d, g->nz_ids + k0, cnt, g->stage, g->copy_stream));
@@ -1200,8 +1234,8 @@ Status fetch_nonzero(cleora_graph* g, float* out_rows, int32_t* out_ids, int64_t
         }
     }
     if (out_ids)
-        CL_CUDA_TRY(cudaMemcpyAsync(out_ids, g->nz_ids, (size_t)n * sizeof(int32_t),
-                                    out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, g->copy_stream));
+        CL_CUDA_TRY(cudaMemcpyAsync(out_ids, g->nz_ids, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                    g->copy_stream));
     CL_CUDA_TRY(cudaEventRecord(g->ev_copied, g->copy_stream));
     g->copy_pending = true;
     if (wait) CL_CUDA_TRY(cudaStreamSynchronize(g->copy_stream));

@@ -4,8 +4,8 @@
 // reading RZ; Algorithm 1 line 7), so the rows with entries plus their ids are the
 // whole result.  On the bench graph (c4) 52.6% of the rows have no entries: the device-to-host copy of
 // the result, which bounds the end-to-end step, halves.  The ids are selected once per handle (they
-// depend on M only); the rows are packed slice by slice into a device staging buffer on the copy stream,
-// each slice copied out as one linear DMA.
+// depend on M only); the rows are packed into a device staging buffer in the handle's stream order and
+// copied out as one linear DMA (api.cu fetch_nonzero; 256 MB slices when the whole buffer cannot be had).
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 

@@ -74,11 +74,14 @@ def test_tiny_graphs(cl, seed):
         G.close()
 
 
-def test_directed_sinks_several_slices_async_trim_and_device_outputs(cl):
+@pytest.mark.parametrize("slices", ["0", "1"])
+def test_directed_sinks_several_slices_async_trim_and_device_outputs(cl, slices, monkeypatch):
     """A directed R-MAT graph (most rows are sinks, c4's kind) at d = 1024 whose rows with entries
     exceed one 256 MB staging slice; the async form into pinned memory followed by cleora_trim (the
-    bench's e2e pipeline) and the device-output form give the same bits as the synchronous fetch."""
+    bench's e2e pipeline) and the device-output form give the same bits as the synchronous fetch.
+    slices = "1": the sliced path (CLEORA_FETCH_SLICES=1) instead of one whole-result staging buffer."""
     import torch
+    monkeypatch.setenv("CLEORA_FETCH_SLICES", slices)
     g = gen.rmat_directed(400_000, 19, 1_600_000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=7)
     M = oracle.build_from(g)
     want = _rows_with_entries(M)
