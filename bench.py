@@ -610,7 +610,8 @@ def main():
         # the result as a user fetches it: the rows with entries and their ids (cleora_fetch_nonzero;
         # every other row is exactly 0 after a step, reading RZ), packed into the front of the same
         # pinned buffers; the dense N x d fetch is measured beside it
-        n_nzr = g.n - info["zero_rows"] if world == 1 else None
+        # (P > 1: each rank fetches its own shard's rows with entries; the bytes below are the whole job's)
+        n_nzr = None
         ids = [torch.empty(g.n, dtype=torch.int32).pin_memory() for _ in outs]
 
         def e2e_build():
@@ -671,6 +672,17 @@ def main():
                 pipelined = False
                 cl.cleora_release_cached_memory()
         h2d = g.n_edges * 8 + (g.n_edges * 4 if g.w is not None else 0)
+        if not args.dense_fetch:
+            G = e2e_build()
+            n_rank = cl.cleora_nonzero_count(G)
+            G.close()
+            if world > 1:
+                import torch.distributed as dist
+                t = torch.tensor([n_rank], dtype=torch.int64, device=dev)
+                dist.all_reduce(t)
+                n_nzr = int(t.item())
+            else:
+                n_nzr = n_rank
 
         def measure(compact):
             k2 = k_serial = max(2, min(args.steps, 5))
@@ -701,7 +713,8 @@ def main():
         if n_nzr is not None and not args.dense_fetch:
             e2e = measure(True)
             e2e["result"] = (f"cleora_fetch_nonzero: the {n_nzr:,} rows with entries (d fp32 each) and their "
-                             f"int32 ids; the other {g.n - n_nzr:,} rows are exactly 0 after a step (reading RZ)")
+                             f"int32 ids{', each rank its own shard' if world > 1 else ''}; the other "
+                             f"{g.n - n_nzr:,} rows are exactly 0 after a step (reading RZ)")
             e2e["dense_fetch"] = {k: dense[k] for k in ("value", "ms_per_step", "d2h_bytes_per_step", "mode",
                                                         "serial_ms_per_step")}
         else:
