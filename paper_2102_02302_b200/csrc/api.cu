@@ -274,7 +274,7 @@ Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, int flag
         cudaGetLastError();
         *p = nullptr;
         // out of memory: give cached segments back to the driver, largest first, until it fits
-        if (e == cudaErrorMemoryAllocation && release_largest(dev)) {
+        if (e == cudaErrorMemoryAllocation && !(flags & kAllocNoEvict) && release_largest(dev)) {
             g_oom_fallbacks.fetch_add(1);
             static const bool tr = getenv("CLEORA_TRACE") != nullptr;
             if (tr) fprintf(stderr, "[cleora trace] out of memory for %s (%zu bytes): released a cached segment\n", what, bytes);
@@ -1206,7 +1206,10 @@ Status fetch_nonzero(cleora_graph* g, float* out_rows, int32_t* out_ids, int64_t
                 g->stage = nullptr;
                 g->stage_bytes = 0;
             }
-            if (!g->stage && dalloc((void**)&g->stage, full, g->stream, "fetch staging (whole result)").good())
+            // only from the cache or free memory: evicting cached blocks for it would make the next
+            // graph's build allocate them again (c5's pipeline, where HBM is full); else slices
+            if (!g->stage &&
+                dalloc((void**)&g->stage, full, g->stream, "fetch staging (whole result)", kAllocNoEvict).good())
                 g->stage_bytes = full;
             whole = g->stage != nullptr;
         }

@@ -57,7 +57,8 @@ void count_launches(int64_t n);
 // flags: kAllocBase -- at the base of a cudaMalloc segment (CUDA IPC exports whole allocations);
 // kAllocTransient -- freed before the API call returns (a hint: the cache serves both alike, api.cu;
 // small builds carve such buffers out of one arena, build.cu)
-enum { kAllocBase = 1, kAllocTransient = 2 };
+// kAllocNoEvict -- on out-of-memory fail at once instead of releasing cached segments
+enum { kAllocBase = 1, kAllocTransient = 2, kAllocNoEvict = 4 };
 Status dalloc(void** p, size_t bytes, cudaStream_t s, const char* what, int flags = 0);
 void dfree(void* p, cudaStream_t s);
 
