@@ -421,6 +421,7 @@ struct cleora_graph {
     // buffer's rows (spmm_tma.cu, reading R21)
     double* lazy_buf = nullptr;
     bool env_lazy = true, env_t0_all = false;
+    bool env_drop_ungathered = true;    // lazy steps skip the stores of never-gathered rows (CLEORA_KEEP_UNGATHERED=1: not)
     // T_0 written only for the rows a step can gather (in-degree > 0, g->indeg): the other rows are
     // never read before the first step overwrites them, unless T_0 itself is read -- complete_t0 fills
     // them in then (fetch, trim, merge, reconstruct, set_rows)
@@ -1426,6 +1427,7 @@ int cleora_init(cleora_graph* g, int32_t d, uint64_t seed) {
     g->env_defer = getenv("CLEORA_NO_DEFER") == nullptr;
     g->env_lazy = !(getenv("CLEORA_LAZY") && atoi(getenv("CLEORA_LAZY")) == 0);
     g->env_t0_all = getenv("CLEORA_T0_ALL") && atoi(getenv("CLEORA_T0_ALL")) != 0;
+    g->env_drop_ungathered = !(getenv("CLEORA_KEEP_UNGATHERED") && atoi(getenv("CLEORA_KEEP_UNGATHERED")) != 0);
     if (dp != g->dp || !g->T[0]) {
         free_T(g);
         // N x dp rows, then N fp32 row scales (lazy steps, reading R21: a peer's scales ride in the same
@@ -1654,6 +1656,7 @@ int cleora_iterate(cleora_graph* g, int32_t k) {
             a.scale_off = (int64_t)g->n * g->dp;
             a.ss_half = lazy && i + 1 < k ? g->lazy_buf : nullptr;
             a.lazy_out = 0;
+            a.drop_rows = (a.ss_half && g->env_drop_ungathered) ? g->indeg : nullptr;
             Status s = Status::ok();
             if (lazy && i > 0) {
                 // T_in holds the previous step's rows unnormalised: fold their scales into the weights
@@ -1919,6 +1922,7 @@ int cleora_reconstruct(const cleora_graph* g, const int32_t* new_idx, const int3
         a.lazy_out = 0;
         a.scale_off = 0;
         a.ss_half = nullptr;
+        a.drop_rows = nullptr;
         a.peer_mask = nullptr;
         a.gather_mode = g->gmode;
         a.pass = 0;

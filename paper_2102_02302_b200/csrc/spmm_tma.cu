@@ -176,8 +176,10 @@ __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, f
                                                bool empty) {
     const int dp = FULL ? 128 * V : a.dp;
     if (empty && a.skip_zero_rows) return;           // acc is still all zeros
+    // a lazy step's never-gathered row (a.drop_rows): nothing to store, the call's last step computes it
+    const bool drop = HALF && !empty && a.drop_rows && __ldg(a.drop_rows + row) == 0;
     if (HALF && a.pass == 1) {
-        if (!empty) {
+        if (!empty && !drop) {
             if (a.ss_half) {                         // lazy step: this half's sum of squares for pass 2, and
                 double ss = 0.0;                     // the half itself, unnormalised, to the peers as well
 #pragma unroll
@@ -199,6 +201,11 @@ __device__ __forceinline__ void finalize_row_t(const SpmmArgs& a, int64_t row, f
     if (HALF && a.pass == 2 && a.lazy_out) {
         // lazy step: both halves stay unnormalised in T_out (the first from pass 1), the row scale goes
         // to the row scales -- no read-back and rewrite of the first half (c4: 2 x 4.7 GB per step)
+        if (drop) {                                  // warp-uniform (one row per warp)
+#pragma unroll
+            for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            return;
+        }
         double ss = 0.0;
 #pragma unroll
         for (int v = 0; v < V; v++) ss += sq4(acc[v]);
@@ -364,10 +371,12 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
                 y.x += q.x; y.y += q.y; y.z += q.z; y.w += q.w;
             }
         }
+        // a lazy step's never-gathered row (a.drop_rows): stores skipped, block-uniform
+        const bool drop = a.drop_rows && __ldg(a.drop_rows + it.row) == 0;
         if (it.nparts == 1) {
             float4* outr = reinterpret_cast<float4*>(a.T_out + (int64_t)it.row * a.dp);
             if (a.pass == 1) {
-                if (mine) {
+                if (mine && !drop) {
                     if (a.ss_half) put_out4(a, it.row, t, y);   // lazy step: the peers get the half too
                     else __stcg(outr + t, y);
                 }
@@ -376,8 +385,8 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
                 const double tot = block_sum(sq4(y), scratch);
                 const double inv = inv_norm(tot);
                 if (a.lazy_out) {                     // lazy step: unnormalised, the scale aside
-                    if (mine) put_out4(a, it.row, t, y);
-                    if (t == 0) put_scale(a, it.row, (float)inv);
+                    if (mine && !drop) put_out4(a, it.row, t, y);
+                    if (t == 0 && !drop) put_scale(a, it.row, (float)inv);
                 } else {
                     put_out4(a, it.row, t, scale4(y, inv));
                 }
@@ -407,8 +416,9 @@ __device__ void heavy_item_t(const SpmmArgs& a, int64_t idx, Ring& r, float4* sm
                     const double tot = block_sum(zx * zx + zy * zy + zz * zz + zw * zw, scratch);
                     const double inv = inv_norm(tot);
                     if (a.lazy_out) {                 // lazy step: unnormalised, the scale aside
-                        if (t < nqf) put_out4(a, it.row, t, make_float4((float)zx, (float)zy, (float)zz, (float)zw));
-                        if (t == 0) put_scale(a, it.row, (float)inv);
+                        if (t < nqf && !drop)
+                            put_out4(a, it.row, t, make_float4((float)zx, (float)zy, (float)zz, (float)zw));
+                        if (t == 0 && !drop) put_scale(a, it.row, (float)inv);
                     } else if (t < nqf) {
                         put_out4(a, it.row, t,
                                  make_float4((float)(zx * inv), (float)(zy * inv), (float)(zz * inv), (float)(zw * inv)));

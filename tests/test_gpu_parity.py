@@ -567,6 +567,45 @@ def test_lazy_normalisation_between_steps(cl, heavy, monkeypatch):
 
 
 
+@pytest.mark.parametrize("heavy", ["256", "8"])
+def test_lazy_steps_skip_never_gathered_rows(cl, heavy, monkeypatch):
+    """A lazy step stores nothing for a row with entries that no row gathers (in-degree 0): no later
+    step of the call reads it and the call's last step computes it anew.  Forced on small graphs
+    (CLEORA_HOT_MB tiny makes the in-degree available); the result of every call split is bitwise the
+    one with those rows stored (CLEORA_KEEP_UNGATHERED=1) and within the bars of the oracle: light,
+    single- and multi-part heavy source-only rows (threshold 8), both gather engines."""
+    monkeypatch.setenv("CLEORA_HOT_MB", "0.001")
+    monkeypatch.setenv("CLEORA_HALVES", "1")
+    monkeypatch.setenv("CLEORA_HEAVY_THRESH", heavy)
+    rng = np.random.default_rng(41)
+    n = 6000
+    # node n - 1: a source-only hub (3,000 out-edges, nothing points at it) -- a heavy never-gathered row
+    src = np.concatenate([np.full(3000, n - 1, np.int32), rng.integers(0, n - 1, 20000).astype(np.int32)])
+    dst = np.concatenate([rng.integers(0, n - 1, 3000).astype(np.int32), rng.integers(0, n - 1, 20000).astype(np.int32)])
+    hub = gen.EdgeList("srchub", n, src, dst, rng.lognormal(0, 1, src.size).astype(np.float32), True)
+    graphs = [hub, gen.rmat_directed(8192, 13, 60000, (0.57, 0.19, 0.19), 0.0, 1.0, seed=42)]
+    for g in graphs:
+        M = oracle.build_from(g)
+        ind = np.bincount(M.col, minlength=g.n)
+        assert ((np.diff(M.row_ptr) > 0) & (ind == 0)).any(), "no never-gathered row with entries"
+        R_all = oracle.embed(M, 1024, 5, 4, keep_all=True)
+        for mode in ("async", "bulk"):
+            monkeypatch.setenv("CLEORA_GATHER", mode)
+            for split in ((4,), (2, 2), (3, 1)):
+                outs = []
+                for keep in ("0", "1"):
+                    monkeypatch.setenv("CLEORA_KEEP_UNGATHERED", keep)
+                    G = cl.cleora_build(g.src, g.dst, g.w, g.n, g.directed, device=0)
+                    try:
+                        cl.cleora_init(G, 1024, 5)
+                        for k in split:
+                            cl.cleora_iterate(G, k)
+                        outs.append(cl.cleora_fetch(G))
+                    finally:
+                        G.close()
+                assert outs[0].tobytes() == outs[1].tobytes(), f"{g.name} {mode} {split}: differs from keeping them"
+                compare(outs[0], R_all[4], f"{g.name} {mode} heavy={heavy} {split}")
+
 def test_partial_t0_is_completed_on_every_read(cl, monkeypatch):
     """On graphs whose T exceeds the hot-row budget, cleora_init writes T_0 only for rows a step can
     gather (in-degree > 0) and fills in the others when T_0 itself is read.  Forced here on small
